@@ -1,0 +1,127 @@
+"""CPU oracle executor — restates the reference harness call shape.
+
+Every function cites the reference line it follows.  Test infrastructure
+only (see oracle/__init__.py).
+"""
+
+from __future__ import annotations
+
+import contextlib
+import importlib.util
+import io
+import itertools
+import linecache
+import logging
+import sys
+import types
+
+import torch
+
+FLOAT_RTOL = 1e-6   # runner.py:30
+FLOAT_ATOL = 1e-7   # runner.py:31
+
+_ids = itertools.count()
+
+
+def make_args(spec_args: list[dict], seed: int, dtype: torch.dtype | None = None,
+              shapes: list | None = None) -> list:
+    """runner.py:114-125 `_make_args`: manual_seed, then per arg a value
+    tensor, uniform `rand*(hi-lo)+lo` or `randn`.  `shapes` rescales the
+    manifest shapes to the BASELINE configs; `dtype` casts the
+    fp32 draws (bf16 runs use the same draws, rounded)."""
+    torch.manual_seed(seed)
+    out = []
+    for i, a in enumerate(spec_args):
+        shape = shapes[i] if shapes is not None else a.get("shape")
+        if "value" in a:
+            t = torch.tensor(a["value"])
+        elif a.get("dist") == "uniform":
+            t = torch.rand(shape) * (a["high"] - a["low"]) + a["low"]
+        else:
+            t = torch.randn(shape)
+        if dtype is not None and t.is_floating_point():
+            t = t.to(dtype)
+        out.append(t)
+    return out
+
+
+def load_program(text: str, tag: str = "prog") -> types.ModuleType:
+    """runner.py:105-111 `_load_module`, from source text instead of a path."""
+    name = f"_gm_oracle_{tag}_{next(_ids)}"
+    filename = f"<oracle:{name}>"
+    linecache.cache[filename] = (len(text), None, text.splitlines(True), filename)
+    module = types.ModuleType(name)
+    module.__file__ = filename
+    sys.modules[name] = module
+    exec(compile(text, filename, "exec"), module.__dict__)
+    return module
+
+
+class _LogCapture(logging.Handler):
+    """runner.py:128-135."""
+
+    def __init__(self):
+        super().__init__(level=logging.DEBUG)
+        self.lines: list[str] = []
+
+    def emit(self, record: logging.LogRecord) -> None:
+        self.lines.append(record.getMessage())
+
+
+@contextlib.contextmanager
+def capture_side_effects():
+    """runner.py:138-151: stdout text and root-logger lines around a call."""
+    handler = _LogCapture()
+    root = logging.getLogger()
+    old_level = root.level
+    root.addHandler(handler)
+    root.setLevel(logging.DEBUG)
+    buf = io.StringIO()
+    try:
+        with contextlib.redirect_stdout(buf):
+            yield buf, handler
+    finally:
+        root.removeHandler(handler)
+        root.setLevel(old_level)
+
+
+def call_captured(fn, args):
+    """runner.py:154-157: fn(*clones) with side effects captured; returns
+    (result, stdout lines + log lines)."""
+    with capture_side_effects() as (buf, handler):
+        result = fn(*[a.clone() if isinstance(a, torch.Tensor) else a for a in args])
+    return result, buf.getvalue().splitlines() + handler.lines
+
+
+def diffs(a: torch.Tensor, b: torch.Tensor) -> tuple[float, float]:
+    """runner.py:160-168: max abs / max rel difference in fp64."""
+    if a.shape != b.shape:
+        return float("inf"), float("inf")
+    fa, fb = a.double(), b.double()
+    abs_diff = (fa - fb).abs()
+    denom = fa.abs().clamp_min(1e-12)
+    return (float(abs_diff.max()) if abs_diff.numel() else 0.0,
+            float((abs_diff / denom).max()) if abs_diff.numel() else 0.0)
+
+
+def count_breaks(fn, args) -> int:
+    """runner.py:171-177: graph splits reported by torch._dynamo.explain."""
+    torch._dynamo.reset()
+    explanation = torch._dynamo.explain(fn)(*[a.clone() if isinstance(a, torch.Tensor) else a for a in args])
+    return explanation.graph_break_count
+
+
+def reference_callable(text: str, callable_name: str, dtype: torch.dtype | None = None):
+    """Load a transformed program and return its entry callable on CPU in
+    `dtype` (modules are cast; functions take the cast inputs)."""
+    mod = load_program(text, callable_name)
+    fn = getattr(mod, callable_name)
+    if dtype is not None and isinstance(fn, torch.nn.Module):
+        fn.to(dtype)
+    return fn
+
+
+def run_reference(text: str, callable_name: str, args: list, dtype: torch.dtype | None = None):
+    """The reference's hot path on CPU: (output, side-effect lines)."""
+    fn = reference_callable(text, callable_name, dtype)
+    return call_captured(fn, args)

@@ -1,0 +1,760 @@
+"""Region specialisation and CUDA code generation (sm_100a, via NVRTC).
+
+Given a region DAG (ir.py) and the runtime arguments, `Plan` decides
+
+  * the iteration space S (the common shape of the elementwise outputs and
+    of every reduction operand) and how each input is read (full, periodic,
+    strided broadcast, or scalar);
+  * the passes: a reduction whose operand needs only scalars known before
+    pass p runs in pass p; an elementwise output is stored in the first pass
+    where all its scalars are known.  A predicated block is one reduction
+    pass plus one select pass (transform.py:386-388 then :374-376);
+  * guards: an elementwise node that feeds only one side of a `where` with a
+    uniform (scalar) predicate is evaluated under that predicate, so the
+    untaken arm costs nothing — the reference evaluates both arms eagerly
+    (transform.py:404-412), which is equivalent because arms are pure;
+  * residency: inputs read by more than one pass are staged once in shared
+    memory (bulk copy) and re-read from there.
+
+and `emit()` writes the kernel on top of csrc/gm_region.cuh.
+
+Numerics follow torch's CPU eager kernels (the reference executes the
+transformed program eagerly on CPU, runner.py:154-157), measured in this
+repo's tests: one rounding per operator to the result dtype; Python scalars
+are rounded to the tensor dtype for add/sub/compare/clamp but kept in fp32
+for mul/div; `s / x` is `s * reciprocal(x)`; mean = (float)sum / N rounded
+once; reductions accumulate in fp32 per thread and fp64 across threads.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+from .ir import COMPARE, REDUCE, Graph, Node, Unsupported, infer, is_fusable_dtype, topo
+
+DT_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2, torch.bool: 4}
+DT_SIZE = {torch.float32: 4, torch.bfloat16: 2, torch.float16: 2, torch.bool: 1}
+RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "amax": 1, "amin": 2, "prod": 3, "any": 4,
+          "all": 5}
+
+MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strided", "scalar"
+
+UNROLL = 2
+STATIC_SMEM_RESERVE = 8 * 1024
+
+
+def _round_f(dtype) -> str:
+    """Float-code rounding wrapper for a result dtype."""
+    if dtype == torch.bfloat16:
+        return "gm::rbf"
+    if dtype == torch.float16:
+        return "gm::rh"
+    return ""
+
+
+def _round_d(dtype) -> str:
+    """Double-code rounding to a scalar dtype."""
+    if dtype == torch.float32:
+        return "(double)(float)"
+    if dtype == torch.bfloat16:
+        return "gm::rbf_d"
+    if dtype == torch.float16:
+        return "gm::rh_d"
+    if dtype == torch.bool:
+        return "gm_bool"
+    if dtype in (torch.int64, torch.int32, torch.int16, torch.int8, torch.uint8):
+        return "gm_trunc"
+    return ""  # Python float/int/bool host values: double
+
+
+def _fl(v: float) -> str:
+    """Exact float literal."""
+    f = float(v)
+    if math.isnan(f):
+        return "__int_as_float(0x7fc00000)"
+    if math.isinf(f):
+        return "__int_as_float(0x7f800000)" if f > 0 else "__int_as_float(0xff800000)"
+    return f"{f!r}"
+
+
+@dataclass
+class InputPlan:
+    free_index: int
+    node: Node
+    mode: str
+    dtype: torch.dtype
+    slot: int              # index into P.in
+    resident: bool = False
+    passes: set = field(default_factory=set)
+
+
+class Plan:
+    """One specialisation of a region for concrete argument types/shapes."""
+
+    def __init__(self, graph: Graph, outputs: list[Node], args: list, name: str = "region",
+                 device_info: tuple[int, int] = (148, 232448), allow_cpu: bool = False):
+        self.device_info = device_info
+        self.allow_cpu = allow_cpu
+        self.graph = graph
+        self.outputs = outputs
+        self.name = name
+        infer(graph, args, outputs)
+        self.order = topo(outputs)
+        self._classify(args)
+        self._passes()
+        self._inputs(args)
+        self.source = self._emit()
+        digest = hashlib.sha1(self.source.encode()).hexdigest()[:16]
+        self.kernel = f"gm_region_{digest}"
+        self.source = self.source.replace("GM_KERNEL_NAME", self.kernel)
+
+    # -- classification -----------------------------------------------------
+    def _classify(self, args) -> None:
+        elem_roots = [o for o in self.outputs if o.kind == "elem"]
+        red_nodes = [n for n in self.order if n.op in REDUCE]
+        for n in red_nodes:
+            if n.args[0].kind != "elem":
+                raise Unsupported("reduction of a scalar")
+        shapes = {o.shape for o in elem_roots} | {n.args[0].shape for n in red_nodes}
+        if len(shapes) > 1:
+            raise Unsupported(f"outputs/reductions disagree on shape: {shapes}")
+        self.shape = next(iter(shapes)) if shapes else ()
+        self.n = math.prod(self.shape) if shapes else 0
+        for node in self.order:
+            if node.kind == "elem":
+                if not is_fusable_dtype(node.dtype):
+                    raise Unsupported(f"elementwise dtype {node.dtype}")
+                if torch.broadcast_shapes(node.shape, self.shape) != tuple(self.shape):
+                    raise Unsupported("node does not broadcast to the iteration space")
+            elif node.kind == "dscalar":
+                if node.dtype not in (torch.float32, torch.bfloat16, torch.float16, torch.bool, torch.int64,
+                                      torch.int32):
+                    raise Unsupported(f"scalar dtype {node.dtype}")
+        for o in self.outputs:
+            if o.kind == "host":
+                raise Unsupported("host-only output")
+            if o.kind == "elem" and tuple(o.shape) != tuple(self.shape):
+                raise Unsupported("output shape differs from the iteration space")
+        for node in self.order:
+            if node.op == "free" and node.kind == "elem":
+                t = args[node.value]
+                if t.device.type != "cuda" and not self.allow_cpu:
+                    raise Unsupported("tensor not on a CUDA device")
+
+    # -- passes ---------------------------------------------------------------
+    def _passes(self) -> None:
+        avail: dict[int, int] = {}   # scalar node -> level it becomes known
+        need: dict[int, int] = {}    # elem node -> pass it can run in
+        for node in self.order:
+            if node.kind == "elem":
+                need[node.uid] = max(
+                    [need[a.uid] if a.kind == "elem" else avail[a.uid] for a in node.args] or [0]
+                )
+            elif node.op in REDUCE:
+                avail[node.uid] = need[node.args[0].uid] + 1
+            else:  # host / dscalar
+                avail[node.uid] = max([avail[a.uid] if a.kind != "elem" else 0 for a in node.args] or [0])
+                if any(a.kind == "elem" for a in node.args):
+                    raise Unsupported("scalar computed from an elementwise value without reduction")
+        self.avail, self.need = avail, need
+        self.reductions = [n for n in self.order if n.op in REDUCE]
+        npass = 0
+        for o in self.outputs:
+            if o.kind == "elem" and o.op != "free":
+                npass = max(npass, need[o.uid] + 1)
+        for r in self.reductions:
+            npass = max(npass, avail[r.uid])
+        self.npass = npass
+        self.pass_outputs = {p: [] for p in range(npass)}
+        for j, o in enumerate(self.outputs):
+            if o.kind == "elem" and o.op != "free":
+                self.pass_outputs[need[o.uid]].append((j, o))
+        self.pass_reds = {p: [r for r in self.reductions if need[r.args[0].uid] == p] for p in range(npass)}
+        if len(self.reductions) > nat.MAX_RED:
+            raise Unsupported("too many reductions in one region")
+        # scalar slots
+        self.scalars = [n for n in self.order if n.kind in ("host", "dscalar") and n.op != "const"]
+        self.slot = {n.uid: i for i, n in enumerate(self.scalars)}
+        self.max_level = max([avail[n.uid] for n in self.scalars] or [0])
+
+    # -- inputs ---------------------------------------------------------------
+    def _inputs(self, args) -> None:
+        self.inputs: list[InputPlan] = []
+        self.host_frees: list[Node] = []
+        self.dscalar_frees: list[Node] = []
+        used_passes: dict[int, set] = {}
+        for p in range(self.npass):
+            for node in self._pass_nodes(p):
+                if node.op == "free" and node.kind == "elem":
+                    used_passes.setdefault(node.uid, set()).add(p)
+        for node in self.order:
+            if node.op != "free":
+                continue
+            if node.kind == "host":
+                self.host_frees.append(node)
+            elif node.kind == "dscalar":
+                self.dscalar_frees.append(node)
+        if len(self.host_frees) > nat.MAX_HS:
+            raise Unsupported("too many host scalars")
+        for node in self.order:
+            if node.op == "free" and node.kind in ("elem", "dscalar"):
+                t = args[node.value]
+                if node.kind == "dscalar":
+                    mode = MODE_SCALAR
+                else:
+                    mode = self._mode(t)
+                self.inputs.append(InputPlan(node.value, node, mode, t.dtype, len(self.inputs),
+                                             passes=used_passes.get(node.uid, set())))
+        if len(self.inputs) > nat.MAX_IN:
+            raise Unsupported("too many tensor inputs")
+        elem_out = [o for o in self.outputs if o.kind == "elem" and o.op != "free"]
+        scal_out = [o for o in self.outputs if o.kind == "dscalar"]
+        if len(elem_out) + len(scal_out) > nat.MAX_OUT:
+            raise Unsupported("too many outputs")
+        self.in_by_uid = {ip.node.uid: ip for ip in self.inputs}
+
+    def _mode(self, t: torch.Tensor) -> str:
+        S = tuple(self.shape)
+        if t.numel() == 1:
+            return MODE_SCALAR
+        if tuple(t.shape) == S and t.is_contiguous() and t.data_ptr() % 16 == 0:
+            return MODE_FULL
+        # periodic: contiguous tensor equal to S's trailing dims (leading 1s)
+        shp = list(t.shape)
+        while shp and shp[0] == 1:
+            shp.pop(0)
+        if t.is_contiguous() and shp and tuple(shp) == S[len(S) - len(shp):] and t.data_ptr() % 16 == 0:
+            return MODE_PERIODIC
+        return MODE_STRIDED
+
+    # -- guards -----------------------------------------------------------------
+    def _pass_roots(self, p: int) -> list[Node]:
+        return [o for _, o in self.pass_outputs[p]] + [r.args[0] for r in self.pass_reds[p]]
+
+    def _pass_nodes(self, p: int) -> list[Node]:
+        """Elementwise nodes pass p evaluates (scalars come from s_scal, so
+        the traversal stops at them)."""
+        seen: set[int] = set()
+        order: list[Node] = []
+
+        def visit(n: Node) -> None:
+            if n.uid in seen or n.kind != "elem":
+                return
+            seen.add(n.uid)
+            for a in n.args:
+                visit(a)
+            order.append(n)
+
+        for r in self._pass_roots(p):
+            visit(r)
+        return order
+
+    def _guards(self, p: int) -> dict[int, frozenset]:
+        """DNF guard per elementwise node of pass p: a set of conjunctions of
+        (scalar-node uid, polarity) literals."""
+        TRUE = frozenset()
+        dnf: dict[int, set] = {}
+
+        def add(node: Node, conj: frozenset) -> bool:
+            cur = dnf.setdefault(node.uid, set())
+            if any(d <= conj for d in cur):
+                return False
+            for d in [d for d in cur if conj < d]:
+                cur.discard(d)
+            cur.add(conj)
+            # resolution: X+{c} and X+{!c} -> X
+            changed = True
+            while changed:
+                changed = False
+                for a in list(cur):
+                    for lit in a:
+                        b = (a - {lit}) | {(lit[0], not lit[1])}
+                        if b in cur:
+                            cur.discard(a)
+                            cur.discard(b)
+                            merged = a - {lit}
+                            if not any(d <= merged for d in cur):
+                                cur.add(merged)
+                            changed = True
+                            break
+                    if changed:
+                        break
+            return True
+
+        work = [(r, TRUE) for r in self._pass_roots(p)]
+        while work:
+            node, conj = work.pop()
+            if node.kind != "elem":
+                continue
+            if not add(node, conj):
+                continue
+            if node.op == "where" and node.args[0].kind != "elem":
+                c = node.args[0]
+                work.append((node.args[1], conj | {(c.uid, True)}))
+                work.append((node.args[2], conj | {(c.uid, False)}))
+            else:
+                for a in node.args:
+                    work.append((a, conj))
+        return {uid: frozenset(v) for uid, v in dnf.items()}
+
+    # -- emission ---------------------------------------------------------------
+    def _sv(self, node: Node) -> str:
+        """Scalar value (double expression) of a host/dscalar/const node."""
+        if node.op == "const":
+            v = node.value
+            return "1.0" if v is True else ("0.0" if v is False else _fl(v))
+        return f"s_scal[{self.slot[node.uid]}]"
+
+    def _sf(self, node: Node) -> str:
+        """Scalar value as a float local inside a pass."""
+        if node.op == "const":
+            v = node.value
+            return "1.f" if v is True else ("0.f" if v is False else f"((float){_fl(v)})")
+        return f"sf{node.uid}"
+
+    def _ev(self, node: Node, lane: str, u: int) -> str:
+        if node.kind == "elem":
+            return f"n{node.uid}_{u}[{lane}]"
+        return self._sf(node)
+
+    def _scalar_operand(self, s: Node, op: str, res_dtype, operand_index: int) -> str:
+        """torch CPU treatment of a scalar operand of an elementwise op."""
+        v = self._sf(s)
+        r = _round_f(res_dtype)
+        if op in ("mul",):
+            return v
+        if op == "div":
+            return v  # divisor stays fp32 (x / s == x / float(s)); dividend case handled by caller
+        return f"{r}({v})" if r else v
+
+    def _elem_code(self, node: Node, u: int) -> list[str]:
+        L = "l"
+        dst = f"n{node.uid}_{u}[{L}]"
+        R = _round_f(node.dtype) if node.dtype != torch.bool else ""
+        a = node.args
+        op = node.op
+
+        def ev(x: Node, i: int = 0) -> str:
+            if x.kind == "elem":
+                return self._ev(x, L, u)
+            return self._scalar_operand(x, op, node.dtype, i)
+
+        def wrap(expr: str) -> str:
+            return f"{R}({expr})" if R else expr
+
+        if op == "free":
+            ip = self.in_by_uid[node.uid]
+            dt = DT_CODE[ip.dtype]
+            k = ip.slot
+            if ip.mode == MODE_FULL:
+                return [f"gm::load8<{dt}>(P.in[{k}], sres{k}, e{u}, le{u}, nv{u}, n{node.uid}_{u});"]
+            if ip.mode == MODE_PERIODIC:
+                return [f"gm::load8_periodic<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
+            if ip.mode == MODE_STRIDED:
+                return [f"gm::load8_strided<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
+            return [f"#pragma unroll\nfor (int l = 0; l < GM_VEC; ++l) n{node.uid}_{u}[l] = sin{k};"]
+        body: str
+        if op in ("add", "sub", "mul"):
+            fn = {"add": "gm::add", "sub": "gm::sub", "mul": "gm::mul"}[op]
+            body = wrap(f"{fn}({ev(a[0], 0)}, {ev(a[1], 1)})")
+        elif op == "div":
+            if a[0].kind != "elem" and a[1].kind == "elem":
+                # s / x == s * reciprocal(x), reciprocal rounded to the dtype
+                rr = _round_f(a[1].dtype if a[1].dtype != torch.bool else node.dtype)
+                rec = f"gm::div(1.f, {self._ev(a[1], L, u)})"
+                rec = f"{rr}({rec})" if rr else rec
+                body = wrap(f"gm::mul({rec}, {self._sf(a[0])})")
+            else:
+                body = wrap(f"gm::div({ev(a[0], 0)}, {ev(a[1], 1)})")
+        elif op == "pow":
+            base = ev(a[0], 0)
+            if a[1].op == "const" and a[0].kind == "elem":
+                ex = float(a[1].value)
+                special = {
+                    2.0: f"gm::mul({base}, {base})",
+                    3.0: f"gm::mul(gm::mul({base}, {base}), {base})",
+                    0.5: f"gm::fsqrt({base})",
+                    -0.5: f"gm::div(1.f, gm::fsqrt({base}))",
+                    1.0: f"{base}",
+                    -1.0: f"gm::div(1.f, {base})",
+                    -2.0: f"gm::div(1.f, gm::mul({base}, {base}))",
+                    0.0: "1.f",
+                }
+                body = wrap(special.get(ex, f"powf({base}, {_fl(ex)}f)"))
+            else:
+                body = wrap(f"powf({ev(a[0], 0)}, {ev(a[1], 1)})")
+        elif op in COMPARE:
+            cmpd = torch.result_type(a[0].meta, a[1].meta)
+            rc = _round_f(cmpd)
+
+            def cv(x: Node) -> str:
+                s = self._ev(x, L, u) if x.kind == "elem" else self._sf(x)
+                return f"{rc}({s})" if (rc and x.kind != "elem") else s
+
+            sym = {"gt": ">", "ge": ">=", "lt": "<", "le": "<=", "eq": "==", "ne": "!="}[op]
+            body = f"(({cv(a[0])} {sym} {cv(a[1])}) ? 1.f : 0.f)"
+        elif op in ("maximum", "minimum"):
+            fn = "gm::nmax" if op == "maximum" else "gm::nmin"
+            body = wrap(f"{fn}({ev(a[0], 0)}, {ev(a[1], 1)})")
+        elif op == "logical_and":
+            body = f"((({ev(a[0])}) != 0.f && ({ev(a[1])}) != 0.f) ? 1.f : 0.f)"
+        elif op == "logical_or":
+            body = f"((({ev(a[0])}) != 0.f || ({ev(a[1])}) != 0.f) ? 1.f : 0.f)"
+        elif op == "logical_not":
+            body = f"((({ev(a[0])}) == 0.f) ? 1.f : 0.f)"
+        elif op == "where":
+            if a[0].kind != "elem":
+                return self._uniform_select(node, u)
+            body = wrap(f"(({self._ev(a[0], L, u)}) != 0.f ? {ev(a[1], 1)} : {ev(a[2], 2)})")
+        elif op == "clamp":
+            has_lo, has_hi = node.value
+            x = ev(a[0])
+            i = 1
+            if has_lo:
+                x = f"gm::nmax({x}, {ev(a[i], i)})"
+                i += 1
+            if has_hi:
+                x = f"gm::nmin({x}, {ev(a[i], i)})"
+            body = wrap(x)
+        else:
+            x = ev(a[0])
+            un = {
+                "neg": f"(-{x})", "pos": f"({x})", "abs": f"fabsf({x})", "relu": f"gm::relu({x})",
+                "sigmoid": f"gm::sigmoid({x})", "tanh": f"tanhf({x})", "exp": f"expf({x})",
+                "log": f"logf({x})", "sqrt": f"gm::fsqrt({x})", "rsqrt": f"gm::div(1.f, gm::fsqrt({x}))",
+                "sin": f"sinf({x})", "cos": f"cosf({x})", "silu": f"gm::silu({x})",
+                "square": f"gm::mul({x}, {x})", "reciprocal": f"gm::div(1.f, {x})",
+            }
+            if op not in un:
+                raise Unsupported(f"codegen for {op}")
+            body = wrap(un[op])
+        return [f"#pragma unroll\nfor (int l = 0; l < GM_VEC; ++l) {dst.replace('[l]', '[l]')} = {body};"]
+
+    def _uniform_select(self, node: Node, u: int) -> list[str]:
+        c, ta, ea = node.args
+        R = _round_f(node.dtype) if node.dtype != torch.bool else ""
+
+        def val(x: Node) -> str:
+            if x.kind == "elem":
+                s = f"n{x.uid}_{u}[l]"
+                # promote/round into the result dtype (exact when widening)
+                return f"{R}({s})" if (R and x.dtype != node.dtype) else s
+            s = self._sf(x)
+            return f"{R}({s})" if R else s
+
+        cond = f"sb{c.uid}"
+        return [
+            f"if ({cond}) {{\n#pragma unroll\nfor (int l = 0; l < GM_VEC; ++l) n{node.uid}_{u}[l] = {val(ta)};\n}} "
+            f"else {{\n#pragma unroll\nfor (int l = 0; l < GM_VEC; ++l) n{node.uid}_{u}[l] = {val(ea)};\n}}"
+        ]
+
+    def _guard_expr(self, dnf: frozenset) -> str:
+        if any(len(c) == 0 for c in dnf):
+            return ""
+        terms = []
+        for conj in sorted(dnf, key=lambda c: sorted(c)):
+            lits = [f"sb{uid}" if pol else f"!sb{uid}" for uid, pol in sorted(conj)]
+            terms.append("(" + " && ".join(lits) + ")")
+        return " || ".join(terms)
+
+    def _scalar_code(self, node: Node) -> str:
+        """Double-precision statement computing scalar slot of `node`."""
+        slot = self.slot[node.uid]
+        dst = f"s_scal[{slot}]"
+        if node.op == "free":
+            if node.kind == "host":
+                j = self.host_frees.index(node)
+                return f"{dst} = P.hs[{j}];"
+            ip = self.in_by_uid[node.uid]
+            if ip.dtype == torch.int64:
+                return f"{dst} = (double)(*(const long long*)P.in[{ip.slot}].ptr);"
+            if ip.dtype == torch.int32:
+                return f"{dst} = (double)(*(const int*)P.in[{ip.slot}].ptr);"
+            return f"{dst} = (double)gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);"
+        if node.op in REDUCE:
+            raise AssertionError("reductions are finished by _finish_reduction")
+        R = _round_d(node.dtype) if node.kind == "dscalar" else ""
+        a = node.args
+        op = node.op
+
+        def sv(x: Node) -> str:
+            return self._sv(x)
+
+        if op in COMPARE:
+            cmpd = torch.result_type(a[0].meta, a[1].meta) if any(torch.is_tensor(x.meta) for x in a) else None
+            rc = _round_d(cmpd) if cmpd is not None else ""
+            sym = {"gt": ">", "ge": ">=", "lt": "<", "le": "<=", "eq": "==", "ne": "!="}[op]
+            l0 = f"{rc}({sv(a[0])})" if rc else sv(a[0])
+            l1 = f"{rc}({sv(a[1])})" if rc else sv(a[1])
+            return f"{dst} = (({l0}) {sym} ({l1})) ? 1.0 : 0.0;"
+        if op in ("add", "sub", "mul", "div"):
+            sym = {"add": "+", "sub": "-", "mul": "*", "div": "/"}[op]
+            # operands are first converted to the common dtype
+            if node.kind == "dscalar" and node.dtype in (torch.float32, torch.bfloat16, torch.float16):
+                rcast = _round_d(node.dtype)
+                e = f"({rcast}({sv(a[0])}) {sym} {rcast}({sv(a[1])}))"
+            else:
+                e = f"({sv(a[0])} {sym} {sv(a[1])})"
+            return f"{dst} = {R}({e});" if R else f"{dst} = {e};"
+        if op == "pow":
+            e = f"pow({sv(a[0])}, {sv(a[1])})"
+            return f"{dst} = {R}({e});" if R else f"{dst} = {e};"
+        if op == "where":
+            return f"{dst} = ({sv(a[0])} != 0.0) ? {R}({sv(a[1])}) : {R}({sv(a[2])});" if R else \
+                f"{dst} = ({sv(a[0])} != 0.0) ? {sv(a[1])} : {sv(a[2])};"
+        if op in ("maximum", "minimum"):
+            fn = "gm::dmax" if op == "maximum" else "gm::dmin"
+            return f"{dst} = {R}({fn}({sv(a[0])}, {sv(a[1])}));"
+        if op == "logical_and":
+            return f"{dst} = ({sv(a[0])} != 0.0 && {sv(a[1])} != 0.0) ? 1.0 : 0.0;"
+        if op == "logical_or":
+            return f"{dst} = ({sv(a[0])} != 0.0 || {sv(a[1])} != 0.0) ? 1.0 : 0.0;"
+        if op == "logical_not":
+            return f"{dst} = ({sv(a[0])} == 0.0) ? 1.0 : 0.0;"
+        if op == "clamp":
+            has_lo, has_hi = node.value
+            x = sv(a[0])
+            i = 1
+            if has_lo:
+                x = f"gm::dmax({x}, {sv(a[i])})"
+                i += 1
+            if has_hi:
+                x = f"gm::dmin({x}, {sv(a[i])})"
+            return f"{dst} = {R}({x});" if R else f"{dst} = {x};"
+        x = sv(a[0])
+        un = {
+            "neg": f"(-{x})", "pos": f"({x})", "abs": f"fabs({x})", "relu": f"({x} > 0.0 ? {x} : 0.0)",
+            "sigmoid": f"(double)gm::sigmoid((float){x})", "tanh": f"(double)tanhf((float){x})",
+            "exp": f"(double)expf((float){x})", "log": f"(double)logf((float){x})",
+            "sqrt": f"(double)gm::fsqrt((float){x})", "rsqrt": f"(double)gm::div(1.f, gm::fsqrt((float){x}))",
+            "sin": f"(double)sinf((float){x})", "cos": f"(double)cosf((float){x})",
+            "silu": f"(double)gm::silu((float){x})", "square": f"({x} * {x})",
+            "reciprocal": f"(1.0 / {x})",
+        }
+        if op not in un:
+            raise Unsupported(f"scalar codegen for {op}")
+        return f"{dst} = {R}({un[op]});" if R else f"{dst} = {un[op]};"
+
+    def _finish_reduction(self, r: Node, k: int) -> str:
+        """Scalar slot of reduction `r` from the grid-reduced double s_red[k]."""
+        dst = f"s_scal[{self.slot[r.uid]}]"
+        R = _round_d(r.dtype)
+        x = f"s_red[{k}]"
+        if r.op == "mean":
+            e = f"(double)__fdiv_rn((float){x}, (float){self.n}.0)"
+            return f"{dst} = {R}({e});"
+        if r.op == "norm":
+            return f"{dst} = {R}((double)gm::fsqrt((float){x}));"
+        if r.op in ("any", "all"):
+            return f"{dst} = ({x} != 0.0) ? 1.0 : 0.0;"
+        if r.op == "count_nonzero":
+            return f"{dst} = {x};"
+        return f"{dst} = {R}({x});" if R else f"{dst} = {x};"
+
+    def _emit(self) -> str:
+        out: list[str] = []
+        w = out.append
+        nscal = max(1, len(self.scalars))
+        resident = self._plan_residency_flags()
+        w('#include "gm_region.cuh"')
+        w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
+        w("#define gm_trunc(x) ((double)(long long)(x))")
+        w(f"// region {self.name}: shape {list(self.shape)}, {self.npass} pass(es), "
+          f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s)")
+        w('extern "C" __global__ void __launch_bounds__(GM_THREADS, 1)')
+        w("GM_KERNEL_NAME(const __grid_constant__ gm::Params P) {")
+        w("  using namespace gm;")
+        w("  extern __shared__ __align__(128) unsigned char smem[];")
+        w("  __shared__ u64 s_bars[GM_MAX_PIECES];")
+        w("  __shared__ double s_warp[GM_WARPS * GM_MAX_RED];")
+        w("  __shared__ double s_red[GM_MAX_RED];")
+        w(f"  __shared__ double s_scal[{nscal}];")
+        w("  const i64 v0 = (i64)blockIdx.x * P.vpc;")
+        w("  const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;")
+        w("  (void)v1; (void)s_bars; (void)s_warp; (void)s_red;")
+        any_res = any(resident)
+        w("  Stage st; st.bars = s_bars; st.waited = 0; st.npieces = 0; st.piece_vecs = 1;")
+        if any_res:
+            es = ", ".join(str(DT_SIZE[ip.dtype]) for ip in self.inputs)
+            rs = ", ".join("1" if r else "0" for r in resident)
+            w(f"  const int es_[{len(self.inputs)}] = {{{es}}};")
+            w(f"  const int res_[{len(self.inputs)}] = {{{rs}}};")
+            w(f"  stage_issue(P, smem, {len(self.inputs)}, es_, res_, v0, v1, st);")
+        for ip, r in zip(self.inputs, resident):
+            if ip.mode == MODE_FULL:
+                w(f"  const u32 sres{ip.slot} = {'smem_u32(smem + P.in[%d].smem_off)' % ip.slot if r else '0u'};")
+        # level-0 scalars
+        self._emit_scalar_level(w, 0)
+        red_slot = {r.uid: i for i, r in enumerate(self.reductions)}
+        for p in range(self.npass):
+            elem_nodes = self._pass_nodes(p)
+            reds = self.pass_reds[p]
+            outs = self.pass_outputs[p]
+            if not elem_nodes and not reds and not outs:
+                continue
+            w(f"  {{ // ---- pass {p}")
+            guards = self._guards(p)
+            # uniform locals: scalars used by this pass's elementwise code
+            used_scal = []
+            for n in elem_nodes:
+                for a in n.args:
+                    if a.kind != "elem" and a.op != "const" and a not in used_scal:
+                        used_scal.append(a)
+            for conj_set in guards.values():
+                for conj in conj_set:
+                    for uid, _ in conj:
+                        node = self.graph.nodes[uid]
+                        if node not in used_scal:
+                            used_scal.append(node)
+            for s in used_scal:
+                w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
+                w(f"    const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
+            for ip in self.inputs:
+                if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
+                    w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
+            for k, r in enumerate(reds):
+                w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
+            w(f"    for (i64 vb = v0 + threadIdx.x; vb < v1; vb += {UNROLL} * GM_THREADS) {{")
+            for u in range(UNROLL):
+                w(f"      const i64 vv{u} = vb + {u} * GM_THREADS;")
+                w(f"      const i64 e{u} = vv{u} * GM_VEC;")
+                w(f"      const int nv{u} = vv{u} < v1 ? (int)((P.n - e{u}) < GM_VEC ? (P.n - e{u}) : GM_VEC) : 0;")
+                w(f"      const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
+            if p == 0 and any_res:
+                w(f"      stage_wait(st, ((vb + {UNROLL - 1} * GM_THREADS) < v1 ? (vb + {UNROLL - 1} * GM_THREADS) : (v1 - 1)) - v0);")
+            for u in range(UNROLL):
+                for n in elem_nodes:
+                    w(f"      float n{n.uid}_{u}[GM_VEC];")
+            # loads first (unconditional full/periodic/strided), for all unrolled vectors
+            loads = [n for n in elem_nodes if n.op == "free" and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))]
+            for u in range(UNROLL):
+                w(f"      if (nv{u} > 0) {{")
+                for n in loads:
+                    for line in self._elem_code(n, u):
+                        w("        " + line.replace("\n", "\n        "))
+                w("      }")
+            for u in range(UNROLL):
+                w(f"      if (nv{u} > 0) {{")
+                cur_guard = None
+                open_block = False
+                for n in elem_nodes:
+                    if n in loads:
+                        continue
+                    g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
+                    if g != cur_guard:
+                        if open_block:
+                            w("        }")
+                            open_block = False
+                        if g:
+                            w(f"        if ({g}) {{")
+                            open_block = True
+                        cur_guard = g
+                    for line in self._elem_code(n, u):
+                        w("          " + line.replace("\n", "\n          "))
+                if open_block:
+                    w("        }")
+                for k, r in enumerate(reds):
+                    x = r.args[0]
+                    src = f"n{x.uid}_{u}"
+                    if r.op == "norm":
+                        w(f"        {{ float t_[GM_VEC];\n#pragma unroll\n        for (int l = 0; l < GM_VEC; ++l) t_[l] = gm::mul({src}[l], {src}[l]);\n        acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, t_, nv{u}); }}")
+                    elif r.op == "count_nonzero":
+                        w(f"        {{ float t_[GM_VEC];\n#pragma unroll\n        for (int l = 0; l < GM_VEC; ++l) t_[l] = {src}[l] != 0.f ? 1.f : 0.f;\n        acc{k} = gm::acc8(0, acc{k}, t_, nv{u}); }}")
+                    else:
+                        w(f"        acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, {src}, nv{u});")
+                for j, o in outs:
+                    k = self._out_slot(j)
+                    w(f"        gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
+                w("      }")
+            w("    }")
+            if p == 0 and any_res:
+                w("    stage_finish(st);")
+            if reds:
+                nr = len(reds)
+                w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
+                w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
+                w(f"    const int slots_[{nr}] = {{{', '.join(str(red_slot[r.uid]) for r in reds)}}};")
+                w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red);")
+                w("    if (threadIdx.x == 0) {")
+                for k, r in enumerate(reds):
+                    w("      " + self._finish_reduction(r, k))
+                w("    }")
+                w("    __syncthreads();")
+                self._emit_scalar_level(w, p + 1)
+            w("  }")
+        # scalar outputs and the debug mirror
+        w("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
+        for j, o in enumerate(self.outputs):
+            if o.kind == "dscalar":
+                k = self._out_slot(j)
+                val = self._sv(o)
+                if o.dtype == torch.int64:
+                    w(f"    *(long long*)P.out[{k}].ptr = (long long){val};")
+                elif o.dtype == torch.int32:
+                    w(f"    *(int*)P.out[{k}].ptr = (int){val};")
+                else:
+                    w(f"    gm::store_scalar<{DT_CODE[o.dtype]}>(P.out[{k}], {val});")
+        w("    if (P.scal_out) {")
+        w(f"      for (int i = 0; i < {len(self.scalars)}; ++i) ((double*)P.scal_out)[i] = s_scal[i];")
+        w("    }")
+        w("  }")
+        w("}")
+        return "\n".join(out) + "\n"
+
+    def _emit_scalar_level(self, w, level: int) -> None:
+        nodes = [n for n in self.scalars if self.avail[n.uid] == level and n.op not in REDUCE]
+        if not nodes:
+            if level == 0:
+                w("  __syncthreads();")
+            return
+        w("  if (threadIdx.x == 0) {")
+        for n in nodes:
+            w("    " + self._scalar_code(n))
+        w("  }")
+        w("  __syncthreads();")
+
+    def _out_slot(self, j: int) -> int:
+        k = 0
+        for i, o in enumerate(self.outputs):
+            if o.kind == "elem" and o.op == "free":
+                continue
+            if o.kind == "host":
+                continue
+            if i == j:
+                return k
+            k += 1
+        raise AssertionError(j)
+
+    # -- residency --------------------------------------------------------------
+    def _plan_residency_flags(self) -> list[bool]:
+        """Inputs read by >= 2 passes become resident when the CTA chunks fit
+        in shared memory at one CTA per SM (decided from the shape and the
+        device, so the kernel source is a function of the plan key)."""
+        nvec = -(-self.n // nat.VEC) if self.n else 0
+        sms, smem_optin = self.device_info
+        grid0 = max(1, min(sms, -(-nvec // (nat.THREADS * UNROLL)))) if nvec else 1
+        vpc0 = -(-nvec // grid0) if nvec else 0
+        budget = smem_optin - STATIC_SMEM_RESERVE
+        flags = [False] * len(self.inputs)
+        cands = [ip for ip in self.inputs
+                 if ip.mode == MODE_FULL and len(ip.passes) >= 2 and DT_SIZE[ip.dtype] >= 2
+                 and (self.n * DT_SIZE[ip.dtype]) % 16 == 0]
+        cands.sort(key=lambda ip: (-len(ip.passes), ip.slot))
+        used = 0
+        self.smem_off = {}
+        for ip in cands:
+            nbytes = vpc0 * nat.VEC * DT_SIZE[ip.dtype]
+            nbytes = (nbytes + 127) // 128 * 128
+            if used + nbytes <= budget:
+                self.smem_off[ip.slot] = used
+                used += nbytes
+                flags[ip.slot] = True
+                ip.resident = True
+        self.res_grid, self.res_vpc, self.res_smem = (grid0, vpc0, used) if used else (None, None, 0)
+        self.resident_flags = flags
+        return flags

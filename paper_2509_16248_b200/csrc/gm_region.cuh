@@ -1,0 +1,586 @@
+// gm_region.cuh — hand-written sm_100a device skeleton for fused regions.
+//
+// A "region" is a run of straight-line statements of a GraphMend-transformed
+// forward that the lowering fuses into one kernel: the predicate reductions
+// of predicated blocks (transform.py:386-388 `__gm_pred_k = <T>.<red>() <cmp> c`),
+// the arm expressions (transform.py:395-423) and the `torch.where` selects
+// (transform.py:374-376), plus the elementwise statements around them.
+//
+// Execution model (one launch, persistent CTAs, at most one per SM):
+//   * the iteration space (n elements, row-major) is cut into 8-element
+//     vectors; CTA b owns the contiguous vectors [b*vpc, (b+1)*vpc);
+//   * pass p evaluates the elementwise code that only needs scalars known
+//     before p, accumulates the reductions of pass p and stores the outputs
+//     of pass p; after a pass with reductions every CTA publishes one partial
+//     per reduction, a self-resetting grid barrier runs, and every CTA
+//     combines the partials in the same fixed order (bit-identical scalars in
+//     all CTAs, run-to-run deterministic) — no host readback, no .item();
+//   * inputs read by more than one pass are staged once into shared memory
+//     with cp.async.bulk (bulk-copy engine, mbarrier complete_tx) and stay
+//     resident: 148 SMs x ~200 KB hold a 25 MB activation, so a predicate
+//     input is read from HBM exactly once;
+//   * everything else streams with 128-bit ld.global.nc / st.global.
+// Scalar predicates are CTA-uniform, so untaken arms are skipped by a
+// uniform branch and their inputs are never loaded.
+//
+// Compiled twice: by nvcc into libgm_b200.so (precompiled canonical
+// branch-select, gm_runtime.cu) and by NVRTC under the generated region
+// sources (codegen.py).  It therefore includes no system headers.
+
+#pragma once
+
+namespace gm {
+
+typedef unsigned long long u64;
+typedef long long i64;
+typedef unsigned int u32;
+typedef unsigned short u16;
+typedef unsigned char u8;
+
+#define GM_MAX_IN 8
+#define GM_MAX_OUT 8
+#define GM_MAX_RED 16
+#define GM_MAX_HS 32
+#define GM_MAX_DIMS 6
+#define GM_MAX_PIECES 16
+#define GM_THREADS 512
+#define GM_WARPS (GM_THREADS / 32)
+#define GM_VEC 8
+
+// element type codes (include/gm_b200.h)
+#define GM_DT_F32 0
+#define GM_DT_BF16 1
+#define GM_DT_F16 2
+#define GM_DT_F64 3
+#define GM_DT_BOOL 4
+
+// reduction combine ops
+#define GM_R_SUM 0
+#define GM_R_MAX 1
+#define GM_R_MIN 2
+#define GM_R_PROD 3
+#define GM_R_OR 4
+#define GM_R_AND 5
+
+// Every field is 8 bytes wide so the ctypes mirror (_native.py) has the same
+// layout with no padding rules involved.
+struct InDesc {
+  i64 ptr;                  // device address of element 0
+  i64 smem_off;             // byte offset of this input's resident chunk (-1: stream)
+  i64 ndim;                 // strided mode: number of iteration dims
+  i64 size[GM_MAX_DIMS];    // strided mode: iteration-space sizes, outer..inner
+  i64 stride[GM_MAX_DIMS];  // strided mode: element strides (0 = broadcast)
+};
+
+struct OutDesc {
+  i64 ptr;
+};
+
+struct Params {
+  i64 n;           // numel of the iteration space
+  i64 nvec;        // ceil(n / GM_VEC)
+  i64 vpc;         // vectors per CTA
+  i64 piece_vecs;  // vectors per bulk-copy piece (resident staging)
+  i64 partials;    // double[GM_MAX_RED][gridDim.x]
+  i64 barrier;     // u32[2] = {arrivals, generation}; zeroed once, self-resetting
+  i64 status;      // int: 0 ok, 1 grid-barrier timeout
+  i64 scal_out;    // double[GM_MAX_RED + ...]: scalar slots mirrored by CTA 0 (or 0)
+  double hs[GM_MAX_HS];  // host scalars (Python numbers) as runtime values
+  InDesc in[GM_MAX_IN];
+  OutDesc out[GM_MAX_OUT];
+};
+
+// ---------------------------------------------------------------------------
+// numerics: IEEE single ops without FMA contraction (torch eager runs every
+// operator as its own kernel, so a*b+c rounds twice there too)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ float relu(float a) { return (a != a) ? a : (a > 0.f ? a : 0.f); }
+__device__ __forceinline__ float sigmoid(float a) { return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-a))); }
+__device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
+__device__ __forceinline__ float neg(float a) { return -a; }
+// NaN-propagating max/min (torch.maximum / Tensor.max semantics)
+__device__ __forceinline__ float nmax(float a, float b) { return (a != a) ? a : ((b != b) ? b : (a > b ? a : b)); }
+__device__ __forceinline__ float nmin(float a, float b) { return (a != a) ? a : ((b != b) ? b : (a < b ? a : b)); }
+__device__ __forceinline__ double dmax(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a > b ? a : b)); }
+__device__ __forceinline__ double dmin(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a < b ? a : b)); }
+
+// bf16 / f16 conversions without cuda_bf16.h
+__device__ __forceinline__ float bf2f(u16 h) { return __uint_as_float(((u32)h) << 16); }
+__device__ __forceinline__ u16 f2bf(float f) {
+  u32 u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (u16)((u >> 16) | 0x40u);  // quiet NaN
+  u += 0x7fffu + ((u >> 16) & 1u);                                       // nearest-even
+  return (u16)(u >> 16);
+}
+__device__ __forceinline__ float h2f(u16 h) {
+  float f;
+  asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
+  return f;
+}
+__device__ __forceinline__ u16 f2h(float f) {
+  u16 h;
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f));
+  return h;
+}
+// per-operator rounding to the result's storage type (eager semantics)
+__device__ __forceinline__ float rbf(float f) { return bf2f(f2bf(f)); }
+__device__ __forceinline__ float rh(float f) { return h2f(f2h(f)); }
+__device__ __forceinline__ double rbf_d(double d) { return (double)rbf((float)d); }
+__device__ __forceinline__ double rh_d(double d) { return (double)rh((float)d); }
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  u32 r;
+  asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void ldg16(const void* p, u32& a, u32& b, u32& c, u32& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
+}
+__device__ __forceinline__ void ldg8b(const void* p, u32& a, u32& b) {
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+}
+__device__ __forceinline__ void lds16(u32 s, u32& a, u32& b, u32& c, u32& d) {
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(s));
+}
+__device__ __forceinline__ void lds8b(u32 s, u32& a, u32& b) {
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(s));
+}
+__device__ __forceinline__ void stg16(void* p, u32 a, u32 b, u32 c, u32 d) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void stg8b(void* p, u32 a, u32 b) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ u32 ld_acquire(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(u32* p, u32 v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ u32 atom_add_acq_rel(u32* p, u32 v) {
+  u32 old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 globaltimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// mbarrier + bulk copy (sm_90+; the bulk-copy engine on Blackwell)
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "GM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra GM_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// element access
+// ---------------------------------------------------------------------------
+template <int DT> struct Elem;
+template <> struct Elem<GM_DT_F32> {
+  static constexpr int ES = 4;
+  __device__ static __forceinline__ float ld(const void* p, i64 i) { return ((const float*)p)[i]; }
+  __device__ static __forceinline__ void st(void* p, i64 i, float v) { ((float*)p)[i] = v; }
+  __device__ static __forceinline__ void ldg8(const void* p, float (&x)[8]) {
+    u32 a, b, c, d, e, f, g, h;
+    ldg16(p, a, b, c, d);
+    ldg16((const char*)p + 16, e, f, g, h);
+    x[0] = __uint_as_float(a); x[1] = __uint_as_float(b); x[2] = __uint_as_float(c); x[3] = __uint_as_float(d);
+    x[4] = __uint_as_float(e); x[5] = __uint_as_float(f); x[6] = __uint_as_float(g); x[7] = __uint_as_float(h);
+  }
+  __device__ static __forceinline__ void lds8(u32 s, float (&x)[8]) {
+    u32 a, b, c, d, e, f, g, h;
+    lds16(s, a, b, c, d);
+    lds16(s + 16, e, f, g, h);
+    x[0] = __uint_as_float(a); x[1] = __uint_as_float(b); x[2] = __uint_as_float(c); x[3] = __uint_as_float(d);
+    x[4] = __uint_as_float(e); x[5] = __uint_as_float(f); x[6] = __uint_as_float(g); x[7] = __uint_as_float(h);
+  }
+  __device__ static __forceinline__ float lds1(u32 s) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(s));
+    return v;
+  }
+  __device__ static __forceinline__ void stg8(void* p, const float (&y)[8]) {
+    stg16(p, __float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3]));
+    stg16((char*)p + 16, __float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]),
+          __float_as_uint(y[7]));
+  }
+};
+template <int DT> struct Elem16 {
+  // bf16 / f16: 8 elements = 16 bytes
+  static constexpr int ES = 2;
+  __device__ static __forceinline__ float cv(u16 h) { return DT == GM_DT_BF16 ? bf2f(h) : h2f(h); }
+  __device__ static __forceinline__ u16 rc(float f) { return DT == GM_DT_BF16 ? f2bf(f) : f2h(f); }
+  __device__ static __forceinline__ float ld(const void* p, i64 i) { return cv(((const u16*)p)[i]); }
+  __device__ static __forceinline__ void st(void* p, i64 i, float v) { ((u16*)p)[i] = rc(v); }
+  __device__ static __forceinline__ void unpack(u32 w, float& lo, float& hi) {
+    lo = cv((u16)(w & 0xffffu));
+    hi = cv((u16)(w >> 16));
+  }
+  __device__ static __forceinline__ u32 pack(float lo, float hi) { return (u32)rc(lo) | ((u32)rc(hi) << 16); }
+  __device__ static __forceinline__ void ldg8(const void* p, float (&x)[8]) {
+    u32 a, b, c, d;
+    ldg16(p, a, b, c, d);
+    unpack(a, x[0], x[1]); unpack(b, x[2], x[3]); unpack(c, x[4], x[5]); unpack(d, x[6], x[7]);
+  }
+  __device__ static __forceinline__ void lds8(u32 s, float (&x)[8]) {
+    u32 a, b, c, d;
+    lds16(s, a, b, c, d);
+    unpack(a, x[0], x[1]); unpack(b, x[2], x[3]); unpack(c, x[4], x[5]); unpack(d, x[6], x[7]);
+  }
+  __device__ static __forceinline__ float lds1(u32 s) {
+    u16 v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(s));
+    return cv(v);
+  }
+  __device__ static __forceinline__ void stg8(void* p, const float (&y)[8]) {
+    stg16(p, pack(y[0], y[1]), pack(y[2], y[3]), pack(y[4], y[5]), pack(y[6], y[7]));
+  }
+};
+template <> struct Elem<GM_DT_BF16> : Elem16<GM_DT_BF16> {};
+template <> struct Elem<GM_DT_F16> : Elem16<GM_DT_F16> {};
+template <> struct Elem<GM_DT_BOOL> {
+  static constexpr int ES = 1;
+  __device__ static __forceinline__ float ld(const void* p, i64 i) { return ((const u8*)p)[i] ? 1.f : 0.f; }
+  __device__ static __forceinline__ void st(void* p, i64 i, float v) { ((u8*)p)[i] = (v != 0.f) ? 1 : 0; }
+  __device__ static __forceinline__ void ldg8(const void* p, float (&x)[8]) {
+    u32 a, b;
+    ldg8b(p, a, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[k] = ((a >> (8 * k)) & 0xffu) ? 1.f : 0.f;
+      x[4 + k] = ((b >> (8 * k)) & 0xffu) ? 1.f : 0.f;
+    }
+  }
+  __device__ static __forceinline__ void lds8(u32 s, float (&x)[8]) {
+    u32 a, b;
+    lds8b(s, a, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[k] = ((a >> (8 * k)) & 0xffu) ? 1.f : 0.f;
+      x[4 + k] = ((b >> (8 * k)) & 0xffu) ? 1.f : 0.f;
+    }
+  }
+  __device__ static __forceinline__ float lds1(u32 s) {
+    u16 v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(s));
+    return v ? 1.f : 0.f;
+  }
+  __device__ static __forceinline__ void stg8(void* p, const float (&y)[8]) {
+    u32 a = 0, b = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a |= (y[k] != 0.f ? 1u : 0u) << (8 * k);
+      b |= (y[4 + k] != 0.f ? 1u : 0u) << (8 * k);
+    }
+    stg8b(p, a, b);
+  }
+};
+
+// Full-size contiguous input: vector `e` (first element index, multiple of 8),
+// `nv` valid lanes; `sres` = shared address of the CTA's resident chunk
+// (0 when streaming), `le` = element index local to the chunk.
+template <int DT>
+__device__ __forceinline__ void load8(const InDesc& d, u32 sres, i64 e, i64 le, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  if (nv == GM_VEC) {
+    if (sres)
+      E::lds8(sres + (u32)(le * E::ES), x);
+    else
+      E::ldg8((const char*)d.ptr + e * E::ES, x);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k)
+      x[k] = (k < nv) ? (sres ? E::lds1(sres + (u32)((le + k) * E::ES)) : E::ld((const void*)d.ptr, e + k)) : 0.f;
+  }
+}
+
+// Broadcast / strided input: element offsets decoded from the iteration index.
+template <int DT>
+__device__ __forceinline__ void load8_strided(const InDesc& d, i64 e, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+#pragma unroll
+  for (int k = 0; k < GM_VEC; ++k) {
+    float v = 0.f;
+    if (k < nv) {
+      i64 i = e + k, off = 0;
+      for (int j = (int)d.ndim - 1; j >= 0; --j) {
+        const i64 s = d.size[j];
+        off += (i % s) * d.stride[j];
+        i /= s;
+      }
+      v = E::ld((const void*)d.ptr, off);
+    }
+    x[k] = v;
+  }
+}
+
+// Periodic broadcast along the innermost dims (e.g. a [D] bias over [..., D]):
+// element i reads index i % period; vector loads when the period keeps the
+// 8 lanes contiguous.
+template <int DT>
+__device__ __forceinline__ void load8_periodic(const InDesc& d, i64 e, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  const i64 period = d.size[0];
+  const i64 j = e % period;
+  if (nv == GM_VEC && (period % GM_VEC) == 0) {
+    E::ldg8((const char*)d.ptr + j * E::ES, x);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, (e + k) % period) : 0.f;
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ float load_scalar(const InDesc& d) {
+  return Elem<DT>::ld((const void*)d.ptr, 0);
+}
+
+template <int DT>
+__device__ __forceinline__ void store8(const OutDesc& o, i64 e, int nv, const float (&y)[8]) {
+  typedef Elem<DT> E;
+  if (nv == GM_VEC) {
+    E::stg8((char*)o.ptr + e * E::ES, y);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k)
+      if (k < nv) E::st((void*)o.ptr, e + k, y[k]);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void store_scalar(const OutDesc& o, double v) {
+  Elem<DT>::st((void*)o.ptr, 0, (float)v);
+}
+
+// ---------------------------------------------------------------------------
+// resident staging: the CTA's chunk of every resident input is bulk-copied
+// into shared memory in GM_MAX_PIECES pieces, one mbarrier per piece.
+// `es[k]` = element size of input k, `res[k]` = 1 if resident.
+// ---------------------------------------------------------------------------
+struct Stage {
+  u64* bars;        // [GM_MAX_PIECES] in static smem
+  int npieces;
+  i64 piece_vecs;
+  int waited;       // pieces this thread has already waited for (in order)
+};
+
+__device__ __forceinline__ void stage_issue(const Params& P, unsigned char* smem, int nin, const int* es,
+                                            const int* res, i64 v0, i64 v1, Stage& st) {
+  st.piece_vecs = P.piece_vecs;
+  const i64 nv = v1 - v0;
+  st.npieces = nv > 0 ? (int)((nv + P.piece_vecs - 1) / P.piece_vecs) : 0;
+  st.waited = 0;
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < st.npieces; ++p) mbar_init(&st.bars[p], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const i64 e_end_cta = (v1 * GM_VEC < P.n) ? v1 * GM_VEC : P.n;
+    for (int p = 0; p < st.npieces; ++p) {
+      const i64 pv0 = v0 + (i64)p * P.piece_vecs;
+      const i64 pv1 = (pv0 + P.piece_vecs < v1) ? pv0 + P.piece_vecs : v1;
+      const i64 e0 = pv0 * GM_VEC;
+      const i64 e1 = (pv1 * GM_VEC < e_end_cta) ? pv1 * GM_VEC : e_end_cta;
+      u32 tx = 0;
+      for (int k = 0; k < nin; ++k)
+        if (res[k]) tx += (u32)((e1 - e0) * es[k]);
+      mbar_expect_tx(&st.bars[p], tx);
+      for (int k = 0; k < nin; ++k) {
+        if (!res[k]) continue;
+        const char* src = (const char*)P.in[k].ptr + e0 * es[k];
+        unsigned char* dst = smem + P.in[k].smem_off + (e0 - v0 * GM_VEC) * es[k];
+        bulk_g2s(dst, src, (u32)((e1 - e0) * es[k]), &st.bars[p]);
+      }
+    }
+  }
+}
+
+// Wait (once, in order) for the piece holding local vector `lv`.
+__device__ __forceinline__ void stage_wait(Stage& st, i64 lv) {
+  const int p = (int)(lv / st.piece_vecs);
+  while (st.waited <= p) {
+    mbar_wait(&st.bars[st.waited], 0);
+    ++st.waited;
+  }
+}
+
+// After the first pass every piece is complete; make that visible to all.
+__device__ __forceinline__ void stage_finish(Stage& st) {
+  if (threadIdx.x == 0)
+    while (st.waited < st.npieces) {
+      mbar_wait(&st.bars[st.waited], 0);
+      ++st.waited;
+    }
+  __syncthreads();
+  st.waited = st.npieces;
+}
+
+// ---------------------------------------------------------------------------
+// grid-wide reduction
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double red_identity(int op) {
+  switch (op) {
+    case GM_R_MAX: return -__longlong_as_double(0x7ff0000000000000LL);
+    case GM_R_MIN: return __longlong_as_double(0x7ff0000000000000LL);
+    case GM_R_PROD: return 1.0;
+    case GM_R_AND: return 1.0;
+    default: return 0.0;
+  }
+}
+__device__ __forceinline__ double red_combine(int op, double a, double b) {
+  switch (op) {
+    case GM_R_MAX: return dmax(a, b);
+    case GM_R_MIN: return dmin(a, b);
+    case GM_R_PROD: return a * b;
+    case GM_R_OR: return (a != 0.0 || b != 0.0) ? 1.0 : 0.0;
+    case GM_R_AND: return (a != 0.0 && b != 0.0) ? 1.0 : 0.0;
+    default: return a + b;
+  }
+}
+
+// Self-resetting generation barrier over all CTAs of the launch.  The grid
+// is sized by the host to be co-resident (<= SMs x occupancy); a 2 s
+// globaltimer bound turns a residency violation into status=1, not a hang.
+__device__ __forceinline__ void grid_sync(const Params& P) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32* bar = (u32*)P.barrier;
+    const u32 gen = ld_acquire(bar + 1);
+    const u32 prev = atom_add_acq_rel(bar, 1u);
+    if (prev == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      st_release(bar + 1, gen + 1);
+    } else {
+      const u64 t0 = globaltimer();
+      while (ld_acquire(bar + 1) == gen) {
+        if (globaltimer() - t0 > 2000000000ull) {
+          *(volatile int*)P.status = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Reduce `nr` per-thread values across the grid.  `ops[r]` combine op,
+// `slots[r]` partials slot.  Result lands in s_out[r] in every CTA.
+// Combination order is fixed (warp butterfly -> warps in order -> CTAs in
+// order), so every CTA and every run produces the same bits.
+__device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
+                                            double* vals, double* s_warp, double* s_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = 0; r < nr; ++r) {
+    double v = vals[r];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = red_combine(ops[r], v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
+  }
+  __syncthreads();
+  double* partials = (double*)P.partials;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < nr; ++r) {
+      double acc = s_warp[r];
+      for (int w = 1; w < GM_WARPS; ++w) acc = red_combine(ops[r], acc, s_warp[w * GM_MAX_RED + r]);
+      partials[(i64)slots[r] * gridDim.x + blockIdx.x] = acc;
+    }
+  }
+  if (gridDim.x > 1) grid_sync(P);
+  else __syncthreads();
+  if (warp == 0) {
+    for (int r = 0; r < nr; ++r) {
+      double acc = red_identity(ops[r]);
+      for (u32 b = lane; b < gridDim.x; b += 32)
+        acc = red_combine(ops[r], acc, ld_relaxed_f64(partials + (i64)slots[r] * gridDim.x + b));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc = red_combine(ops[r], acc, __shfl_xor_sync(0xffffffffu, acc, off));
+      if (lane == 0) s_out[r] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// Per-thread float accumulation of one 8-lane vector (masked to nv lanes).
+__device__ __forceinline__ float acc8(int op, float acc, const float (&x)[8], int nv) {
+  float t;
+  if (nv == GM_VEC) {
+    switch (op) {
+      case GM_R_MAX: t = nmax(nmax(nmax(x[0], x[1]), nmax(x[2], x[3])), nmax(nmax(x[4], x[5]), nmax(x[6], x[7]))); return nmax(acc, t);
+      case GM_R_MIN: t = nmin(nmin(nmin(x[0], x[1]), nmin(x[2], x[3])), nmin(nmin(x[4], x[5]), nmin(x[6], x[7]))); return nmin(acc, t);
+      case GM_R_PROD: t = ((x[0] * x[1]) * (x[2] * x[3])) * ((x[4] * x[5]) * (x[6] * x[7])); return acc * t;
+      case GM_R_OR:
+        return (acc != 0.f || x[0] != 0.f || x[1] != 0.f || x[2] != 0.f || x[3] != 0.f || x[4] != 0.f ||
+                x[5] != 0.f || x[6] != 0.f || x[7] != 0.f) ? 1.f : 0.f;
+      case GM_R_AND:
+        return (acc != 0.f && x[0] != 0.f && x[1] != 0.f && x[2] != 0.f && x[3] != 0.f && x[4] != 0.f &&
+                x[5] != 0.f && x[6] != 0.f && x[7] != 0.f) ? 1.f : 0.f;
+      default: t = ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7])); return acc + t;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < GM_VEC; ++k) {
+    if (k >= nv) break;
+    switch (op) {
+      case GM_R_MAX: acc = nmax(acc, x[k]); break;
+      case GM_R_MIN: acc = nmin(acc, x[k]); break;
+      case GM_R_PROD: acc = acc * x[k]; break;
+      case GM_R_OR: acc = (acc != 0.f || x[k] != 0.f) ? 1.f : 0.f; break;
+      case GM_R_AND: acc = (acc != 0.f && x[k] != 0.f) ? 1.f : 0.f; break;
+      default: acc = acc + x[k]; break;
+    }
+  }
+  return acc;
+}
+__device__ __forceinline__ float acc_identity(int op) {
+  switch (op) {
+    case GM_R_MAX: return -__int_as_float(0x7f800000);
+    case GM_R_MIN: return __int_as_float(0x7f800000);
+    case GM_R_PROD: return 1.f;
+    case GM_R_AND: return 1.f;
+    default: return 0.f;
+  }
+}
+
+}  // namespace gm

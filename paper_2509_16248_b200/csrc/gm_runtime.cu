@@ -1,0 +1,516 @@
+// gm_runtime.cu — libgm_b200.so: the C ABI declared in include/gm_b200.h.
+//
+//  * region compiler/loader: NVRTC -> sm_100a cubin -> driver module (libcuda
+//    resolved with dlopen so the library loads on GPU-less hosts);
+//    the generated sources include the hand-written skeleton gm_region.cuh,
+//    which is embedded here as an NVRTC header (gm_region_cuh.inc, produced
+//    by the build from the same file nvcc compiles below);
+//  * gm_branch_select_f32: the canonical predicated block of the corpus
+//    (corpus/phi4_like/original.py:8-11 after transform.py:359-376) as a
+//    precompiled instance of the same skeleton;
+//  * the log ring: pinned, device-mapped host memory, a gather kernel for the
+//    elements torch's repr reads, and a stream-ordered step commit.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <dlfcn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gm_b200.h"
+#include "gm_region.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define GM_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(GM_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define GM_CU(call)                                                         \
+  do {                                                                      \
+    CUresult r_ = (call);                                                   \
+    if (r_ != CUDA_SUCCESS) {                                               \
+      const char* s_ = nullptr;                                             \
+      g_drv.GetErrorString(r_, &s_);                                          \
+      return fail(GM_E_CUDA, "%s: %s", #call, s_ ? s_ : "unknown error"); \
+    }                                                                       \
+  } while (0)
+
+// Driver API entry points, resolved with dlopen so the library loads (and the
+// CPU test-suite can check its exports) on hosts without a GPU driver.
+struct DriverApi {
+  CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*ModuleUnload)(CUmodule) = nullptr;
+  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           CUstream, void**, void**) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  bool loaded = false;
+} g_drv;
+
+int load_driver() {
+  if (g_drv.loaded) return 0;
+  void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return -1;
+#define GM_SYM(field, name) g_drv.field = (decltype(g_drv.field))dlsym(h, name); if (!g_drv.field) return -1;
+  GM_SYM(ModuleLoadData, "cuModuleLoadData");
+  GM_SYM(ModuleGetFunction, "cuModuleGetFunction");
+  GM_SYM(ModuleUnload, "cuModuleUnload");
+  GM_SYM(LaunchKernel, "cuLaunchKernel");
+  GM_SYM(FuncSetAttribute, "cuFuncSetAttribute");
+  GM_SYM(OccupancyMaxActiveBlocksPerMultiprocessor, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+  GM_SYM(CtxGetCurrent, "cuCtxGetCurrent");
+  GM_SYM(GetErrorString, "cuGetErrorString");
+#undef GM_SYM
+  g_drv.loaded = true;
+  return 0;
+}
+
+const char kRegionHeader[] =
+#include "gm_region_cuh.inc"
+    ;
+
+int g_cc_major = 0, g_cc_minor = 0, g_num_sms = 0, g_smem_optin = 0, g_device = -1;
+
+}  // namespace
+
+struct gm_region_s {
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  int smem = 0;
+};
+
+struct gm_logring_s {
+  void* host = nullptr;             // pinned, mapped ring
+  void* dev = nullptr;              // device alias of `host`
+  size_t bytes = 0;
+  unsigned long long* dstep = nullptr;       // device step counter
+  volatile unsigned long long* hcommit = nullptr;  // mapped: committed steps
+  unsigned long long* dcommit = nullptr;     // device alias of hcommit
+};
+
+// ===========================================================================
+// precompiled canonical branch-select (skeleton instance)
+// ===========================================================================
+namespace {
+
+struct BsArgs {
+  int red, cmp;
+  double thr, a1, b1, a2, b2;
+  double* stat_out;
+};
+
+__global__ void __launch_bounds__(GM_THREADS, 1)
+    gm_branch_select_f32_kernel(const __grid_constant__ gm::Params P, const __grid_constant__ BsArgs A) {
+  using namespace gm;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ u64 s_bars[GM_MAX_PIECES];
+  __shared__ double s_warp[GM_WARPS * GM_MAX_RED];
+  __shared__ double s_red[GM_MAX_RED];
+  const i64 v0 = (i64)blockIdx.x * P.vpc;
+  const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;
+  const bool resident = P.in[0].smem_off >= 0;
+  const u32 sres = resident ? smem_u32(smem + P.in[0].smem_off) : 0u;
+  Stage st;
+  st.bars = s_bars;
+  const int es[1] = {4};
+  const int res[1] = {resident ? 1 : 0};
+  if (resident) stage_issue(P, smem, 1, es, res, v0, v1, st);
+  const int op = (A.red == 2) ? GM_R_MAX : (A.red == 3) ? GM_R_MIN : GM_R_SUM;
+  // pass 0: statistic of x
+  float acc = acc_identity(op);
+  for (i64 v = v0 + threadIdx.x; v < v1; v += GM_THREADS) {
+    const i64 e = v * GM_VEC;
+    const int nv = (int)((P.n - e) < GM_VEC ? (P.n - e) : GM_VEC);
+    if (resident) stage_wait(st, v - v0);
+    float x[GM_VEC];
+    load8<GM_DT_F32>(P.in[0], sres, e, e - v0 * GM_VEC, nv, x);
+    if (A.red == 4) {
+#pragma unroll
+      for (int k = 0; k < GM_VEC; ++k) x[k] = x[k] * x[k];
+    }
+    acc = acc8(op, acc, x, nv);
+  }
+  if (resident) stage_finish(st);
+  double vals[1] = {(double)acc};
+  const int ops[1] = {op};
+  const int slots[1] = {0};
+  grid_reduce(P, 1, ops, slots, vals, s_warp, s_red);
+  // statistic in T's dtype (fp32), compared with the threshold cast to fp32
+  const double r = s_red[0];
+  float stat;
+  if (A.red == 1) stat = __fdiv_rn((float)r, (float)P.n);
+  else if (A.red == 4) stat = (float)sqrt(r);
+  else stat = (float)r;
+  const float thr = (float)A.thr;
+  const bool pred = (A.cmp == 0) ? stat > thr : (A.cmp == 1) ? stat >= thr : (A.cmp == 2) ? stat < thr : stat <= thr;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && A.stat_out) {
+    A.stat_out[0] = (double)stat;
+    A.stat_out[1] = pred ? 1.0 : 0.0;
+  }
+  const float sa = pred ? (float)A.a1 : (float)A.a2;
+  const float sb = pred ? (float)A.b1 : (float)A.b2;
+  // pass 1: only the selected arm is evaluated (the predicate is uniform)
+  for (i64 v = v0 + threadIdx.x; v < v1; v += GM_THREADS) {
+    const i64 e = v * GM_VEC;
+    const int nv = (int)((P.n - e) < GM_VEC ? (P.n - e) : GM_VEC);
+    float x[GM_VEC], y[GM_VEC];
+    load8<GM_DT_F32>(P.in[0], sres, e, e - v0 * GM_VEC, nv, x);
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) y[k] = add(mul(x[k], sa), sb);
+    store8<GM_DT_F32>(P.out[0], e, nv, y);
+  }
+}
+
+// ===========================================================================
+// log ring kernels
+// ===========================================================================
+struct GatherArgs {
+  const void* src;
+  void* ring_dev;
+  const unsigned long long* dstep;
+  unsigned long long step_bytes, n_slots, offset;
+  long long total;  // number of gathered elements
+  int dtype, ndim, esize, pad;
+  long long count[GM_MAX_DIMS], head[GM_MAX_DIMS], size[GM_MAX_DIMS], stride[GM_MAX_DIMS];
+};
+
+__global__ void gm_logring_gather_kernel(const __grid_constant__ GatherArgs A) {
+  const unsigned long long step = *A.dstep;
+  char* dst = (char*)A.ring_dev + (step % A.n_slots) * A.step_bytes + A.offset;
+  for (long long t = threadIdx.x; t < A.total; t += blockDim.x) {
+    long long rem = t, off = 0;
+    for (int d = A.ndim - 1; d >= 0; --d) {
+      const long long k = rem % A.count[d];
+      rem /= A.count[d];
+      const long long idx = (k < A.head[d]) ? k : (A.size[d] - A.count[d] + k);
+      off += idx * A.stride[d];
+    }
+    const char* s = (const char*)A.src + off * A.esize;
+    switch (A.esize) {
+      case 1: ((unsigned char*)dst)[t] = *(const unsigned char*)s; break;
+      case 2: ((unsigned short*)dst)[t] = *(const unsigned short*)s; break;
+      case 4: ((unsigned int*)dst)[t] = *(const unsigned int*)s; break;
+      default: ((unsigned long long*)dst)[t] = *(const unsigned long long*)s; break;
+    }
+  }
+}
+
+__global__ void gm_logring_commit_kernel(unsigned long long* dstep, unsigned long long* dcommit) {
+  const unsigned long long s = *dstep + 1;
+  *dstep = s;
+  __threadfence_system();
+  *(volatile unsigned long long*)dcommit = s;
+}
+
+int esize_of(int dtype) {
+  switch (dtype) {
+    case GM_F32: case GM_I32: return 4;
+    case GM_BF16: case GM_F16: return 2;
+    case GM_BOOL: case GM_U8: return 1;
+    default: return 8;
+  }
+}
+
+int ensure_ctx() {
+  CUcontext ctx = nullptr;
+  GM_CU(g_drv.CtxGetCurrent(&ctx));
+  if (!ctx) {
+    GM_CUDA(cudaFree(0));  // binds the primary context of the current device
+  }
+  return GM_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int gm_abi_version(void) { return GM_ABI_VERSION; }
+
+const char* gm_last_error(void) { return g_err.c_str(); }
+
+int gm_init(int device, int* num_sms, int* smem_optin_bytes) {
+  if (device < 0) return fail(GM_E_INVALID, "gm_init: bad device %d", device);
+  GM_CUDA(cudaSetDevice(device));
+  if (load_driver()) return fail(GM_E_CUDA, "gm_init: cannot load libcuda.so.1: %s", dlerror());
+  int r = ensure_ctx();
+  if (r) return r;
+  GM_CUDA(cudaDeviceGetAttribute(&g_cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  GM_CUDA(cudaDeviceGetAttribute(&g_cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  GM_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, device));
+  GM_CUDA(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  g_device = device;
+  if (num_sms) *num_sms = g_num_sms;
+  if (smem_optin_bytes) *smem_optin_bytes = g_smem_optin;
+  return GM_OK;
+}
+
+// NVRTC -> cubin for sm_<major><minor>a.  Exposed separately so the CPU
+// test suite can check generated sources compile without a GPU.
+int gm_region_compile_cubin(const char* cuda_src, int cc_major, int cc_minor, void** cubin, size_t* cubin_bytes,
+                            char* log, size_t log_cap) {
+  if (!cuda_src || !cubin || !cubin_bytes) return fail(GM_E_INVALID, "gm_region_compile_cubin: null argument");
+  nvrtcProgram prog;
+  const char* headers[1] = {kRegionHeader};
+  const char* names[1] = {"gm_region.cuh"};
+  nvrtcResult rc = nvrtcCreateProgram(&prog, cuda_src, "gm_region_gen.cu", 1, headers, names);
+  if (rc != NVRTC_SUCCESS) return fail(GM_E_COMPILE, "nvrtcCreateProgram: %s", nvrtcGetErrorString(rc));
+  char arch[64];
+  snprintf(arch, sizeof(arch), "--gpu-architecture=sm_%d%da", cc_major, cc_minor);
+  const char* opts[] = {arch, "-std=c++17", "-lineinfo", "--fmad=false", "-DGM_NVRTC=1"};
+  rc = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string lg(log_size + 1, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &lg[0]);
+  if (log && log_cap) {
+    strncpy(log, lg.c_str(), log_cap - 1);
+    log[log_cap - 1] = 0;
+  }
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(GM_E_COMPILE, "nvrtc: %s\n%s", nvrtcGetErrorString(rc), lg.c_str());
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  void* buf = malloc(n);
+  if (!buf) {
+    nvrtcDestroyProgram(&prog);
+    return fail(GM_E_NOMEM, "cubin alloc");
+  }
+  nvrtcGetCUBIN(prog, (char*)buf);
+  nvrtcDestroyProgram(&prog);
+  *cubin = buf;
+  *cubin_bytes = n;
+  return GM_OK;
+}
+
+void gm_free(void* p) { free(p); }
+
+int gm_region_compile(const char* cuda_src, const char* kernel_name, gm_region* out, char* log, size_t log_cap) {
+  if (!kernel_name || !out) return fail(GM_E_INVALID, "gm_region_compile: null argument");
+  if (g_device < 0) return fail(GM_E_INVALID, "gm_region_compile: gm_init not called");
+  void* cubin = nullptr;
+  size_t nbytes = 0;
+  int r = gm_region_compile_cubin(cuda_src, g_cc_major, g_cc_minor, &cubin, &nbytes, log, log_cap);
+  if (r) return r;
+  r = ensure_ctx();
+  if (r) {
+    free(cubin);
+    return r;
+  }
+  gm_region_s* reg = new gm_region_s();
+  CUresult cr = g_drv.ModuleLoadData(&reg->mod, cubin);
+  free(cubin);
+  if (cr != CUDA_SUCCESS) {
+    delete reg;
+    const char* s = nullptr;
+    g_drv.GetErrorString(cr, &s);
+    return fail(GM_E_CUDA, "cuModuleLoadData: %s", s ? s : "?");
+  }
+  cr = g_drv.ModuleGetFunction(&reg->fn, reg->mod, kernel_name);
+  if (cr != CUDA_SUCCESS) {
+    g_drv.ModuleUnload(reg->mod);
+    delete reg;
+    return fail(GM_E_CUDA, "cuModuleGetFunction(%s) failed", kernel_name);
+  }
+  *out = reg;
+  return GM_OK;
+}
+
+int gm_region_set_smem(gm_region r, int smem_bytes) {
+  if (!r) return fail(GM_E_INVALID, "gm_region_set_smem: null region");
+  GM_CU(g_drv.FuncSetAttribute(r->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem_bytes));
+  r->smem = smem_bytes;
+  return GM_OK;
+}
+
+int gm_region_occupancy(gm_region r, int threads, int smem_bytes, int* blocks_per_sm) {
+  if (!r || !blocks_per_sm) return fail(GM_E_INVALID, "gm_region_occupancy: null argument");
+  GM_CU(g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, r->fn, threads, (size_t)smem_bytes));
+  return GM_OK;
+}
+
+int gm_region_launch(gm_region r, const void* params, size_t params_bytes, int grid, int threads, int smem_bytes,
+                     void* stream) {
+  if (!r || !params) return fail(GM_E_INVALID, "gm_region_launch: null argument");
+  if (params_bytes != sizeof(gm::Params))
+    return fail(GM_E_INVALID, "gm_region_launch: params %zu bytes, expected %zu", params_bytes, sizeof(gm::Params));
+  if (smem_bytes > r->smem) {
+    int e = gm_region_set_smem(r, smem_bytes);
+    if (e) return e;
+  }
+  void* args[1] = {const_cast<void*>(params)};
+  GM_CU(g_drv.LaunchKernel(r->fn, grid, 1, 1, threads, 1, 1, smem_bytes, (CUstream)stream, args, nullptr));
+  return GM_OK;
+}
+
+int gm_region_release(gm_region r) {
+  if (!r) return GM_OK;
+  if (r->mod) g_drv.ModuleUnload(r->mod);
+  delete r;
+  return GM_OK;
+}
+
+size_t gm_region_params_bytes(void) { return sizeof(gm::Params); }
+
+size_t gm_branch_select_scratch_bytes(void) { return 64 + 8 * 4096; }
+
+int gm_branch_select_f32(const float* x, float* out, int64_t n, int red, int cmp, double thr, double a1, double b1,
+                         double a2, double b2, void* scratch, double* stat_out, void* stream) {
+  if (g_device < 0) return fail(GM_E_INVALID, "gm_branch_select_f32: gm_init not called");
+  if (!x || !out || !scratch || n <= 0) return fail(GM_E_INVALID, "gm_branch_select_f32: bad argument");
+  if (red < 0 || red > 4 || cmp < 0 || cmp > 3) return fail(GM_E_INVALID, "gm_branch_select_f32: bad red/cmp");
+  if (((uintptr_t)x | (uintptr_t)out) & 15) return fail(GM_E_INVALID, "gm_branch_select_f32: pointers must be 16B aligned");
+  gm::Params P;
+  memset(&P, 0, sizeof(P));
+  P.n = n;
+  P.nvec = (n + GM_VEC - 1) / GM_VEC;
+  int grid = (int)((P.nvec + GM_THREADS * 4 - 1) / (GM_THREADS * 4));
+  if (grid > g_num_sms) grid = g_num_sms;
+  if (grid < 1) grid = 1;
+  P.vpc = (P.nvec + grid - 1) / grid;
+  grid = (int)((P.nvec + P.vpc - 1) / P.vpc);
+  const long long chunk_bytes = P.vpc * GM_VEC * 4;
+  int smem = 0;
+  P.in[0].ptr = (long long)(uintptr_t)x;
+  P.in[0].smem_off = -1;
+  if (chunk_bytes <= g_smem_optin - 4096 && (n * 4) % 16 == 0) {
+    P.in[0].smem_off = 0;
+    smem = (int)chunk_bytes;
+    P.piece_vecs = (P.vpc + GM_MAX_PIECES - 1) / GM_MAX_PIECES;
+    if (P.piece_vecs < 64) P.piece_vecs = 64;
+  } else {
+    P.piece_vecs = P.vpc;
+  }
+  P.out[0].ptr = (long long)(uintptr_t)out;
+  char* s = (char*)scratch;
+  P.barrier = (long long)(uintptr_t)s;
+  P.status = (long long)(uintptr_t)(s + 8);
+  P.partials = (long long)(uintptr_t)(s + 64);
+  if ((size_t)grid * 8 > gm_branch_select_scratch_bytes() - 64) return fail(GM_E_INVALID, "grid too large for scratch");
+  BsArgs A;
+  A.red = red;
+  A.cmp = cmp;
+  A.thr = thr;
+  A.a1 = a1;
+  A.b1 = b1;
+  A.a2 = a2;
+  A.b2 = b2;
+  A.stat_out = stat_out;
+  if (smem > 48 * 1024)
+    GM_CUDA(cudaFuncSetAttribute(gm_branch_select_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  gm_branch_select_f32_kernel<<<grid, GM_THREADS, smem, (cudaStream_t)stream>>>(P, A);
+  GM_CUDA(cudaGetLastError());
+  return GM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// log ring
+// ---------------------------------------------------------------------------
+int gm_logring_open(size_t bytes, gm_logring* out) {
+  if (!out || bytes == 0) return fail(GM_E_INVALID, "gm_logring_open: bad argument");
+  gm_logring_s* r = new gm_logring_s();
+  r->bytes = bytes;
+  cudaError_t e = cudaHostAlloc(&r->host, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    delete r;
+    return fail(GM_E_NOMEM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+  }
+  memset(r->host, 0, bytes);
+  GM_CUDA(cudaHostGetDevicePointer(&r->dev, r->host, 0));
+  void* hc = nullptr;
+  GM_CUDA(cudaHostAlloc(&hc, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(hc, 0, 64);
+  r->hcommit = (volatile unsigned long long*)hc;
+  GM_CUDA(cudaHostGetDevicePointer((void**)&r->dcommit, hc, 0));
+  GM_CUDA(cudaMalloc((void**)&r->dstep, 64));
+  GM_CUDA(cudaMemset(r->dstep, 0, 64));
+  GM_CUDA(cudaDeviceSynchronize());
+  *out = r;
+  return GM_OK;
+}
+
+int gm_logring_close(gm_logring r) {
+  if (!r) return GM_OK;
+  cudaDeviceSynchronize();
+  if (r->host) cudaFreeHost(r->host);
+  if (r->hcommit) cudaFreeHost((void*)r->hcommit);
+  if (r->dstep) cudaFree(r->dstep);
+  delete r;
+  return GM_OK;
+}
+
+void* gm_logring_host_ptr(gm_logring r) { return r ? r->host : nullptr; }
+size_t gm_logring_bytes(gm_logring r) { return r ? r->bytes : 0; }
+uint64_t* gm_logring_step_ptr(gm_logring r) { return r ? (uint64_t*)r->dstep : nullptr; }
+uint64_t gm_logring_committed(gm_logring r) { return r ? *r->hcommit : 0; }
+
+int gm_logring_gather(gm_logring r, const void* src, int dtype, int ndim, const int64_t* stride, const int64_t* counts,
+                      const int64_t* index_lists, uint64_t step_bytes, uint64_t n_slots, uint64_t offset,
+                      void* stream) {
+  // index_lists carries, per dim, {head, size}: the gathered index k maps to
+  // k (k < head) or size - count + k (torch's edgeitems summarisation).
+  if (!r || !src || ndim < 0 || ndim > GM_MAX_DIMS || !n_slots)
+    return fail(GM_E_INVALID, "gm_logring_gather: bad argument");
+  GatherArgs A;
+  memset(&A, 0, sizeof(A));
+  A.src = src;
+  A.ring_dev = r->dev;
+  A.dstep = r->dstep;
+  A.step_bytes = step_bytes;
+  A.n_slots = n_slots;
+  A.offset = offset;
+  A.dtype = dtype;
+  A.ndim = ndim;
+  A.esize = esize_of(dtype);
+  long long total = 1;
+  for (int d = 0; d < ndim; ++d) {
+    A.count[d] = counts[d];
+    A.head[d] = index_lists[2 * d];
+    A.size[d] = index_lists[2 * d + 1];
+    A.stride[d] = stride[d];
+    total *= counts[d];
+  }
+  A.total = total;
+  if ((unsigned long long)(total * A.esize) + offset > step_bytes || step_bytes * n_slots > r->bytes)
+    return fail(GM_E_RING_FULL, "gm_logring_gather: record does not fit the ring slot");
+  gm_logring_gather_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(A);
+  GM_CUDA(cudaGetLastError());
+  return GM_OK;
+}
+
+int gm_logring_commit(gm_logring r, void* stream) {
+  if (!r) return fail(GM_E_INVALID, "gm_logring_commit: null ring");
+  gm_logring_commit_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(r->dstep, r->dcommit);
+  GM_CUDA(cudaGetLastError());
+  return GM_OK;
+}
+
+}  // extern "C"

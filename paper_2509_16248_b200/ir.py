@@ -1,0 +1,402 @@
+"""Expression IR for fused regions of a GraphMend-transformed forward.
+
+The transform emits straight-line Python (transform.py:359-444):
+    __gm_pred_k = <cond>                       (transform.py:386-388)
+    __gm_then_T_k = <pure expr> ...            (transform.py:404-412)
+    T = torch.where(__gm_pred_k, then, else)   (transform.py:374-376, :420-422)
+whose arms are restricted by the purity gate to names, constants,
+`+ - * / // % ** @`, unary +/-, comparisons, subscripts, torch.* calls and the
+allowlisted tensor methods (transform.py:225-289, data/pure_ops.cfg), and
+whose predicates are reductions from attr_table.cfg (analysis.py:472-501).
+
+This module parses such statements into a DAG of `Node`s.  Anything outside
+the fusable subset (matmul, calls on modules, subscripts, reductions with a
+`dim`, ...) raises `Unsupported`, and the lowering leaves that statement to
+PyTorch.  Types and shapes are not guessed: `infer()` evaluates the DAG on
+`meta` tensors, so promotion and broadcasting are torch's own.
+"""
+
+from __future__ import annotations
+
+import ast
+import math
+from dataclasses import dataclass, field
+from typing import Any
+
+import torch
+
+
+class Unsupported(Exception):
+    """The expression leaves the fusable subset."""
+
+
+UNARY = {
+    "neg", "pos", "abs", "relu", "sigmoid", "tanh", "exp", "log", "sqrt", "rsqrt", "sin", "cos",
+    "silu", "square", "reciprocal", "logical_not",
+}
+BINARY = {"add", "sub", "mul", "div", "pow", "maximum", "minimum", "gt", "ge", "lt", "le", "eq", "ne",
+          "logical_and", "logical_or"}
+COMPARE = {"gt", "ge", "lt", "le", "eq", "ne"}
+REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_nonzero"}
+
+# torch.<name>(...) / torch.nn.functional.<name>(...) spellings
+_TORCH_FUNCS = {
+    "relu": "relu", "sigmoid": "sigmoid", "tanh": "tanh", "exp": "exp", "log": "log", "sqrt": "sqrt",
+    "rsqrt": "rsqrt", "abs": "abs", "sin": "sin", "cos": "cos", "neg": "neg", "negative": "neg",
+    "square": "square", "reciprocal": "reciprocal", "silu": "silu", "logical_not": "logical_not",
+    "add": "add", "sub": "sub", "subtract": "sub", "mul": "mul", "multiply": "mul", "div": "div",
+    "true_divide": "div", "divide": "div", "pow": "pow", "maximum": "maximum", "minimum": "minimum",
+    "gt": "gt", "greater": "gt", "ge": "ge", "lt": "lt", "less": "lt", "le": "le", "eq": "eq", "ne": "ne",
+    "logical_and": "logical_and", "logical_or": "logical_or", "where": "where", "clamp": "clamp",
+    "clip": "clamp", "sum": "sum", "mean": "mean", "amax": "amax", "amin": "amin", "prod": "prod",
+    "any": "any", "all": "all", "count_nonzero": "count_nonzero", "norm": "norm",
+    "max": "max", "min": "min",
+}
+# Tensor.<name>(...) spellings (pure_ops.cfg plus the attr_table reductions)
+_METHODS = dict(_TORCH_FUNCS)
+_METHODS.update({"clamp_min": "clamp_min", "clamp_max": "clamp_max"})
+
+_BINOP = {ast.Add: "add", ast.Sub: "sub", ast.Mult: "mul", ast.Div: "div", ast.Pow: "pow"}
+_CMPOP = {ast.Gt: "gt", ast.GtE: "ge", ast.Lt: "lt", ast.LtE: "le", ast.Eq: "eq", ast.NotEq: "ne"}
+
+
+@dataclass(eq=False)
+class Node:
+    op: str                      # "free", "const", or an op name above
+    args: tuple = ()
+    value: Any = None            # free: arg index; const: Python value; clamp: (has_lo, has_hi)
+    # filled by infer()
+    kind: str = ""               # "host" | "dscalar" | "elem"
+    dtype: Any = None            # torch dtype (host: python type)
+    shape: tuple = ()
+    meta: Any = None
+    uid: int = -1
+
+    def __repr__(self) -> str:  # pragma: no cover - debugging aid
+        return f"Node#{self.uid}({self.op}, {self.kind}, {self.dtype}, {self.shape})"
+
+
+@dataclass
+class FreeVar:
+    """A value the region reads from the enclosing scope: a Name or an
+    attribute chain rooted at a name not assigned in the region."""
+    text: str
+    node: Node
+
+
+@dataclass
+class Graph:
+    frees: list[FreeVar] = field(default_factory=list)
+    nodes: list[Node] = field(default_factory=list)
+
+    def add(self, node: Node) -> Node:
+        node.uid = len(self.nodes)
+        self.nodes.append(node)
+        return node
+
+
+def attr_chain(expr: ast.expr) -> list[str] | None:
+    parts: list[str] = []
+    cur = expr
+    while isinstance(cur, ast.Attribute):
+        parts.append(cur.attr)
+        cur = cur.value
+    if isinstance(cur, ast.Name):
+        parts.append(cur.id)
+        return parts[::-1]
+    return None
+
+
+class Builder:
+    """AST -> Node for one region.  `env` maps region-assigned names to the
+    node of their current binding (SSA by construction)."""
+
+    def __init__(self, graph: Graph, torch_names: set[str], functional_names: set[str]):
+        self.g = graph
+        self.env: dict[str, Node] = {}
+        self.torch_names = torch_names          # aliases of the torch module
+        self.functional_names = functional_names  # aliases of torch.nn.functional
+        self._free_by_text: dict[str, Node] = {}
+        self._consts: dict[tuple, Node] = {}
+
+    # -- leaves -------------------------------------------------------------
+    def free(self, text: str) -> Node:
+        if text not in self._free_by_text:
+            node = self.g.add(Node("free", value=len(self.g.frees)))
+            self.g.frees.append(FreeVar(text, node))
+            self._free_by_text[text] = node
+        return self._free_by_text[text]
+
+    def const(self, value) -> Node:
+        key = (type(value), value)
+        if key not in self._consts:
+            self._consts[key] = self.g.add(Node("const", value=value))
+        return self._consts[key]
+
+    def op(self, name: str, *args: Node, value=None) -> Node:
+        return self.g.add(Node(name, tuple(args), value=value))
+
+    # -- expressions ------------------------------------------------------------
+    def expr(self, e: ast.expr) -> Node:
+        if isinstance(e, ast.Name):
+            if e.id in self.env:
+                return self.env[e.id]
+            if e.id in self.torch_names or e.id in self.functional_names:
+                raise Unsupported("module used as a value")
+            return self.free(e.id)
+        if isinstance(e, ast.Constant):
+            if isinstance(e.value, bool) or isinstance(e.value, (int, float)):
+                return self.const(e.value)
+            raise Unsupported(f"constant {e.value!r}")
+        if isinstance(e, ast.Attribute):
+            chain = attr_chain(e)
+            if chain is None or chain[0] in self.env or chain[0] in self.torch_names:
+                raise Unsupported("attribute of a region value")
+            return self.free(".".join(chain))
+        if isinstance(e, ast.BinOp):
+            name = _BINOP.get(type(e.op))
+            if name is None:
+                raise Unsupported(f"operator {type(e.op).__name__}")
+            return self.op(name, self.expr(e.left), self.expr(e.right))
+        if isinstance(e, ast.UnaryOp):
+            if isinstance(e.op, ast.USub):
+                return self.op("neg", self.expr(e.operand))
+            if isinstance(e.op, ast.UAdd):
+                return self.op("pos", self.expr(e.operand))
+            raise Unsupported(f"unary {type(e.op).__name__}")
+        if isinstance(e, ast.Compare):
+            if len(e.ops) != 1:
+                raise Unsupported("chained comparison")
+            name = _CMPOP.get(type(e.ops[0]))
+            if name is None:
+                raise Unsupported(f"comparison {type(e.ops[0]).__name__}")
+            return self.op(name, self.expr(e.left), self.expr(e.comparators[0]))
+        if isinstance(e, ast.Call):
+            return self.call(e)
+        raise Unsupported(type(e).__name__)
+
+    def call(self, c: ast.Call) -> Node:
+        func = c.func
+        if not isinstance(func, ast.Attribute):
+            raise Unsupported("call of a plain name")
+        chain = attr_chain(func)
+        is_torch = chain is not None and (
+            (len(chain) == 2 and chain[0] in self.torch_names)
+            or (len(chain) == 2 and chain[0] in self.functional_names)
+            or (len(chain) == 4 and chain[0] in self.torch_names and chain[1:3] == ["nn", "functional"])
+        )
+        if is_torch:
+            name = _TORCH_FUNCS.get(chain[-1])
+            if name is None:
+                raise Unsupported(f"torch.{chain[-1]}")
+            args = [self.expr(a) for a in c.args]
+            return self.apply(name, args, c.keywords, method=False)
+        # method call on an expression (receiver may be a region value or free)
+        name = _METHODS.get(func.attr)
+        if name is None:
+            raise Unsupported(f"method .{func.attr}")
+        recv = self.expr(func.value)
+        args = [recv] + [self.expr(a) for a in c.args]
+        return self.apply(name, args, c.keywords, method=True)
+
+    def apply(self, name: str, args: list[Node], keywords: list[ast.keyword], method: bool) -> Node:
+        kw = {}
+        for k in keywords:
+            if k.arg is None:
+                raise Unsupported("**kwargs")
+            kw[k.arg] = k.value
+        if any(isinstance(a, ast.Starred) for a in args):
+            raise Unsupported("*args")
+        if name in ("max", "min"):
+            if len(args) == 1 and not kw:
+                return self.op("amax" if name == "max" else "amin", args[0])
+            if len(args) == 2 and not kw:
+                return self.op("maximum" if name == "max" else "minimum", args[0], args[1])
+            raise Unsupported(f"{name} with dim")
+        if name in REDUCE:
+            if len(args) != 1 or kw:
+                raise Unsupported(f"{name} with arguments")
+            return self.op(name, args[0])
+        if name in UNARY:
+            if len(args) != 1 or kw:
+                raise Unsupported(f"{name} arguments")
+            return self.op(name, args[0])
+        if name in BINARY:
+            if len(args) != 2 or kw:
+                raise Unsupported(f"{name} arguments")
+            return self.op(name, args[0], args[1])
+        if name == "where":
+            if len(args) != 3 or kw:
+                raise Unsupported("where arguments")
+            return self.op("where", *args)
+        if name in ("clamp", "clamp_min", "clamp_max"):
+            x = args[0]
+            lo = hi = None
+            rest = args[1:]
+            if name == "clamp_min":
+                lo = rest[0] if rest else None
+            elif name == "clamp_max":
+                hi = rest[0] if rest else None
+            else:
+                if len(rest) >= 1:
+                    lo = rest[0]
+                if len(rest) >= 2:
+                    hi = rest[1]
+            for k, v in kw.items():
+                if k == "min":
+                    lo = self.expr(v)
+                elif k == "max":
+                    hi = self.expr(v)
+                else:
+                    raise Unsupported(f"clamp keyword {k}")
+            if lo is None and hi is None:
+                raise Unsupported("clamp without bounds")
+            ops = [x] + [n for n in (lo, hi) if n is not None]
+            return self.op("clamp", *ops, value=(lo is not None, hi is not None))
+        raise Unsupported(name)
+
+
+# ---------------------------------------------------------------------------
+# meta evaluation: torch decides dtypes and shapes
+# ---------------------------------------------------------------------------
+
+def _t(x):
+    return x
+
+
+META_FNS = {
+    "neg": lambda a: -a,
+    "pos": lambda a: +a,
+    "abs": lambda a: a.abs() if torch.is_tensor(a) else abs(a),
+    "relu": lambda a: torch.relu(a),
+    "sigmoid": lambda a: torch.sigmoid(a),
+    "tanh": lambda a: torch.tanh(a),
+    "exp": lambda a: torch.exp(a),
+    "log": lambda a: torch.log(a),
+    "sqrt": lambda a: torch.sqrt(a),
+    "rsqrt": lambda a: torch.rsqrt(a),
+    "sin": lambda a: torch.sin(a),
+    "cos": lambda a: torch.cos(a),
+    "silu": lambda a: torch.nn.functional.silu(a),
+    "square": lambda a: torch.square(a),
+    "reciprocal": lambda a: torch.reciprocal(a),
+    "logical_not": lambda a: torch.logical_not(a),
+    "add": lambda a, b: a + b,
+    "sub": lambda a, b: a - b,
+    "mul": lambda a, b: a * b,
+    "div": lambda a, b: a / b,
+    "pow": lambda a, b: a ** b,
+    "maximum": lambda a, b: torch.maximum(a, b),
+    "minimum": lambda a, b: torch.minimum(a, b),
+    "gt": lambda a, b: a > b,
+    "ge": lambda a, b: a >= b,
+    "lt": lambda a, b: a < b,
+    "le": lambda a, b: a <= b,
+    "eq": lambda a, b: a == b,
+    "ne": lambda a, b: a != b,
+    "logical_and": lambda a, b: torch.logical_and(a, b),
+    "logical_or": lambda a, b: torch.logical_or(a, b),
+    "where": lambda c, a, b: torch.where(c, a, b),
+    "sum": lambda a: a.sum(),
+    "mean": lambda a: a.mean(),
+    "amax": lambda a: a.max(),
+    "amin": lambda a: a.min(),
+    "norm": lambda a: a.norm(),
+    "prod": lambda a: a.prod(),
+    "any": lambda a: a.any(),
+    "all": lambda a: a.all(),
+    "count_nonzero": lambda a: torch.count_nonzero(a),
+}
+
+
+def _meta_clamp(node: Node, vals):
+    has_lo, has_hi = node.value
+    x = vals[0]
+    i = 1
+    lo = hi = None
+    if has_lo:
+        lo = vals[i]
+        i += 1
+    if has_hi:
+        hi = vals[i]
+    return torch.clamp(x, min=lo, max=hi)
+
+
+def _as_meta(v):
+    if torch.is_tensor(v):
+        return torch.empty_strided(v.shape, v.stride(), dtype=v.dtype, device="meta")
+    return v
+
+
+def infer(graph: Graph, args: list, needed: list[Node]) -> None:
+    """Evaluate the nodes `needed` depends on with meta tensors; set kind,
+    dtype and shape.  Raises Unsupported on anything torch rejects."""
+    order = topo(needed)
+    for node in order:
+        if node.op == "free":
+            v = _as_meta(args[node.value])
+            if not (torch.is_tensor(v) or isinstance(v, (bool, int, float))):
+                raise Unsupported(f"free value of type {type(v).__name__}")
+        elif node.op == "const":
+            v = node.value
+        else:
+            vals = [a.meta for a in node.args]
+            try:
+                if node.op == "clamp":
+                    v = _meta_clamp(node, vals)
+                else:
+                    if all(not torch.is_tensor(x) for x in vals) and node.op not in (
+                        "add", "sub", "mul", "div", "pow", "neg", "pos", "abs", "gt", "ge", "lt", "le", "eq", "ne",
+                    ):
+                        # torch functions on Python numbers: compute on a 0-d tensor
+                        raise Unsupported(f"{node.op} of host scalars")
+                    v = META_FNS[node.op](*vals)
+            except Unsupported:
+                raise
+            except Exception as exc:  # torch rejected the combination
+                raise Unsupported(f"{node.op}: {exc}") from exc
+        node.meta = v
+        if torch.is_tensor(v):
+            node.kind = "dscalar" if v.dim() == 0 else "elem"
+            node.dtype = v.dtype
+            node.shape = tuple(v.shape)
+        elif isinstance(v, (bool, int, float)):
+            node.kind = "host"
+            node.dtype = type(v)
+            node.shape = ()
+        else:
+            raise Unsupported(f"value of type {type(v).__name__}")
+
+
+def topo(roots: list[Node]) -> list[Node]:
+    seen: set[int] = set()
+    order: list[Node] = []
+    stack = [(r, False) for r in reversed(roots)]
+    while stack:
+        node, done = stack.pop()
+        if done:
+            order.append(node)
+            continue
+        if id(node) in seen:
+            continue
+        seen.add(id(node))
+        stack.append((node, True))
+        for a in reversed(node.args):
+            if id(a) not in seen:
+                stack.append((a, False))
+    return order
+
+
+def is_fusable_dtype(dt) -> bool:
+    return dt in (torch.float32, torch.bfloat16, torch.float16, torch.bool)
+
+
+def host_value_repr(v) -> str:
+    if isinstance(v, bool):
+        return "1.0" if v else "0.0"
+    f = float(v)
+    if math.isnan(f):
+        return "(0.0/0.0)"
+    if math.isinf(f):
+        return "(1.0/0.0)" if f > 0 else "(-1.0/0.0)"
+    return repr(f)

@@ -1,0 +1,331 @@
+"""I/O-deferral runtime: device log ring + host drain.
+
+The reference defers `print` / `logger.*` by capturing the argument tuple at
+the call site and replaying `callee(*__gm_defer_k)` before each return
+(transform.py:744-771, :675-734).  Executed on a GPU, that replay still
+formats CUDA tensors inside the forward — a device-to-host read per tensor.
+
+Here a replay inside an active step
+  * keeps host constants as they are (the tuple holds them by reference);
+  * for each CUDA tensor argument launches one gather kernel that copies
+    exactly the elements torch's repr reads (get_summarized_data: edgeitems
+    3 per dim when numel > threshold 1000, torch/_tensor_str.py) into a slot
+    of a pinned, device-mapped host ring (gm_logring_gather);
+  * records (callee, argument template) in the step's call list.
+At the end of the step a commit kernel publishes the step number to mapped
+host memory.  A host thread (or `flush()`) waits for the commit — it never
+synchronises the stream — rebuilds CPU tensors whose repr is identical to
+the original's, and calls the original callee in source order, so level
+checks happen at drain time exactly as if the call ran late.
+
+Outside a step (a plain call of the lowered function) replay is immediate,
+which is the reference's behaviour.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+import time
+from collections import deque
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+
+EDGEITEMS = 3      # torch._tensor_str.PRINT_OPTS defaults
+THRESHOLD = 1000
+
+_DT = {
+    torch.float32: (nat.GM_F32, 4), torch.bfloat16: (nat.GM_BF16, 2), torch.float16: (nat.GM_F16, 2),
+    torch.float64: (nat.GM_F64, 8), torch.bool: (nat.GM_BOOL, 1), torch.int32: (nat.GM_I32, 4),
+    torch.int64: (nat.GM_I64, 8), torch.uint8: (nat.GM_U8, 1),
+}
+
+
+def summary_plan(shape: tuple[int, ...]) -> tuple[list[int], list[int]]:
+    """(count, head) per dim of the elements torch's repr reads."""
+    numel = math.prod(shape)
+    summarize = numel > THRESHOLD
+    counts, heads = [], []
+    for s in shape:
+        if summarize and s > 2 * EDGEITEMS:
+            counts.append(2 * EDGEITEMS)
+            heads.append(EDGEITEMS)
+        else:
+            counts.append(s)
+            heads.append(s)
+    return counts, heads
+
+
+@dataclass
+class TensorRef:
+    offset: int
+    dtype: torch.dtype
+    shape: tuple
+    counts: list
+    heads: list
+    grad_fn: str | None
+    requires_grad: bool
+
+
+@dataclass
+class StepTemplate:
+    calls: list = field(default_factory=list)   # (site, callee, [arg | TensorRef])
+    discard: bool = False
+
+
+class _TensorText:
+    """str()/repr() of a tensor that carried a grad_fn (or requires_grad) in
+    the forward; the reconstructed CPU tensor has neither, so the suffix is
+    added the way torch._tensor_str._str_intern does."""
+
+    def __init__(self, t: torch.Tensor, grad_fn: str | None, requires_grad: bool):
+        self.t = t
+        self.grad_fn = grad_fn
+        self.requires_grad = requires_grad
+
+    def __repr__(self) -> str:
+        from torch import _tensor_str as ts
+
+        with torch.no_grad():
+            prefix = "tensor("
+            indent = len(prefix)
+            suffixes = []
+            t = self.t
+            default = t.dtype in (torch.get_default_dtype(), torch.int64, torch.bool)
+            if t.numel() == 0:
+                body = "[]"
+                if t.dim() != 1:
+                    suffixes.append("size=" + str(tuple(t.shape)))
+                if t.dtype != torch.get_default_dtype():
+                    suffixes.append("dtype=" + str(t.dtype))
+            else:
+                if not default:
+                    suffixes.append("dtype=" + str(t.dtype))
+                body = ts._tensor_str(t, indent)
+            if self.grad_fn is not None:
+                suffixes.append(f"grad_fn=<{self.grad_fn}>")
+            elif self.requires_grad:
+                suffixes.append("requires_grad=True")
+            return ts._add_suffixes(prefix + body, suffixes, indent, force_newline=False)
+
+    __str__ = __repr__
+
+    def __format__(self, spec):
+        return format(str(self), spec)
+
+
+class LogRing:
+    """Pinned, device-mapped ring for one device."""
+
+    def __init__(self, device: torch.device, slot_bytes: int = 1 << 20, n_slots: int = 64):
+        self.device = device
+        self.slot_bytes = slot_bytes
+        self.n_slots = n_slots
+        nat.init(device.index)
+        h = ctypes.c_void_p()
+        nat.check(nat.lib().gm_logring_open(slot_bytes * n_slots, ctypes.byref(h)), "gm_logring_open")
+        self.handle = h
+        self.host = nat.lib().gm_logring_host_ptr(h)
+        self.lock = threading.RLock()
+        self.pending: deque = deque()        # (step_number, template)
+        self.launched = 0                    # steps committed by launches (device counter target)
+        self.drained = 0
+        self._active: StepTemplate | None = None
+        self._cursor = 0
+        self.gathers = 0
+        self._thread = None
+        self._stop = False
+
+    # -- producer side (forward) ------------------------------------------------
+    def begin(self, discard: bool = False) -> None:
+        if self._active is not None:
+            raise RuntimeError("log ring step already active")
+        self._active = StepTemplate(discard=discard)
+        self._cursor = 0
+
+    def record(self, site: int, callee, args: tuple) -> None:
+        tmpl = self._active
+        out = []
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        for a in args:
+            if torch.is_tensor(a) and a.device.type == "cuda":
+                if a.dtype not in _DT:
+                    raise TypeError(f"log ring: unsupported dtype {a.dtype}")
+                code, es = _DT[a.dtype]
+                shape = tuple(a.shape)
+                counts, heads = summary_plan(shape)
+                nbytes = math.prod(counts) * es
+                off = (self._cursor + 15) // 16 * 16
+                if off + nbytes > self.slot_bytes:
+                    raise nat.NativeError("log ring slot overflow: raise slot_bytes")
+                self._cursor = off + nbytes
+                nd = len(shape)
+                st = (ctypes.c_int64 * max(1, nd))(*a.stride())
+                ct = (ctypes.c_int64 * max(1, nd))(*counts)
+                hl = (ctypes.c_int64 * max(2, 2 * nd))(*[v for h, s in zip(heads, shape) for v in (h, s)])
+                nat.check(
+                    nat.lib().gm_logring_gather(self.handle, ctypes.c_void_p(a.data_ptr()), code, nd, st, ct, hl,
+                                                self.slot_bytes, self.n_slots, off, ctypes.c_void_p(stream)),
+                    "gm_logring_gather",
+                )
+                self.gathers += 1
+                gf = a.grad_fn
+                out.append(TensorRef(off, a.dtype, shape, counts, heads,
+                                     type(gf).__name__ if gf is not None else None, a.requires_grad))
+            elif torch.is_tensor(a):
+                out.append(a.detach().clone() if not a.requires_grad else a)
+            else:
+                out.append(a)
+        tmpl.calls.append((site, callee, out))
+
+    def end(self) -> StepTemplate:
+        tmpl = self._active
+        self._active = None
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        nat.check(nat.lib().gm_logring_commit(self.handle, ctypes.c_void_p(stream)), "gm_logring_commit")
+        return tmpl
+
+    @property
+    def active(self) -> bool:
+        return self._active is not None
+
+    def enqueue(self, tmpl: StepTemplate) -> None:
+        """Register one launched step (eager or graph replay) in order."""
+        with self.lock:
+            # back-pressure: never run more than n_slots-1 steps ahead of the drain
+            while self.launched - self.drained >= self.n_slots - 1:
+                self._drain_one(block=True)
+            self.launched += 1
+            self.pending.append((self.launched, tmpl))
+
+    # -- consumer side (host) -------------------------------------------------------
+    def committed(self) -> int:
+        return int(nat.lib().gm_logring_committed(self.handle))
+
+    def _rebuild(self, ref: TensorRef, slot: int):
+        code, es = _DT[ref.dtype]
+        n = math.prod(ref.counts)
+        addr = self.host + slot * self.slot_bytes + ref.offset
+        raw = (ctypes.c_uint8 * (n * es)).from_address(addr)
+        block = torch.frombuffer(bytearray(raw), dtype=ref.dtype).reshape(ref.counts) if n else \
+            torch.empty(ref.counts, dtype=ref.dtype)
+        if list(ref.counts) == list(ref.shape):
+            full = block.clone()
+        else:
+            full = torch.empty(ref.shape, dtype=ref.dtype)
+            idx = []
+            nd = len(ref.shape)
+            for d, (c, h, s) in enumerate(zip(ref.counts, ref.heads, ref.shape)):
+                ix = torch.tensor([k if k < h else s - c + k for k in range(c)], dtype=torch.long)
+                view = [1] * nd
+                view[d] = c
+                idx.append(ix.view(view))
+            full[tuple(idx)] = block
+        if ref.grad_fn is not None or ref.requires_grad:
+            return _TensorText(full, ref.grad_fn, ref.requires_grad)
+        return full
+
+    def _drain_one(self, block: bool) -> bool:
+        with self.lock:
+            if not self.pending:
+                return False
+            step, tmpl = self.pending[0]
+            while self.committed() < step:
+                if not block:
+                    return False
+                time.sleep(20e-6)
+            self.pending.popleft()
+            slot = (step - 1) % self.n_slots
+            if not tmpl.discard:
+                for _site, callee, args in tmpl.calls:
+                    real = [self._rebuild(a, slot) if isinstance(a, TensorRef) else a for a in args]
+                    callee(*real)
+            self.drained = step
+            return True
+
+    def flush(self) -> None:
+        """Drain every launched step (waits for their commits, in order)."""
+        while self._drain_one(block=True):
+            pass
+
+    def start_drain_thread(self) -> None:
+        if self._thread is not None:
+            return
+
+        def loop():
+            while not self._stop:
+                if not self._drain_one(block=False):
+                    time.sleep(100e-6)
+
+        self._thread = threading.Thread(target=loop, name="gm-logring-drain", daemon=True)
+        self._thread.start()
+
+    def close(self) -> None:
+        self._stop = True
+        if self._thread is not None:
+            self._thread.join(timeout=1.0)
+        try:
+            self.flush()
+        finally:
+            nat.lib().gm_logring_close(self.handle)
+            self.handle = None
+
+
+_rings: dict[int, LogRing] = {}
+_rings_lock = threading.Lock()
+
+
+def ring_for(device: torch.device) -> LogRing:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    with _rings_lock:
+        if idx not in _rings:
+            _rings[idx] = LogRing(torch.device("cuda", idx))
+        return _rings[idx]
+
+
+_tls = threading.local()
+
+
+def active_ring() -> LogRing | None:
+    return getattr(_tls, "ring", None)
+
+
+class step:
+    """Context manager: one forward as one log-ring step on `device`."""
+
+    def __init__(self, device: torch.device, discard: bool = False):
+        self.ring = ring_for(device)
+        self.discard = discard
+        self.template: StepTemplate | None = None
+
+    def __enter__(self):
+        self.ring.begin(self.discard)
+        _tls.ring = self.ring
+        return self
+
+    def __exit__(self, *exc):
+        _tls.ring = None
+        self.template = self.ring.end()
+        return False
+
+
+class ModuleRuntime:
+    """`__gm_rt` of a lowered module: its fused regions and replay sites."""
+
+    def __init__(self, lowered):
+        self.lowered = lowered
+        self.regions = lowered.regions
+        self.sites = lowered.sites
+        self.immediate_replays = 0
+
+    def replay(self, site: int, callee, captured: tuple) -> None:
+        ring = active_ring()
+        if ring is None:
+            self.immediate_replays += 1
+            callee(*captured)
+            return
+        ring.record(site, callee, captured)

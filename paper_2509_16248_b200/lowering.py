@@ -1,0 +1,353 @@
+"""Source-level lowering of a GraphMend-transformed program for B200.
+
+Input: the text `fix_file` returns (transform.py:822-936) — the reference
+transform API is unchanged and is not re-implemented here.  Output: the same
+program where
+
+  * every maximal run of fusable straight-line assignments (predicate
+    bindings `__gm_pred_k = ...`, arm temporaries `__gm_then_T_k` /
+    `__gm_else_T_k`, the `T = torch.where(...)` selects, return hoists
+    `__gm_ret_k = ...` and ordinary elementwise statements around them)
+    becomes ONE call of a fused region (region.py): the predicate reduction,
+    the selected arm and the select run in one sm_100a kernel and only the
+    names read later are materialised;
+  * every deferred replay `callee(*__gm_defer_k)` (transform.py:707-708,
+    :729-731) becomes `__gm_rt.replay(site, callee, __gm_defer_k)`, which
+    hands tensor arguments to the device log ring (logring.py) instead of
+    formatting (and synchronising on) them inside the forward;
+  * capture tuples `__gm_defer_k = (...)` whose elements do not depend on the
+    current region are hoisted above it, so deferral sites do not split
+    regions (the tuple holds references, transform.py:748-753).
+
+Statements outside the fusable subset are left untouched and run as
+PyTorch ops on the device (cuBLAS for Linear/matmul, per `north_star`).
+"""
+
+from __future__ import annotations
+
+import ast
+import copy
+import itertools
+import linecache
+import types
+from dataclasses import dataclass, field
+
+from .ir import Builder, Graph, Unsupported, attr_chain
+from .region import Region
+
+GM_RT = "__gm_rt__"  # dunder suffix: exempt from private-name mangling in class bodies
+_module_ids = itertools.count()
+
+
+@dataclass
+class ReplaySite:
+    site: int
+    callee_src: str
+    capture_name: str
+    function: str
+    lineno: int
+
+
+@dataclass
+class Lowered:
+    original: str
+    source: str
+    regions: list[Region] = field(default_factory=list)
+    sites: list[ReplaySite] = field(default_factory=list)
+    region_sources: list[str] = field(default_factory=list)
+
+
+def _torch_aliases(tree: ast.Module) -> tuple[set[str], set[str]]:
+    torch_names: set[str] = set()
+    functional: set[str] = set()
+    for node in ast.walk(tree):
+        if isinstance(node, ast.Import):
+            for a in node.names:
+                if a.name == "torch":
+                    torch_names.add(a.asname or "torch")
+                elif a.name == "torch.nn.functional" and a.asname:
+                    functional.add(a.asname)
+                elif a.name.startswith("torch.") and not a.asname:
+                    torch_names.add("torch")
+        elif isinstance(node, ast.ImportFrom) and node.module in ("torch.nn", "torch.nn.functional"):
+            for a in node.names:
+                if node.module == "torch.nn" and a.name == "functional":
+                    functional.add(a.asname or "functional")
+    return torch_names or {"torch"}, functional
+
+
+def _is_capture(stmt: ast.stmt) -> str | None:
+    if (
+        isinstance(stmt, ast.Assign)
+        and len(stmt.targets) == 1
+        and isinstance(stmt.targets[0], ast.Name)
+        and stmt.targets[0].id.startswith("__gm_defer_")
+        and isinstance(stmt.value, ast.Tuple)
+    ):
+        return stmt.targets[0].id
+    return None
+
+
+def _is_replay(stmt: ast.stmt) -> tuple[ast.expr, str] | None:
+    if not (isinstance(stmt, ast.Expr) and isinstance(stmt.value, ast.Call)):
+        return None
+    call = stmt.value
+    if call.keywords or len(call.args) != 1 or not isinstance(call.args[0], ast.Starred):
+        return None
+    inner = call.args[0].value
+    if isinstance(inner, ast.Name) and inner.id.startswith("__gm_defer_"):
+        return call.func, inner.id
+    return None
+
+
+def _names_read(node: ast.AST) -> set[str]:
+    return {n.id for n in ast.walk(node) if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Load)}
+
+
+class _FunctionLowerer:
+    def __init__(self, owner: "_Lowerer", fn: ast.FunctionDef):
+        self.owner = owner
+        self.fn = fn
+        # every Name load of the function with its position (for liveness)
+        self.loads: list[tuple[tuple[int, int], str]] = [
+            ((n.lineno, n.col_offset), n.id)
+            for n in ast.walk(fn)
+            if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Load)
+        ]
+
+    def read_after(self, name: str, pos: tuple[int, int]) -> bool:
+        return any(p > pos and n == name for p, n in self.loads)
+
+    # -- region formation -------------------------------------------------------
+    def _build(self, stmts: list[ast.stmt]) -> tuple[Graph, Builder]:
+        g = Graph()
+        b = Builder(g, self.owner.torch_names, self.owner.functional_names)
+        for s in stmts:
+            node = b.expr(s.value)
+            b.env[s.targets[0].id] = node
+        return g, b
+
+    def _eligible(self, stmt: ast.stmt) -> bool:
+        return (
+            isinstance(stmt, ast.Assign)
+            and len(stmt.targets) == 1
+            and isinstance(stmt.targets[0], ast.Name)
+            and not stmt.targets[0].id.startswith("__gm_defer_")
+        )
+
+    def _try_extend(self, run: list[ast.stmt], stmt: ast.stmt) -> bool:
+        if not self._eligible(stmt):
+            return False
+        try:
+            self._build(run + [stmt])
+        except Unsupported:
+            return False
+        return True
+
+    def lower_block(self, stmts: list[ast.stmt], in_loop: bool) -> list[ast.stmt]:
+        out: list[ast.stmt] = []
+        run: list[ast.stmt] = []
+        hoist: list[ast.stmt] = []
+        for stmt in self._split_returns(stmts):
+            cap = _is_capture(stmt)
+            if cap is not None and run:
+                assigned = {s.targets[0].id for s in run}
+                if not (_names_read(stmt.value) & assigned):
+                    hoist.append(stmt)
+                    continue
+            if self._try_extend(run, stmt):
+                run.append(stmt)
+                continue
+            out.extend(self.flush(run, hoist, in_loop))
+            run, hoist = [], []
+            if self._try_extend([], stmt):
+                run.append(stmt)
+                continue
+            out.append(self.lower_stmt(stmt, in_loop))
+        out.extend(self.flush(run, hoist, in_loop))
+        return out
+
+    def _split_returns(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
+        """`return <fusable expr>` -> `__gm_retv_k = <expr>; return __gm_retv_k`
+        so the returned expression can join the preceding region."""
+        out: list[ast.stmt] = []
+        for s in stmts:
+            if isinstance(s, ast.Return) and s.value is not None and not isinstance(s.value, (ast.Name, ast.Constant)):
+                try:
+                    Builder(Graph(), self.owner.torch_names, self.owner.functional_names).expr(s.value)
+                except Unsupported:
+                    out.append(s)
+                    continue
+                name = f"__gm_retv_{self.owner.next_ret()}"
+                a = ast.copy_location(ast.Assign(targets=[ast.Name(name, ast.Store())], value=s.value), s)
+                r = ast.copy_location(ast.Return(ast.Name(name, ast.Load())), s)
+                r.end_lineno, r.end_col_offset = s.end_lineno, s.end_col_offset
+                self.loads.append(((s.end_lineno, s.end_col_offset + 1), name))
+                out.extend([a, r])
+            else:
+                out.append(s)
+        return out
+
+    def lower_stmt(self, stmt: ast.stmt, in_loop: bool) -> ast.stmt:
+        rep = _is_replay(stmt)
+        if rep is not None:
+            func, cap = rep
+            site = self.owner.new_site(ast.unparse(func), cap, self.fn.name, stmt.lineno)
+            call = ast.Call(
+                func=ast.Attribute(ast.Name(GM_RT, ast.Load()), "replay", ast.Load()),
+                args=[ast.Constant(site), func, ast.Name(cap, ast.Load())],
+                keywords=[],
+            )
+            return ast.copy_location(ast.Expr(call), stmt)
+        loop = in_loop or isinstance(stmt, (ast.For, ast.AsyncFor, ast.While))
+        for attr in ("body", "orelse", "finalbody"):
+            block = getattr(stmt, attr, None)
+            if isinstance(block, list) and block and isinstance(block[0], ast.stmt):
+                setattr(stmt, attr, self.lower_block(block, loop))
+        if isinstance(stmt, ast.Try):
+            for h in stmt.handlers:
+                h.body = self.lower_block(h.body, loop)
+        return stmt
+
+    def flush(self, run: list[ast.stmt], hoist: list[ast.stmt], in_loop: bool) -> list[ast.stmt]:
+        if not run:
+            return list(hoist)
+        graph, b = self._build(run)
+        assigned: list[str] = []
+        for s in run:
+            name = s.targets[0].id
+            if name in assigned:
+                assigned.remove(name)
+            assigned.append(name)
+        last = run[-1]
+        end = (last.end_lineno, last.end_col_offset)
+        live = [n for n in assigned if in_loop or self.read_after(n, end)]
+        out_nodes = [b.env[n] for n in live]
+        if not live or not any(n.op not in ("free", "const") for n in graph.nodes):
+            return list(hoist) + list(run)
+        rid = len(self.owner.regions)
+        src = "\n".join(ast.unparse(s) for s in run)
+        fallback = self.owner.make_fallback(rid, run, graph, live)
+        region = Region(rid, f"{self.fn.name}:{run[0].lineno}-{last.end_lineno}", graph, live, out_nodes,
+                        fallback, src)
+        self.owner.regions.append(region)
+        self.owner.region_sources.append(src)
+        args = [ast.parse(fv.text, mode="eval").body for fv in graph.frees]
+        call = ast.Call(
+            func=ast.Subscript(
+                ast.Attribute(ast.Name(GM_RT, ast.Load()), "regions", ast.Load()), ast.Constant(rid), ast.Load()
+            ),
+            args=args,
+            keywords=[],
+        )
+        if len(live) == 1:
+            target: ast.expr = ast.Name(live[0], ast.Store())
+        else:
+            target = ast.Tuple([ast.Name(n, ast.Store()) for n in live], ast.Store())
+        stmt = ast.Assign(targets=[target], value=call)
+        ast.copy_location(stmt, run[0])
+        return list(hoist) + [stmt]
+
+
+class _Lowerer:
+    def __init__(self, text: str):
+        self.text = text
+        self.tree = ast.parse(text)
+        self.torch_names, self.functional_names = _torch_aliases(self.tree)
+        self.regions: list[Region] = []
+        self.region_sources: list[str] = []
+        self.sites: list[ReplaySite] = []
+        self.fallback_defs: list[ast.FunctionDef] = []
+
+    def next_ret(self) -> int:
+        self._ret = getattr(self, "_ret", -1) + 1
+        return self._ret
+
+    def new_site(self, callee_src: str, cap: str, fn: str, lineno: int) -> int:
+        sid = len(self.sites)
+        self.sites.append(ReplaySite(sid, callee_src, cap, fn, lineno))
+        return sid
+
+    def make_fallback(self, rid: int, run: list[ast.stmt], graph: Graph, live: list[str]):
+        """The region's original statements as a function of its free values."""
+        params = [f"__gm_a{i}" for i in range(len(graph.frees))]
+        attr_frees = {fv.text: params[i] for i, fv in enumerate(graph.frees) if "." in fv.text}
+        name_frees = [(fv.text, params[i]) for i, fv in enumerate(graph.frees) if "." not in fv.text]
+
+        class _Sub(ast.NodeTransformer):
+            def visit_Attribute(self, node):
+                chain = attr_chain(node)
+                if chain is not None and isinstance(node.ctx, ast.Load):
+                    text = ".".join(chain)
+                    if text in attr_frees:
+                        return ast.copy_location(ast.Name(attr_frees[text], ast.Load()), node)
+                return self.generic_visit(node)
+
+        body: list[ast.stmt] = [
+            ast.Assign(targets=[ast.Name(n, ast.Store())], value=ast.Name(p, ast.Load())) for n, p in name_frees
+        ]
+        body += [_Sub().visit(copy.deepcopy(s)) for s in run]
+        ret = ast.Name(live[0], ast.Load()) if len(live) == 1 else ast.Tuple(
+            [ast.Name(n, ast.Load()) for n in live], ast.Load())
+        body.append(ast.Return(ret))
+        fdef = ast.FunctionDef(
+            name=f"__gm_fallback_{rid}",
+            args=ast.arguments(posonlyargs=[], args=[ast.arg(p) for p in params], vararg=None, kwonlyargs=[],
+                               kw_defaults=[], kwarg=None, defaults=[]),
+            body=body,
+            decorator_list=[],
+            returns=None,
+            type_params=[],
+        )
+        self.fallback_defs.append(fdef)
+        holder = {"rid": rid}
+        self._pending = getattr(self, "_pending", [])
+        self._pending.append(holder)
+
+        def call(*args, _holder=holder):
+            return _holder["fn"](*args)
+
+        return call
+
+    def run(self) -> Lowered:
+        fns = [n for n in ast.walk(self.tree) if isinstance(n, (ast.FunctionDef, ast.AsyncFunctionDef))]
+        for fn in fns:
+            fl = _FunctionLowerer(self, fn)
+            fn.body = fl.lower_block(fn.body, in_loop=False)
+        ast.fix_missing_locations(self.tree)
+        source = ast.unparse(self.tree)
+        return Lowered(self.text, source, self.regions, self.sites, self.region_sources)
+
+
+def lower(text: str) -> tuple[Lowered, "_Lowerer"]:
+    lw = _Lowerer(text)
+    return lw.run(), lw
+
+
+def load(text: str, name: str | None = None, runtime=None) -> tuple[types.ModuleType, Lowered]:
+    """Lower `text` and execute it as a fresh module whose `__gm_rt` is the
+    module runtime (logring.ModuleRuntime)."""
+    from .logring import ModuleRuntime
+
+    lowered, lw = lower(text)
+    mod_name = name or f"_gm_b200_prog_{next(_module_ids)}"
+    filename = f"<gm-b200:{mod_name}>"
+    module = types.ModuleType(mod_name)
+    module.__file__ = filename
+    rt = runtime or ModuleRuntime(lowered)
+    module.__dict__[GM_RT] = rt
+    # fallbacks are compiled in the module namespace so globals resolve
+    fb_mod = ast.Module(body=lw.fallback_defs, type_ignores=[])
+    ast.fix_missing_locations(fb_mod)
+    fb_src = ast.unparse(fb_mod)
+    full = lowered.source + "\n\n" + fb_src + "\n"
+    linecache.cache[filename] = (len(full), None, full.splitlines(True), filename)
+    code = compile(full, filename, "exec")
+    import sys
+
+    sys.modules[mod_name] = module
+    exec(code, module.__dict__)
+    for holder in getattr(lw, "_pending", []):
+        holder["fn"] = module.__dict__[f"__gm_fallback_{holder['rid']}"]
+    lowered.source = full
+    return module, lowered

@@ -1,0 +1,213 @@
+"""Runtime side of a fused region: specialisation cache, launch, scratch.
+
+A `Region` is created by the lowering (lowering.py) for one run of fusable
+statements.  Calling it with the region's free values launches one
+NVRTC-compiled sm_100a kernel (codegen.py + csrc/gm_region.cuh) on the
+current CUDA stream and returns the live-out tensors.  Launches are
+stream-ordered and graph-capturable; no call synchronises with the host.
+
+When the arguments leave the fusable subset (integer tensors, CPU tensors,
+shapes that do not broadcast to one iteration space, ...), the region runs
+its original statements with PyTorch instead — the exact code the reference
+transform emitted (`fallback`), on the device the tensors live on.  Every
+such decision is recorded in `Region.stats` so tests can assert that the
+fused kernel is what ran.  Missing native code is never a fallback: a
+NativeError propagates.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+from .codegen import DT_SIZE, MODE_FULL, MODE_PERIODIC, MODE_SCALAR, MODE_STRIDED, UNROLL, Plan
+from .ir import Graph, Node, Unsupported
+
+_kernel_cache: dict[str, nat.CompiledRegion] = {}
+_kernel_lock = threading.Lock()
+
+
+def compiled_kernel(source: str, kernel: str) -> nat.CompiledRegion:
+    with _kernel_lock:
+        k = _kernel_cache.get(source)
+        if k is None:
+            k = nat.CompiledRegion(source, kernel)
+            _kernel_cache[source] = k
+        return k
+
+
+def arg_key(a) -> tuple:
+    if torch.is_tensor(a):
+        return ("t", a.dtype, tuple(a.shape), tuple(a.stride()), a.device.type, a.device.index,
+                a.data_ptr() % 16 == 0)
+    if isinstance(a, (bool, int, float)):
+        return ("h", type(a))
+    return ("o", type(a))
+
+
+@dataclass
+class RegionStats:
+    launches: int = 0
+    fallbacks: int = 0
+    fallback_reasons: list = field(default_factory=list)
+
+
+class _Spec:
+    """A compiled specialisation plus its launch configuration."""
+
+    def __init__(self, region: "Region", args: list):
+        dev = next(a.device for a in args if torch.is_tensor(a) and a.device.type == "cuda")
+        self.device = dev
+        sms, smem_optin = nat.init(dev.index if dev.index is not None else torch.cuda.current_device())
+        plan = Plan(region.graph, region.out_nodes, args, name=region.name, device_info=(sms, smem_optin))
+        self.plan = plan
+        self.kernel = compiled_kernel(plan.source, plan.kernel)
+        n = plan.n
+        nvec = -(-n // nat.VEC) if n else 0
+        threads = nat.THREADS
+        if plan.res_grid is not None:
+            grid, vpc, smem = plan.res_grid, plan.res_vpc, plan.res_smem
+            occ = self.kernel.occupancy(threads, smem)
+            if occ < 1:
+                raise nat.NativeError(f"region {region.name}: resident plan does not fit ({smem} B smem)")
+        elif plan.reductions:
+            occ = max(1, self.kernel.occupancy(threads, 0))
+            grid = max(1, min(sms * occ, -(-nvec // (threads * UNROLL)) if nvec else 1))
+            vpc = -(-nvec // grid) if nvec else 0
+            smem = 0
+        else:
+            # pure map: no grid barrier, any grid size
+            per_cta = threads * UNROLL * 4
+            grid = max(1, -(-nvec // per_cta)) if nvec else 1
+            vpc = -(-nvec // grid) if nvec else 0
+            smem = 0
+        if vpc:
+            grid = max(1, -(-nvec // vpc))
+        self.grid, self.vpc, self.smem, self.threads = grid, vpc, smem, threads
+        self.nred = len(plan.reductions)
+        self.nscal = len(plan.scalars)
+        # scratch: barrier(8) status(4) | partials | scalar mirror
+        part_bytes = 8 * max(1, self.nred) * grid
+        self.scratch = torch.zeros(64 + part_bytes + 8 * max(1, self.nscal), dtype=torch.uint8, device=dev)
+        base = self.scratch.data_ptr()
+        P = nat.Params()
+        P.n = n
+        P.nvec = nvec
+        P.vpc = vpc
+        P.piece_vecs = max(64, -(-vpc // nat.MAX_PIECES)) if vpc else 1
+        P.barrier = base
+        P.status = base + 8
+        P.partials = base + 64
+        P.scal_out = base + 64 + part_bytes
+        self.template = P
+        self.in_slots = []  # (slot, free_index, mode)
+        for ip in plan.inputs:
+            d = P.inp[ip.slot]
+            d.smem_off = plan.smem_off.get(ip.slot, -1) if plan.res_grid is not None else -1
+            if ip.mode == MODE_PERIODIC:
+                t = args[ip.free_index]
+                d.size[0] = t.numel()
+            elif ip.mode == MODE_STRIDED:
+                t = args[ip.free_index]
+                S = tuple(plan.shape)
+                ex = t.expand(S)
+                if len(S) > nat.MAX_DIMS:
+                    raise Unsupported("too many dims for a strided input")
+                d.ndim = len(S)
+                for j, (s, st) in enumerate(zip(S, ex.stride())):
+                    d.size[j] = s
+                    d.stride[j] = st
+            self.in_slots.append((ip.slot, ip.free_index))
+        self.hs_index = [node.value for node in plan.host_frees]
+        # outputs
+        self.out_specs = []  # (out position, kind, dtype, kernel slot or None)
+        k = 0
+        for j, o in enumerate(plan.outputs):
+            if o.op == "free":
+                self.out_specs.append((j, "alias", o.value, None))
+            elif o.kind == "elem":
+                self.out_specs.append((j, "elem", o.dtype, k))
+                k += 1
+            else:
+                self.out_specs.append((j, "scalar", o.dtype, k))
+                k += 1
+        self.shape = tuple(plan.shape)
+
+    def run(self, args: list):
+        P = nat.Params()
+        ctypes.memmove(ctypes.byref(P), ctypes.byref(self.template), ctypes.sizeof(P))
+        for slot, fi in self.in_slots:
+            P.inp[slot].ptr = args[fi].data_ptr()
+        for j, fi in enumerate(self.hs_index):
+            P.hs[j] = float(args[fi])
+        outs = [None] * len(self.out_specs)
+        for j, kind, info, k in self.out_specs:
+            if kind == "alias":
+                outs[j] = args[info]
+            elif kind == "elem":
+                t = torch.empty(self.shape, dtype=info, device=self.device)
+                P.out[k].ptr = t.data_ptr()
+                outs[j] = t
+            else:
+                t = torch.empty((), dtype=info, device=self.device)
+                P.out[k].ptr = t.data_ptr()
+                outs[j] = t
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.kernel.launch(P, self.grid, self.threads, self.smem, stream)
+        return outs
+
+    def status(self) -> int:
+        """Grid-barrier status word (syncs; diagnostics only)."""
+        return int(self.scratch[8:12].view(torch.int32).item())
+
+    def scalars(self) -> list[float]:
+        """Scalar slots mirrored by CTA 0 of the last launch (syncs; tests)."""
+        off = 64 + 8 * max(1, self.nred) * self.grid
+        return self.scratch[off: off + 8 * self.nscal].view(torch.float64).tolist()
+
+
+class Region:
+    """One fused run of statements of a transformed forward."""
+
+    def __init__(self, rid: int, name: str, graph: Graph, out_names: list[str], out_nodes: list[Node],
+                 fallback, source: str):
+        self.rid = rid
+        self.name = name
+        self.graph = graph
+        self.out_names = out_names
+        self.out_nodes = out_nodes
+        self.fallback = fallback          # the original statements as a function
+        self.source = source              # their text (for reports)
+        self.specs: dict[tuple, object] = {}
+        self.stats = RegionStats()
+        self.last_spec: _Spec | None = None
+
+    def __call__(self, *args):
+        key = tuple(arg_key(a) for a in args)
+        spec = self.specs.get(key)
+        if spec is None:
+            spec = self._specialise(list(args))
+            self.specs[key] = spec
+        if isinstance(spec, str):
+            self.stats.fallbacks += 1
+            return self.fallback(*args)
+        self.stats.launches += 1
+        self.last_spec = spec
+        outs = spec.run(list(args))
+        return outs[0] if len(outs) == 1 else tuple(outs)
+
+    def _specialise(self, args: list):
+        if not any(torch.is_tensor(a) and a.device.type == "cuda" for a in args):
+            reason = "no CUDA tensor argument"
+            self.stats.fallback_reasons.append(reason)
+            return reason
+        try:
+            return _Spec(self, args)
+        except Unsupported as exc:
+            reason = str(exc)
+            self.stats.fallback_reasons.append(reason)
+            return reason

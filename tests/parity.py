@@ -1,0 +1,31 @@
+"""Shared parity helpers for the GPU tests (B200 path vs the CPU oracle)."""
+
+import torch
+
+# north_star: outputs within 1e-5 relative (fp32) or 1e-2 (bf16) of the
+# reference's eager CPU execution of the same transformed program.  Elements
+# near zero get a floor of 1% of the tensor's largest magnitude.
+TOL = {torch.float32: 1e-5, torch.bfloat16: 1e-2, torch.float16: 1e-2}
+
+
+def assert_parity(out: torch.Tensor, ref: torch.Tensor, dtype=torch.float32, what: str = ""):
+    out = out.detach().to("cpu")
+    ref = ref.detach().to("cpu")
+    assert out.shape == ref.shape, (what, out.shape, ref.shape)
+    assert out.dtype == ref.dtype, (what, out.dtype, ref.dtype)
+    if not ref.dtype.is_floating_point:
+        assert torch.equal(out, ref), what
+        return
+    tol = TOL[dtype]
+    o, r = out.double(), ref.double()
+    floor = 0.01 * float(r.abs().max()) if r.numel() else 0.0
+    bad = (o - r).abs() > tol * (r.abs() + floor)
+    nan_ok = torch.isnan(o) == torch.isnan(r)
+    assert bool(nan_ok.all()), f"{what}: NaN pattern differs"
+    bad &= ~torch.isnan(r)
+    if bool(bad.any()):
+        i = int(bad.reshape(-1).nonzero()[0])
+        raise AssertionError(
+            f"{what}: {int(bad.sum())} of {r.numel()} elements out of tolerance {tol}; "
+            f"first at flat index {i}: out={o.reshape(-1)[i].item()!r} ref={r.reshape(-1)[i].item()!r}"
+        )

@@ -1,0 +1,47 @@
+"""Precompiled sm_100a kernels of libgm_b200.so, called through the C ABI."""
+
+import ctypes
+
+import pytest
+import torch
+
+from paper_2509_16248_b200 import _native as nat
+
+RED = {0: "sum", 1: "mean", 2: "max", 3: "min", 4: "norm"}
+CMP = {0: ">", 1: ">=", 2: "<", 3: "<="}
+
+
+def _stat_ref(x: torch.Tensor, red: int) -> torch.Tensor:
+    return {0: x.sum, 1: x.mean, 2: x.max, 3: x.min, 4: x.norm}[red]()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [64, 1000003, 8 * 1024 * 768, 4 * 4096 * 768])
+@pytest.mark.parametrize("red", [0, 1, 2, 3, 4])
+def test_branch_select_f32(n, red):
+    """gm_branch_select_f32 == the transformed phi4 block executed by torch on
+    CPU: pred = x.<red>() > thr; out = where(pred, x*a1 + b1, x*a2 + b2)
+    (corpus/phi4_like/original.py:8-11 after transform.py:359-376)."""
+    lib = nat.lib()
+    nat.init(torch.cuda.current_device())
+    torch.manual_seed(n + red)
+    x = torch.randn(n) + 0.01
+    stat = _stat_ref(x, red)
+    xd = x.cuda()
+    out = torch.empty_like(xd)
+    scratch = torch.zeros(lib.gm_branch_select_scratch_bytes(), dtype=torch.uint8, device="cuda")
+    stat_out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for thr, cmp in ((float(stat) * 0.5 - 1.0, 0), (float(stat) * 1.5 + 1.0, 0), (float(stat) - 1.0, 2)):
+        nat.check(lib.gm_branch_select_f32(ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(out.data_ptr()), n,
+                                           red, cmp, thr, 2.0, 1.0, 0.5, -1.0,
+                                           ctypes.c_void_p(scratch.data_ptr()),
+                                           ctypes.c_void_p(stat_out.data_ptr()), ctypes.c_void_p(stream)))
+        torch.cuda.synchronize()
+        assert int(scratch[8:12].view(torch.int32).item()) == 0, "grid barrier timed out"
+        s = stat_out.cpu()
+        torch.testing.assert_close(torch.tensor(float(s[0]), dtype=torch.float32), stat, rtol=2e-5, atol=1e-4)
+        pred_ref = bool(stat > thr) if cmp == 0 else bool(stat < thr)
+        assert bool(s[1] != 0) == pred_ref
+        ref = torch.where(torch.tensor(pred_ref), x * 2.0 + 1.0, x * 0.5 + -1.0)
+        assert torch.equal(out.cpu(), ref), "affine arm must be bit-exact"
