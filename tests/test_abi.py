@@ -1,0 +1,47 @@
+"""The C ABI library loads on a GPU-less host and exports exactly what
+include/gm_b200.h declares (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+from paper_2509_16248_b200 import _native as nat
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "gm_b200.h")
+
+
+def _declared() -> set[str]:
+    text = open(HEADER).read()
+    return set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(gm_[a-z_0-9]+)\s*\(", text, re.M))
+
+
+def test_library_loads_and_versions():
+    lib = nat.lib()
+    assert lib.gm_abi_version() == nat.ABI_VERSION
+    assert lib.gm_region_params_bytes() == ctypes.sizeof(nat.Params)
+    assert lib.gm_last_error() == b""
+
+
+def test_header_symbols_exported():
+    lib = nat.lib()
+    declared = _declared()
+    assert {"gm_init", "gm_region_compile", "gm_region_launch", "gm_logring_gather"} <= declared
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/gm_b200.h but not exported"
+    assert declared == set(nat.EXPORTED), declared ^ set(nat.EXPORTED)
+
+
+def test_errors_are_status_codes():
+    lib = nat.lib()
+    # no device initialised: compute entry points refuse with a message, never crash
+    rc = lib.gm_region_compile(b"", b"k", ctypes.byref(ctypes.c_void_p()), None, 0)
+    assert rc != 0 and lib.gm_last_error()
+    rc = lib.gm_logring_gather(None, None, 0, 0, None, None, None, 0, 0, 0, None)
+    assert rc == -1
+
+
+def test_nvrtc_compiles_skeleton_for_sm100a():
+    src = ('#include "gm_region.cuh"\nextern "C" __global__ void k(const __grid_constant__ gm::Params P) '
+           '{ float x[8]; gm::load8<GM_DT_BF16>(P.in[0], 0u, 0, 0, 8, x); gm::store8<GM_DT_F32>(P.out[0], 0, 8, x); }\n')
+    cubin = nat.compile_cubin(src, (10, 0))
+    assert cubin[:4] == b"\x7fELF"

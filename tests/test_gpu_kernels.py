@@ -40,7 +40,14 @@ def test_branch_select_f32(n, red):
         torch.cuda.synchronize()
         assert int(scratch[8:12].view(torch.int32).item()) == 0, "grid barrier timed out"
         s = stat_out.cpu()
-        torch.testing.assert_close(torch.tensor(float(s[0]), dtype=torch.float32), stat, rtol=2e-5, atol=1e-4)
+        # fp64 grid combine: the statistic is the correctly rounded fp32 value
+        # (torch's CPU fp32 norm accumulates in fp32 and drifts ~2e-4 relative
+        # at 6M elements, so against torch the bound is looser for norm)
+        exact = {0: x.double().sum, 1: x.double().mean, 2: x.double().max, 3: x.double().min,
+                 4: x.double().norm}[red]()
+        assert abs(float(s[0]) - float(exact)) <= 2e-6 * abs(float(exact)) + 1e-6
+        torch.testing.assert_close(torch.tensor(float(s[0]), dtype=torch.float32), stat,
+                                   rtol=5e-4 if red == 4 else 2e-5, atol=1e-4)
         pred_ref = bool(stat > thr) if cmp == 0 else bool(stat < thr)
         assert bool(s[1] != 0) == pred_ref
         ref = torch.where(torch.tensor(pred_ref), x * 2.0 + 1.0, x * 0.5 + -1.0)

@@ -9,7 +9,7 @@ import torch
 
 from oracle import executor as orc
 from paper_2509_16248_b200 import harness
-from tests.parity import assert_parity
+from parity import assert_parity
 
 CORPUS = ["biogpt_like", "blenderbot_like", "flan_t5_like", "longformer_like", "moe_minicpm_like",
           "pegasus_like", "phi4_like", "qwen_audio_like"]

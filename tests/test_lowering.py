@@ -1,0 +1,115 @@
+"""Lowering of transformed programs (CPU): structure, liveness, and exact
+equivalence of the lowered program with the reference's transformed text
+when regions run their original statements (tensors on CPU)."""
+
+import ast
+
+import pytest
+import torch
+
+from oracle import executor as orc
+from paper_2509_16248_b200 import codegen, lowering
+from paper_2509_16248_b200 import _native as nat
+
+ALL = ["bart_step", "bigbird_like", "biogpt_like", "blenderbot_like", "flan_t5_like", "longformer_like",
+       "moe_minicpm_like", "pegasus_like", "phi4_like", "qwen_audio_like", "toy"]
+
+
+def test_phi4_is_one_region(programs):
+    low, _ = lowering.lower(programs["phi4_like"]["transformed"])
+    assert len(low.regions) == 1
+    r = low.regions[0]
+    assert [fv.text for fv in r.graph.frees] == ["x"]
+    # h, a..d and every __gm_* temporary stay on chip; only the result leaves
+    assert len(r.out_names) == 1 and r.out_names[0].startswith("__gm_retv_")
+
+
+def test_bigbird_regions_and_replay(programs):
+    low, _ = lowering.lower(programs["bigbird_like"]["transformed"])
+    assert [r.out_names for r in low.regions] == [["ctx"], ["res"]]
+    assert [fv.text for fv in low.regions[0].graph.frees] == ["q", "self.scale", "hidden"]
+    assert [(s.callee_src, s.capture_name) for s in low.sites] == [("logger.info", "__gm_defer_0")]
+    tree = ast.parse(low.source)
+    calls = [n for n in ast.walk(tree) if isinstance(n, ast.Call) and isinstance(n.func, ast.Attribute)
+             and n.func.attr == "replay"]
+    assert len(calls) == 1
+
+
+def test_capture_hoisted_not_splitting(programs):
+    """biogpt: two deferrals between elementwise statements -> one region."""
+    low, _ = lowering.lower(programs["biogpt_like"]["transformed"])
+    assert len(low.regions) == 1
+    assert len(low.sites) == 2
+
+
+def test_longformer_item_reads_cut_regions(programs):
+    low, _ = lowering.lower(programs["longformer_like"]["transformed"])
+    assert [r.out_names for r in low.regions] == [["win", "span"], ["scaled", "peak"], ["shifted", "floor"]]
+
+
+def test_name_mangling_safe():
+    src = ("import torch\nclass M(torch.nn.Module):\n    def forward(self, x):\n        __gm_pred_0 = x.sum() > 0\n"
+           "        __gm_then_y_0 = x + 1\n        __gm_else_y_0 = x - 1\n"
+           "        y = torch.where(__gm_pred_0, __gm_then_y_0, __gm_else_y_0)\n        return y * 2\nm = M()\n")
+    mod, low = lowering.load(src)
+    x = torch.randn(5)
+    assert torch.equal(mod.m(x), torch.where(x.sum() > 0, x + 1, x - 1) * 2)
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_lowered_equals_transformed_on_cpu(programs, name):
+    """With CPU tensors every region runs its original statements and every
+    replay is immediate, so the lowered program must be bit-identical to the
+    reference's transformed program — this pins liveness, hoisting, return
+    splitting and the fallback functions."""
+    p = programs[name]
+    for spec in p["inputs"]:
+        shapes = None
+        if name == "bigbird_like":
+            shapes = [[1, 32, 768]]
+        elif name == "bart_step":
+            shapes = [[4, 1, 768]]
+        args = orc.make_args(spec["args"], spec["seed"], shapes=shapes)
+        ref, rt = orc.run_reference(p["transformed"], p["callable"], args)
+        mod, low = lowering.load(p["transformed"])
+        out, t = orc.call_captured(getattr(mod, p["callable"]), args)
+        assert t == rt
+        assert torch.equal(out, ref) if isinstance(ref, torch.Tensor) else out == ref
+        assert all(r.stats.launches == 0 for r in low.regions)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("name", ["phi4_like", "bigbird_like", "qwen_audio_like", "flan_t5_like"])
+def test_region_codegen_compiles_for_sm100a(programs, name, dtype):
+    """Every region of the BASELINE-shaped programs specialises and its
+    generated source compiles with NVRTC for sm_100a (no GPU needed)."""
+    mod, low = lowering.load(programs[name]["transformed"])
+    for r in low.regions:
+        args = []
+        for fv in r.graph.frees:
+            if fv.text.startswith("self."):
+                args.append(getattr(mod.model, fv.text[5:]))
+            elif name == "flan_t5_like":
+                args.append(torch.randn(8192, 768).to(dtype))
+            else:
+                args.append(torch.randn(8, 1024, 768).to(dtype))
+        plan = codegen.Plan(r.graph, r.out_nodes, args, r.name, allow_cpu=True)
+        cubin = nat.compile_cubin(plan.source, (10, 0))
+        assert cubin[:4] == b"\x7fELF"
+
+
+def test_uniform_select_guards_untaken_arm(programs):
+    """bigbird region 0: `hidden` is read only by the else arm, so its load
+    sits under the negated predicate and never happens when the then arm is
+    selected (the reference evaluates both arms, transform.py:404-412)."""
+    mod, low = lowering.load(programs["bigbird_like"]["transformed"])
+    r = low.regions[0]
+    args = [torch.randn(8, 64, 768), 0.125, torch.randn(8, 64, 768)]
+    plan = codegen.Plan(r.graph, r.out_nodes, args, r.name, allow_cpu=True)
+    assert plan.npass == 2 and len(plan.reductions) == 1
+    src = plan.source
+    i = src.index("// ---- pass 1")
+    j = src.index("P.in[1]", i)
+    assert "if ((!sb" in src[i:j]
+    # q is read by both passes and is staged in shared memory once
+    assert plan.resident_flags[0] and not plan.resident_flags[1]
