@@ -1,0 +1,358 @@
+"""Bench: forward latency / throughput of a GraphMend-transformed program on
+the B200 path (BASELINE.json metric; config 2 = BigBird-like layer, seq 1024,
+batch 8, bf16, random-init weights, synthetic inputs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--dtype bf16|fp32]
+    python bench.py --impl reference ...     # the reference's CPU path on the host cores
+
+A step = one forward of the transformed program over one batch.  `value` is
+whole-job samples/s with inputs resident in HBM (graph replay only, device
+timed per step with CUDA events, L2 flushed between steps); `e2e` is the same
+forward through the public API (B200Executor.__call__) from pinned host
+buffers with the H2D input copy and D2H output read inside the timed region.
+Multi-GPU: independent replicas (every predicate is a global
+reduction, so the path does not shard), one process per GPU; the timing is
+the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "p50 forward latency (ms) & samples/s per model; host syncs per forward"
+WORKLOADS = {
+    "bigbird_like": ("config 2: BigBird-RoBERTa-base-shaped layer, seq 1024, batch 8", None),
+    "bart_step": ("config 4: BART-base-shaped decoder step, batch 32", None),
+    "phi4_like": ("config 5: corpus phi4_like at [8,1024,768]", [[8, 1024, 768]]),
+    "qwen_audio_like": ("config 5: corpus qwen_audio_like at [8,1024,768]", [[8, 1024, 768]]),
+    "longformer_like": ("config 3: corpus longformer_like at [4,4096,768]", [[4, 4096, 768]]),
+    "biogpt_like": ("config 5: corpus biogpt_like at [8,1024,768]", [[8, 1024, 768]] * 2),
+}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def _inputs(prog, shapes, dtype):
+    from paper_2509_16248_b200.harness import make_args
+
+    spec = prog["inputs"][0]
+    return make_args(spec["args"], spec["seed"], dtype, shapes)
+
+
+def run_reference(args, ws, rank):
+    """The reference's CPU path: the reference-transformed program executed
+    eagerly on CPU (harness call shape, runner.py:154-157) with all host
+    threads; rank 0 only."""
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import executor as orc
+    from paper_2509_16248_b200.harness import programs
+
+    threads = len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    dtype = {"bf16": torch.bfloat16, "fp32": torch.float32}[args.dtype]
+    prog = programs()[args.workload]
+    shapes = WORKLOADS[args.workload][1]
+    x = _inputs(prog, shapes, dtype)
+    fn = orc.reference_callable(prog["transformed"], prog["callable"], dtype)
+    for _ in range(args.warmup):
+        orc.call_captured(fn, x)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.call_captured(fn, x)
+        times.append(time.perf_counter() - t0)
+    batch = int(x[0].shape[0])
+    total = sum(times)
+    value = batch * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "p50_ms": 1e3 * statistics.median(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (manifest seed/dist), random-init weights",
+        "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
+                   "shape": list(x[0].shape)},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} full forwards of the reference-transformed program, eager "
+                                   f"torch CPU, {threads} threads"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(prog, shapes, dtype, budget_s=15.0):
+    """Bounded CPU-oracle sample on the box's host cores (rank 0, N=1)."""
+    import torch
+
+    from oracle import executor as orc
+
+    threads = len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    x = _inputs(prog, shapes, dtype)
+    fn = orc.reference_callable(prog["transformed"], prog["callable"], dtype)
+    orc.call_captured(fn, x)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end and len(times) < 50:
+        t0 = time.perf_counter()
+        orc.call_captured(fn, x)
+        times.append(time.perf_counter() - t0)
+    batch = int(x[0].shape[0])
+    return {"value": batch * len(times) / sum(times), "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{len(times)} forwards of the reference-transformed program (same inputs), eager torch "
+                      f"CPU, {threads} threads; p50 {1e3 * statistics.median(times):.2f} ms"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="bigbird_like", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    ws, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import torch
+
+    from paper_2509_16248_b200 import compile_program
+    from paper_2509_16248_b200.harness import programs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    dtype = {"bf16": torch.bfloat16, "fp32": torch.float32}[args.dtype]
+    prog = programs()[args.workload]
+    shapes = WORKLOADS[args.workload][1]
+    x_host = [t.pin_memory() for t in _inputs(prog, shapes, dtype)]
+    batch = int(x_host[0].shape[0])
+
+    t0 = time.perf_counter()
+    ex, mod, low = compile_program(prog["transformed"], prog["callable"], device=dev, dtype=dtype)
+    entry = ex.prepare(*[t.to(dev) for t in x_host])
+    torch.cuda.synchronize(dev)
+    cold_ms = 1e3 * (time.perf_counter() - t0)
+    entry.load([t.to(dev) for t in x_host])
+    info = entry.info
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- device-timed replay (inputs resident in HBM)
+    for _ in range(args.warmup):
+        entry.run()
+    ex.flush()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush_buf.zero_()
+            starts[i].record(stream)
+            entry.run()
+            ends[i].record(stream)
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ex.flush()
+    total_ms = sum(step_ms)
+    if pg is not None:
+        t = torch.tensor([total_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total_ms = float(t)
+    value = ws * batch * args.steps / (total_ms / 1e3)
+
+    # ---- dominant fused kernel timed alone (same stream, L2 flushed)
+    fused = [r for r in low.regions if r.last_spec is not None]
+    kernels = []
+    for r in fused:
+        spec = r.last_spec
+        rargs = spec._bench_args if hasattr(spec, "_bench_args") else None
+        kernels.append(_time_region(r, dev, flush_buf, args.steps))
+    kernels = [k for k in kernels if k]
+    dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
+    peak, peak_kind = _peaks()
+    roofline = None
+    if dom:
+        achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": dom["name"], "bytes_alg": dom["bytes"], "kernel_ms": dom["ms"],
+                    "peak_kind": peak_kind, "share_of_step": dom["ms"] / statistics.mean(step_ms)}
+
+    # ---- end to end through the public API (pinned host in, host out)
+    out_host = None
+    e2e_ms = []
+    h2d = sum(t.numel() * t.element_size() for t in x_host)
+    for _ in range(3):
+        out = ex(*x_host)
+        out_host = out.to("cpu", non_blocking=False)
+    ex.flush()
+    barrier()
+    t_e2e = time.perf_counter()
+    for _ in range(args.steps):
+        e0 = time.perf_counter()
+        out = ex(*x_host)
+        out_host = out.to("cpu")
+        e2e_ms.append(1e3 * (time.perf_counter() - e0))
+    barrier()
+    e2e_total = time.perf_counter() - t_e2e
+    ex.flush()
+    if pg is not None:
+        t = torch.tensor([e2e_total], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_total = float(t)
+    d2h = out_host.numel() * out_host.element_size()
+
+    n_region_launch = len(fused)
+    gpu_launches = args.steps * (n_region_launch + 1)  # fused regions + log-ring commit per step
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "samples/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "p50_ms": statistics.median(step_ms),
+        "cold_ms": cold_ms,
+        "host_syncs_per_forward": info.host_syncs,
+        "mode": info.mode,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic inputs (manifest seed/dist at the BASELINE shape), random-init weights (seed 0)",
+        "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
+                   "shape": list(x_host[0].shape), "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "e2e": {"value": ws * batch * args.steps / e2e_total, "unit": "samples/s", "p50_ms": statistics.median(e2e_ms),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": gpu_launches,
+        "roofline": roofline,
+        "kernels": kernels,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(prog, shapes, dtype)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def _time_region(region, dev, flush_buf, steps):
+    """Launch the region's kernel alone (same inputs as in the forward) and
+    time it with CUDA events on the launching stream."""
+    import torch
+
+    spec = region.last_spec
+    args = getattr(region, "last_args", None)
+    if spec is None or args is None:
+        return None
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        spec.run(list(args))
+    times = []
+    for _ in range(min(steps, 100)):
+        flush_buf.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        spec.run(list(args))
+        e.record(stream)
+        e.synchronize()
+        times.append(s.elapsed_time(e))
+    return {"name": f"{spec.plan.kernel} ({region.name})", "ms": statistics.mean(times),
+            "bytes": spec.bytes_alg(list(args)), "grid": spec.grid, "smem": spec.smem,
+            "passes": spec.plan.npass}
+
+
+if __name__ == "__main__":
+    main()

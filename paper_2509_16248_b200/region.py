@@ -160,6 +160,34 @@ class _Spec:
         self.kernel.launch(P, self.grid, self.threads, self.smem, stream)
         return outs
 
+    def bytes_alg(self, args: list) -> int:
+        """Compulsory HBM bytes of the path the last launch executed: every
+        distinct input tensor the executed code reads, once, plus every
+        output (counting only the selected arm's inputs)."""
+        plan = self.plan
+        vals = self.scalars()
+        slot_of = plan.slot
+        total = 0
+        for ip in plan.inputs:
+            t = args[ip.free_index]
+            needed = False
+            for p in range(plan.npass):
+                nodes = plan._pass_nodes(p)
+                if ip.node not in nodes:
+                    continue
+                dnf = plan._guards(p).get(ip.node.uid, frozenset({frozenset()}))
+                for conj in dnf:
+                    if all((vals[slot_of[uid]] != 0.0) == pol for uid, pol in conj):
+                        needed = True
+            if ip.node.kind == "dscalar":
+                needed = True
+            if needed:
+                total += t.numel() * t.element_size()
+        for j, kind, info, k in self.out_specs:
+            if kind == "elem":
+                total += int(torch.Size(self.shape).numel()) * torch.empty((), dtype=info).element_size()
+        return total
+
     def status(self) -> int:
         """Grid-barrier status word (syncs; diagnostics only)."""
         return int(self.scratch[8:12].view(torch.int32).item())
@@ -185,6 +213,7 @@ class Region:
         self.specs: dict[tuple, object] = {}
         self.stats = RegionStats()
         self.last_spec: _Spec | None = None
+        self.last_args: tuple | None = None
 
     def __call__(self, *args):
         key = tuple(arg_key(a) for a in args)
@@ -197,6 +226,7 @@ class Region:
             return self.fallback(*args)
         self.stats.launches += 1
         self.last_spec = spec
+        self.last_args = args
         outs = spec.run(list(args))
         return outs[0] if len(outs) == 1 else tuple(outs)
 
