@@ -366,7 +366,7 @@ class Plan:
             if a[0].kind != "elem" and a[1].kind == "elem":
                 # s / x == s * reciprocal(x), reciprocal rounded to the dtype
                 rr = _round_f(a[1].dtype if a[1].dtype != torch.bool else node.dtype)
-                rec = f"gm::div(1.f, {self._ev(a[1], L, u)})"
+                rec = f"gm::recip({self._ev(a[1], L, u)})"
                 rec = f"{rr}({rec})" if rr else rec
                 body = wrap(f"gm::mul({rec}, {self._sf(a[0])})")
             else:
@@ -379,10 +379,10 @@ class Plan:
                     2.0: f"gm::mul({base}, {base})",
                     3.0: f"gm::mul(gm::mul({base}, {base}), {base})",
                     0.5: f"gm::fsqrt({base})",
-                    -0.5: f"gm::div(1.f, gm::fsqrt({base}))",
+                    -0.5: f"gm::recip(gm::fsqrt({base}))",
                     1.0: f"{base}",
-                    -1.0: f"gm::div(1.f, {base})",
-                    -2.0: f"gm::div(1.f, gm::mul({base}, {base}))",
+                    -1.0: f"gm::recip({base})",
+                    -2.0: f"gm::recip(gm::mul({base}, {base}))",
                     0.0: "1.f",
                 }
                 body = wrap(special.get(ex, f"powf({base}, {_fl(ex)}f)"))
@@ -426,9 +426,9 @@ class Plan:
             un = {
                 "neg": f"(-{x})", "pos": f"({x})", "abs": f"fabsf({x})", "relu": f"gm::relu({x})",
                 "sigmoid": f"gm::sigmoid({x})", "tanh": f"tanhf({x})", "exp": f"expf({x})",
-                "log": f"logf({x})", "sqrt": f"gm::fsqrt({x})", "rsqrt": f"gm::div(1.f, gm::fsqrt({x}))",
+                "log": f"logf({x})", "sqrt": f"gm::fsqrt({x})", "rsqrt": f"gm::recip(gm::fsqrt({x}))",
                 "sin": f"sinf({x})", "cos": f"cosf({x})", "silu": f"gm::silu({x})",
-                "square": f"gm::mul({x}, {x})", "reciprocal": f"gm::div(1.f, {x})",
+                "square": f"gm::mul({x}, {x})", "reciprocal": f"gm::recip({x})",
             }
             if op not in un:
                 raise Unsupported(f"codegen for {op}")
@@ -531,7 +531,7 @@ class Plan:
             "neg": f"(-{x})", "pos": f"({x})", "abs": f"fabs({x})", "relu": f"({x} > 0.0 ? {x} : 0.0)",
             "sigmoid": f"(double)gm::sigmoid((float){x})", "tanh": f"(double)tanhf((float){x})",
             "exp": f"(double)expf((float){x})", "log": f"(double)logf((float){x})",
-            "sqrt": f"(double)gm::fsqrt((float){x})", "rsqrt": f"(double)gm::div(1.f, gm::fsqrt((float){x}))",
+            "sqrt": f"(double)gm::fsqrt((float){x})", "rsqrt": f"(double)gm::recip(gm::fsqrt((float){x}))",
             "sin": f"(double)sinf((float){x})", "cos": f"(double)cosf((float){x})",
             "silu": f"(double)gm::silu((float){x})", "square": f"({x} * {x})",
             "reciprocal": f"(1.0 / {x})",
@@ -566,11 +566,11 @@ class Plan:
         w("#define gm_trunc(x) ((double)(long long)(x))")
         w(f"// region {self.name}: shape {list(self.shape)}, {self.npass} pass(es), "
           f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s)")
-        w('extern "C" __global__ void __launch_bounds__(GM_THREADS, 1)')
+        w(f'extern "C" __global__ void __launch_bounds__(GM_THREADS, {self.minb})')
         w("GM_KERNEL_NAME(const __grid_constant__ gm::Params P) {")
         w("  using namespace gm;")
         w("  extern __shared__ __align__(128) unsigned char smem[];")
-        w("  __shared__ u64 s_bars[GM_MAX_PIECES];")
+        w("  __shared__ u64 s_bars[2 * GM_MAX_PIECES];")
         w("  __shared__ double s_warp[GM_WARPS * GM_MAX_RED];")
         w("  __shared__ double s_red[GM_MAX_RED];")
         w(f"  __shared__ double s_scal[{nscal}];")
@@ -578,13 +578,16 @@ class Plan:
         w("  const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;")
         w("  (void)v1; (void)s_bars; (void)s_warp; (void)s_red;")
         any_res = any(resident)
-        w("  Stage st; st.bars = s_bars; st.waited = 0; st.npieces = 0; st.piece_vecs = 1;")
+        w("  Stage st0, st1; st0.bars = s_bars; st1.bars = s_bars + GM_MAX_PIECES;")
+        w("  st0.waited = st1.waited = 0; st0.npieces = st1.npieces = 0; st0.piece_vecs = st1.piece_vecs = 1;")
         if any_res:
             es = ", ".join(str(DT_SIZE[ip.dtype]) for ip in self.inputs)
-            rs = ", ".join("1" if r else "0" for r in resident)
+            gs = ", ".join(str(g) for g in self.stage_group)
             w(f"  const int es_[{len(self.inputs)}] = {{{es}}};")
-            w(f"  const int res_[{len(self.inputs)}] = {{{rs}}};")
-            w(f"  stage_issue(P, smem, {len(self.inputs)}, es_, res_, v0, v1, st);")
+            w(f"  const int grp_[{len(self.inputs)}] = {{{gs}}};")
+            w(f"  stage_issue(P, smem, {len(self.inputs)}, es_, grp_, v0, v1, st0, st1);")
+        # first pass that reads a group-1 (prefetched) input
+        g1_first = min([min(ip.passes) for ip in self.inputs if self.stage_group[ip.slot] == 1] or [-1])
         for ip, r in zip(self.inputs, resident):
             if ip.mode == MODE_FULL:
                 w(f"  const u32 sres{ip.slot} = {'smem_u32(smem + P.in[%d].smem_off)' % ip.slot if r else '0u'};")
@@ -619,26 +622,30 @@ class Plan:
                     w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
             for k, r in enumerate(reds):
                 w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
-            w(f"    for (i64 vb = v0 + threadIdx.x; vb < v1; vb += {UNROLL} * GM_THREADS) {{")
-            for u in range(UNROLL):
+            U = self.unroll
+            w(f"    for (i64 vb = v0 + threadIdx.x; vb < v1; vb += {U} * GM_THREADS) {{")
+            for u in range(U):
                 w(f"      const i64 vv{u} = vb + {u} * GM_THREADS;")
                 w(f"      const i64 e{u} = vv{u} * GM_VEC;")
                 w(f"      const int nv{u} = vv{u} < v1 ? (int)((P.n - e{u}) < GM_VEC ? (P.n - e{u}) : GM_VEC) : 0;")
                 w(f"      const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
-            if p == 0 and any_res:
-                w(f"      stage_wait(st, ((vb + {UNROLL - 1} * GM_THREADS) < v1 ? (vb + {UNROLL - 1} * GM_THREADS) : (v1 - 1)) - v0);")
-            for u in range(UNROLL):
+            last_v = f"(((vb + {U - 1} * GM_THREADS) < v1 ? (vb + {U - 1} * GM_THREADS) : (v1 - 1)) - v0)"
+            if p == 0 and any(g == 0 for g in self.stage_group):
+                w(f"      stage_wait(st0, {last_v});")
+            if p == g1_first:
+                w(f"      stage_wait(st1, {last_v});")
+            for u in range(U):
                 for n in elem_nodes:
                     w(f"      float n{n.uid}_{u}[GM_VEC];")
             # loads first (unconditional full/periodic/strided), for all unrolled vectors
             loads = [n for n in elem_nodes if n.op == "free" and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))]
-            for u in range(UNROLL):
+            for u in range(U):
                 w(f"      if (nv{u} > 0) {{")
                 for n in loads:
                     for line in self._elem_code(n, u):
                         w("        " + line.replace("\n", "\n        "))
                 w("      }")
-            for u in range(UNROLL):
+            for u in range(U):
                 w(f"      if (nv{u} > 0) {{")
                 cur_guard = None
                 open_block = False
@@ -672,8 +679,10 @@ class Plan:
                     w(f"        gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
                 w("      }")
             w("    }")
-            if p == 0 and any_res:
-                w("    stage_finish(st);")
+            if p == 0 and any(g == 0 for g in self.stage_group):
+                w("    stage_finish(st0);")
+            if p == g1_first:
+                w("    stage_finish(st1);")
             if reds:
                 nr = len(reds)
                 w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
@@ -732,29 +741,58 @@ class Plan:
 
     # -- residency --------------------------------------------------------------
     def _plan_residency_flags(self) -> list[bool]:
-        """Inputs read by >= 2 passes become resident when the CTA chunks fit
-        in shared memory at one CTA per SM (decided from the shape and the
-        device, so the kernel source is a function of the plan key)."""
+        """Launch shape and shared-memory staging, decided from the shape and
+        the device so the kernel source is a function of the plan key.
+
+        Multi-pass regions stage every input some pass re-reads (read from
+        HBM once) and, space permitting, prefetch the inputs later passes
+        read once (their HBM reads then overlap pass 0 and the grid barrier).
+        Two CTAs per SM (32 warps) when the staged chunks fit in half the SM's
+        shared memory, else one.  Single-pass regions stream (no staging)."""
         nvec = -(-self.n // nat.VEC) if self.n else 0
         sms, smem_optin = self.device_info
-        grid0 = max(1, min(sms, -(-nvec // (nat.THREADS * UNROLL)))) if nvec else 1
-        vpc0 = -(-nvec // grid0) if nvec else 0
-        budget = smem_optin - STATIC_SMEM_RESERVE
-        flags = [False] * len(self.inputs)
-        cands = [ip for ip in self.inputs
-                 if ip.mode == MODE_FULL and len(ip.passes) >= 2 and DT_SIZE[ip.dtype] >= 2
-                 and (self.n * DT_SIZE[ip.dtype]) % 16 == 0]
-        cands.sort(key=lambda ip: (-len(ip.passes), ip.slot))
-        used = 0
+        self.unroll = UNROLL if self.reductions else 4
+        self.minb = 2 if self.reductions else 1
         self.smem_off = {}
-        for ip in cands:
-            nbytes = vpc0 * nat.VEC * DT_SIZE[ip.dtype]
-            nbytes = (nbytes + 127) // 128 * 128
-            if used + nbytes <= budget:
-                self.smem_off[ip.slot] = used
-                used += nbytes
+        self.res_grid, self.res_vpc, self.res_smem = None, None, 0
+        self.stage_group = [-1] * len(self.inputs)
+        flags = [False] * len(self.inputs)
+        self.resident_flags = flags
+        if not self.reductions or not nvec:
+            return flags
+        stageable = [ip for ip in self.inputs
+                     if ip.mode == MODE_FULL and ip.passes and DT_SIZE[ip.dtype] >= 2
+                     and (self.n * DT_SIZE[ip.dtype]) % 16 == 0]
+        multi = [ip for ip in stageable if len(ip.passes) >= 2]
+        first0 = [ip for ip in stageable if len(ip.passes) < 2 and 0 in ip.passes]
+        later = [ip for ip in stageable if len(ip.passes) < 2 and 0 not in ip.passes]
+        per_sm = 233472  # B200 shared memory per SM (228 KB)
+        for minb in (2, 1):
+            grid0 = max(1, min(minb * sms, -(-nvec // (nat.THREADS * self.unroll))))
+            vpc0 = -(-nvec // grid0)
+            budget = (per_sm // minb - STATIC_SMEM_RESERVE) if minb > 1 else smem_optin - STATIC_SMEM_RESERVE
+
+            def nbytes(ip):
+                return (vpc0 * nat.VEC * DT_SIZE[ip.dtype] + 127) // 128 * 128
+
+            if sum(nbytes(ip) for ip in multi) > budget and minb > 1:
+                continue
+            used = 0
+            chosen = []
+            for ip in multi + first0 + later:
+                b = nbytes(ip)
+                if used + b <= budget:
+                    chosen.append((ip, used))
+                    used += b
+            if not chosen:
+                break
+            self.minb = minb
+            for ip, off in chosen:
+                self.smem_off[ip.slot] = off
                 flags[ip.slot] = True
                 ip.resident = True
-        self.res_grid, self.res_vpc, self.res_smem = (grid0, vpc0, used) if used else (None, None, 0)
+                self.stage_group[ip.slot] = 0 if 0 in ip.passes else 1
+            self.res_grid, self.res_vpc, self.res_smem = grid0, vpc0, used
+            break
         self.resident_flags = flags
         return flags

@@ -100,7 +100,9 @@ __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b);
 __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
 __device__ __forceinline__ float relu(float a) { return (a != a) ? a : (a > 0.f ? a : 0.f); }
-__device__ __forceinline__ float sigmoid(float a) { return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-a))); }
+// 1/(1+e^-x): __frcp_rn is the correctly rounded reciprocal, identical to 1.f/y
+__device__ __forceinline__ float sigmoid(float a) { return __frcp_rn(__fadd_rn(1.f, expf(-a))); }
+__device__ __forceinline__ float recip(float a) { return __frcp_rn(a); }
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
 __device__ __forceinline__ float neg(float a) { return -a; }
 // NaN-propagating max/min (torch.maximum / Tensor.max semantics)
@@ -109,13 +111,18 @@ __device__ __forceinline__ float nmin(float a, float b) { return (a != a) ? a : 
 __device__ __forceinline__ double dmax(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a > b ? a : b)); }
 __device__ __forceinline__ double dmin(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a < b ? a : b)); }
 
-// bf16 / f16 conversions without cuda_bf16.h
+// bf16 / f16 conversions without cuda_bf16.h (hardware cvt, round-nearest-even)
 __device__ __forceinline__ float bf2f(u16 h) { return __uint_as_float(((u32)h) << 16); }
 __device__ __forceinline__ u16 f2bf(float f) {
-  u32 u = __float_as_uint(f);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return (u16)((u >> 16) | 0x40u);  // quiet NaN
-  u += 0x7fffu + ((u >> 16) & 1u);                                       // nearest-even
-  return (u16)(u >> 16);
+  u16 h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(f));
+  return h;
+}
+// two floats -> packed bf16x2 (lo in bits 0..15)
+__device__ __forceinline__ u32 f2bf2(float lo, float hi) {
+  u32 r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 __device__ __forceinline__ float h2f(u16 h) {
   float f;
@@ -128,7 +135,7 @@ __device__ __forceinline__ u16 f2h(float f) {
   return h;
 }
 // per-operator rounding to the result's storage type (eager semantics)
-__device__ __forceinline__ float rbf(float f) { return bf2f(f2bf(f)); }
+__device__ __forceinline__ float rbf(float f) { return __uint_as_float(f2bf2(0.f, f) & 0xffff0000u); }
 __device__ __forceinline__ float rh(float f) { return h2f(f2h(f)); }
 __device__ __forceinline__ double rbf_d(double d) { return (double)rbf((float)d); }
 __device__ __forceinline__ double rh_d(double d) { return (double)rh((float)d); }
@@ -257,7 +264,9 @@ template <int DT> struct Elem16 {
     lo = cv((u16)(w & 0xffffu));
     hi = cv((u16)(w >> 16));
   }
-  __device__ static __forceinline__ u32 pack(float lo, float hi) { return (u32)rc(lo) | ((u32)rc(hi) << 16); }
+  __device__ static __forceinline__ u32 pack(float lo, float hi) {
+    return DT == GM_DT_BF16 ? f2bf2(lo, hi) : ((u32)rc(lo) | ((u32)rc(hi) << 16));
+  }
   __device__ static __forceinline__ void ldg8(const void* p, float (&x)[8]) {
     u32 a, b, c, d;
     ldg16(p, a, b, c, d);
@@ -394,9 +403,12 @@ __device__ __forceinline__ void store_scalar(const OutDesc& o, double v) {
 }
 
 // ---------------------------------------------------------------------------
-// resident staging: the CTA's chunk of every resident input is bulk-copied
-// into shared memory in GM_MAX_PIECES pieces, one mbarrier per piece.
-// `es[k]` = element size of input k, `res[k]` = 1 if resident.
+// resident staging: the CTA's chunk of every staged input is bulk-copied into
+// shared memory at kernel start, in <= GM_MAX_PIECES pieces per group with one
+// mbarrier per piece.  Group 0 = inputs pass 0 reads (issued first, waited in
+// pass 0); group 1 = inputs first read by a later pass (prefetched behind pass
+// 0 and the grid barrier, waited in the first pass that reads them).
+// `grp[k]` is 0, 1, or -1 (input k streams from global memory).
 // ---------------------------------------------------------------------------
 struct Stage {
   u64* bars;        // [GM_MAX_PIECES] in static smem
@@ -405,35 +417,49 @@ struct Stage {
   int waited;       // pieces this thread has already waited for (in order)
 };
 
+__device__ __forceinline__ void stage_issue_group(const Params& P, unsigned char* smem, int nin, const int* es,
+                                                  const int* grp, int g, i64 v0, i64 v1, Stage& st) {
+  const i64 e_end_cta = (v1 * GM_VEC < P.n) ? v1 * GM_VEC : P.n;
+  for (int p = 0; p < st.npieces; ++p) {
+    const i64 pv0 = v0 + (i64)p * P.piece_vecs;
+    const i64 pv1 = (pv0 + P.piece_vecs < v1) ? pv0 + P.piece_vecs : v1;
+    const i64 e0 = pv0 * GM_VEC;
+    const i64 e1 = (pv1 * GM_VEC < e_end_cta) ? pv1 * GM_VEC : e_end_cta;
+    u32 tx = 0;
+    for (int k = 0; k < nin; ++k)
+      if (grp[k] == g) tx += (u32)((e1 - e0) * es[k]);
+    mbar_expect_tx(&st.bars[p], tx);
+    for (int k = 0; k < nin; ++k) {
+      if (grp[k] != g) continue;
+      const char* src = (const char*)P.in[k].ptr + e0 * es[k];
+      unsigned char* dst = smem + P.in[k].smem_off + (e0 - v0 * GM_VEC) * es[k];
+      bulk_g2s(dst, src, (u32)((e1 - e0) * es[k]), &st.bars[p]);
+    }
+  }
+}
+
 __device__ __forceinline__ void stage_issue(const Params& P, unsigned char* smem, int nin, const int* es,
-                                            const int* res, i64 v0, i64 v1, Stage& st) {
-  st.piece_vecs = P.piece_vecs;
+                                            const int* grp, i64 v0, i64 v1, Stage& a, Stage& b) {
   const i64 nv = v1 - v0;
-  st.npieces = nv > 0 ? (int)((nv + P.piece_vecs - 1) / P.piece_vecs) : 0;
-  st.waited = 0;
+  const int np = nv > 0 ? (int)((nv + P.piece_vecs - 1) / P.piece_vecs) : 0;
+  bool has[2] = {false, false};
+  for (int k = 0; k < nin; ++k)
+    if (grp[k] >= 0) has[grp[k]] = true;
+  Stage* st[2] = {&a, &b};
+  for (int g = 0; g < 2; ++g) {
+    st[g]->piece_vecs = P.piece_vecs;
+    st[g]->npieces = has[g] ? np : 0;
+    st[g]->waited = 0;
+  }
   if (threadIdx.x == 0) {
-    for (int p = 0; p < st.npieces; ++p) mbar_init(&st.bars[p], 1);
+    for (int g = 0; g < 2; ++g)
+      for (int p = 0; p < st[g]->npieces; ++p) mbar_init(&st[g]->bars[p], 1);
     mbar_fence_init();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const i64 e_end_cta = (v1 * GM_VEC < P.n) ? v1 * GM_VEC : P.n;
-    for (int p = 0; p < st.npieces; ++p) {
-      const i64 pv0 = v0 + (i64)p * P.piece_vecs;
-      const i64 pv1 = (pv0 + P.piece_vecs < v1) ? pv0 + P.piece_vecs : v1;
-      const i64 e0 = pv0 * GM_VEC;
-      const i64 e1 = (pv1 * GM_VEC < e_end_cta) ? pv1 * GM_VEC : e_end_cta;
-      u32 tx = 0;
-      for (int k = 0; k < nin; ++k)
-        if (res[k]) tx += (u32)((e1 - e0) * es[k]);
-      mbar_expect_tx(&st.bars[p], tx);
-      for (int k = 0; k < nin; ++k) {
-        if (!res[k]) continue;
-        const char* src = (const char*)P.in[k].ptr + e0 * es[k];
-        unsigned char* dst = smem + P.in[k].smem_off + (e0 - v0 * GM_VEC) * es[k];
-        bulk_g2s(dst, src, (u32)((e1 - e0) * es[k]), &st.bars[p]);
-      }
-    }
+    for (int g = 0; g < 2; ++g)
+      if (has[g]) stage_issue_group(P, smem, nin, es, grp, g, v0, v1, *st[g]);
   }
 }
 

@@ -127,18 +127,19 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
     gm_branch_select_f32_kernel(const __grid_constant__ gm::Params P, const __grid_constant__ BsArgs A) {
   using namespace gm;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ u64 s_bars[GM_MAX_PIECES];
+  __shared__ u64 s_bars[2 * GM_MAX_PIECES];
   __shared__ double s_warp[GM_WARPS * GM_MAX_RED];
   __shared__ double s_red[GM_MAX_RED];
   const i64 v0 = (i64)blockIdx.x * P.vpc;
   const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;
   const bool resident = P.in[0].smem_off >= 0;
   const u32 sres = resident ? smem_u32(smem + P.in[0].smem_off) : 0u;
-  Stage st;
+  Stage st, st_unused;
   st.bars = s_bars;
+  st_unused.bars = s_bars + GM_MAX_PIECES;
   const int es[1] = {4};
-  const int res[1] = {resident ? 1 : 0};
-  if (resident) stage_issue(P, smem, 1, es, res, v0, v1, st);
+  const int grp[1] = {resident ? 0 : -1};
+  if (resident) stage_issue(P, smem, 1, es, grp, v0, v1, st, st_unused);
   const int op = (A.red == 2) ? GM_R_MAX : (A.red == 3) ? GM_R_MIN : GM_R_SUM;
   // pass 0: statistic of x
   float acc = acc_identity(op);

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _native as nat
-from .codegen import DT_SIZE, MODE_FULL, MODE_PERIODIC, MODE_SCALAR, MODE_STRIDED, UNROLL, Plan
+from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
 from .ir import Graph, Node, Unsupported
 
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
@@ -76,12 +76,12 @@ class _Spec:
                 raise nat.NativeError(f"region {region.name}: resident plan does not fit ({smem} B smem)")
         elif plan.reductions:
             occ = max(1, self.kernel.occupancy(threads, 0))
-            grid = max(1, min(sms * occ, -(-nvec // (threads * UNROLL)) if nvec else 1))
+            grid = max(1, min(sms * occ, -(-nvec // (threads * plan.unroll)) if nvec else 1))
             vpc = -(-nvec // grid) if nvec else 0
             smem = 0
         else:
             # pure map: no grid barrier, any grid size
-            per_cta = threads * UNROLL * 4
+            per_cta = threads * plan.unroll * 4
             grid = max(1, -(-nvec // per_cta)) if nvec else 1
             vpc = -(-nvec // grid) if nvec else 0
             smem = 0

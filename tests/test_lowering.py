@@ -111,5 +111,6 @@ def test_uniform_select_guards_untaken_arm(programs):
     i = src.index("// ---- pass 1")
     j = src.index("P.in[1]", i)
     assert "if ((!sb" in src[i:j]
-    # q is read by both passes and is staged in shared memory once
-    assert plan.resident_flags[0] and not plan.resident_flags[1]
+    # q is read by both passes: staged once, waited in pass 0 (group 0);
+    # hidden is read once by pass 1: prefetched behind pass 0 (group 1)
+    assert plan.stage_group == [0, 1]
