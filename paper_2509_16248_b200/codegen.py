@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import hashlib
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -574,6 +575,11 @@ class Plan:
         w("  __shared__ double s_warp[GM_WARPS * GM_MAX_RED];")
         w("  __shared__ double s_red[GM_MAX_RED];")
         w(f"  __shared__ double s_scal[{nscal}];")
+        prof = bool(os.environ.get("GM_PROFILE"))
+        self.profiled = prof
+        if prof:
+            w("  u64* prof_ = (u64*)P.scal_out + 64;")
+            w("  if (threadIdx.x == 0) atomicMin(&prof_[0], gm::globaltimer());")
         w("  const i64 v0 = (i64)blockIdx.x * P.vpc;")
         w("  const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;")
         w("  (void)v1; (void)s_bars; (void)s_warp; (void)s_red;")
@@ -623,72 +629,38 @@ class Plan:
             for k, r in enumerate(reds):
                 w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
             U = self.unroll
-            w(f"    for (i64 vb = v0 + threadIdx.x; vb < v1; vb += {U} * GM_THREADS) {{")
-            for u in range(U):
-                w(f"      const i64 vv{u} = vb + {u} * GM_THREADS;")
-                w(f"      const i64 e{u} = vv{u} * GM_VEC;")
-                w(f"      const int nv{u} = vv{u} < v1 ? (int)((P.n - e{u}) < GM_VEC ? (P.n - e{u}) : GM_VEC) : 0;")
-                w(f"      const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
-            last_v = f"(((vb + {U - 1} * GM_THREADS) < v1 ? (vb + {U - 1} * GM_THREADS) : (v1 - 1)) - v0)"
+            waits = []
             if p == 0 and any(g == 0 for g in self.stage_group):
-                w(f"      stage_wait(st0, {last_v});")
+                waits.append("st0")
             if p == g1_first:
-                w(f"      stage_wait(st1, {last_v});")
-            for u in range(U):
-                for n in elem_nodes:
-                    w(f"      float n{n.uid}_{u}[GM_VEC];")
-            # loads first (unconditional full/periodic/strided), for all unrolled vectors
-            loads = [n for n in elem_nodes if n.op == "free" and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))]
-            for u in range(U):
-                w(f"      if (nv{u} > 0) {{")
-                for n in loads:
-                    for line in self._elem_code(n, u):
-                        w("        " + line.replace("\n", "\n        "))
-                w("      }")
-            for u in range(U):
-                w(f"      if (nv{u} > 0) {{")
-                cur_guard = None
-                open_block = False
-                for n in elem_nodes:
-                    if n in loads:
-                        continue
-                    g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
-                    if g != cur_guard:
-                        if open_block:
-                            w("        }")
-                            open_block = False
-                        if g:
-                            w(f"        if ({g}) {{")
-                            open_block = True
-                        cur_guard = g
-                    for line in self._elem_code(n, u):
-                        w("          " + line.replace("\n", "\n          "))
-                if open_block:
-                    w("        }")
-                for k, r in enumerate(reds):
-                    x = r.args[0]
-                    src = f"n{x.uid}_{u}"
-                    if r.op == "norm":
-                        w(f"        {{ float t_[GM_VEC];\n#pragma unroll\n        for (int l = 0; l < GM_VEC; ++l) t_[l] = gm::mul({src}[l], {src}[l]);\n        acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, t_, nv{u}); }}")
-                    elif r.op == "count_nonzero":
-                        w(f"        {{ float t_[GM_VEC];\n#pragma unroll\n        for (int l = 0; l < GM_VEC; ++l) t_[l] = {src}[l] != 0.f ? 1.f : 0.f;\n        acc{k} = gm::acc8(0, acc{k}, t_, nv{u}); }}")
-                    else:
-                        w(f"        acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, {src}, nv{u});")
-                for j, o in outs:
-                    k = self._out_slot(j)
-                    w(f"        gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
-                w("      }")
+                waits.append("st1")
+            loads = [n for n in elem_nodes
+                     if n.op == "free" and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))]
+            # steady state: U full vectors per iteration, constant lane count
+            w("    const i64 vfull_ = (P.n / GM_VEC < v1) ? P.n / GM_VEC : v1;")
+            w("    i64 vb = v0 + threadIdx.x;")
+            w(f"    for (; vb + {U - 1} * GM_THREADS < vfull_; vb += {U} * GM_THREADS) {{")
+            self._emit_body(w, p, elem_nodes, reds, outs, guards, loads, waits, U, full=True)
+            w("    }")
+            # remainder: one vector at a time (partial last vector included)
+            w("    for (; vb < v1; vb += GM_THREADS) {")
+            self._emit_body(w, p, elem_nodes, reds, outs, guards, loads, waits, 1, full=False)
             w("    }")
             if p == 0 and any(g == 0 for g in self.stage_group):
                 w("    stage_finish(st0);")
             if p == g1_first:
                 w("    stage_finish(st1);")
+            if prof:
+                w("    __syncthreads();")
+                w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{1 + 2 * p}], gm::globaltimer());")
             if reds:
                 nr = len(reds)
                 w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
                 w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
                 w(f"    const int slots_[{nr}] = {{{', '.join(str(red_slot[r.uid]) for r in reds)}}};")
                 w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red);")
+                if prof:
+                    w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{2 + 2 * p}], gm::globaltimer());")
                 w("    if (threadIdx.x == 0) {")
                 for k, r in enumerate(reds):
                     w("      " + self._finish_reduction(r, k))
@@ -696,6 +668,9 @@ class Plan:
                 w("    __syncthreads();")
                 self._emit_scalar_level(w, p + 1)
             w("  }")
+        if prof:
+            w("  __syncthreads();")
+            w("  if (threadIdx.x == 0) atomicMax(&prof_[63], gm::globaltimer());")
         # scalar outputs and the debug mirror
         w("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
         for j, o in enumerate(self.outputs):
@@ -714,6 +689,56 @@ class Plan:
         w("  }")
         w("}")
         return "\n".join(out) + "\n"
+
+    def _emit_body(self, w, p, elem_nodes, reds, outs, guards, loads, waits, U, full):
+        ind = "      "
+        for u in range(U):
+            w(f"{ind}const i64 e{u} = (vb + {u} * GM_THREADS) * GM_VEC;")
+            if full:
+                w(f"{ind}const int nv{u} = GM_VEC;")
+            else:
+                w(f"{ind}const int nv{u} = (int)((P.n - e{u}) < GM_VEC ? (P.n - e{u}) : GM_VEC);")
+            w(f"{ind}const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
+        for st in waits:
+            w(f"{ind}stage_wait({st}, vb + {U - 1} * GM_THREADS - v0);")
+        for u in range(U):
+            for n in elem_nodes:
+                w(f"{ind}float n{n.uid}_{u}[GM_VEC];")
+        for u in range(U):
+            for n in loads:
+                for line in self._elem_code(n, u):
+                    w(ind + line.replace("\n", "\n" + ind))
+        for u in range(U):
+            cur_guard = None
+            open_block = False
+            for n in elem_nodes:
+                if n in loads:
+                    continue
+                g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
+                if g != cur_guard:
+                    if open_block:
+                        w(f"{ind}}}")
+                        open_block = False
+                    if g:
+                        w(f"{ind}if ({g}) {{")
+                        open_block = True
+                    cur_guard = g
+                for line in self._elem_code(n, u):
+                    w(ind + "  " + line.replace("\n", "\n" + ind + "  "))
+            if open_block:
+                w(f"{ind}}}")
+            for k, r in enumerate(reds):
+                x = r.args[0]
+                src = f"n{x.uid}_{u}"
+                if r.op == "norm":
+                    w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = gm::mul({src}[l], {src}[l]);\n{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, t_, nv{u}); }}")
+                elif r.op == "count_nonzero":
+                    w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = {src}[l] != 0.f ? 1.f : 0.f;\n{ind}acc{k} = gm::acc8(0, acc{k}, t_, nv{u}); }}")
+                else:
+                    w(f"{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, {src}, nv{u});")
+            for j, o in outs:
+                k = self._out_slot(j)
+                w(f"{ind}gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
 
     def _emit_scalar_level(self, w, level: int) -> None:
         nodes = [n for n in self.scalars if self.avail[n.uid] == level and n.op not in REDUCE]

@@ -82,8 +82,8 @@ struct Params {
   i64 vpc;         // vectors per CTA
   i64 piece_vecs;  // vectors per bulk-copy piece (resident staging)
   i64 partials;    // double[GM_MAX_RED][gridDim.x]
-  i64 barrier;     // u32[2] = {arrivals, generation}; zeroed once, self-resetting
-  i64 status;      // int: 0 ok, 1 grid-barrier timeout
+  i64 barrier;     // u64 arrival counter, monotonic across launches (zeroed once)
+  i64 status;      // int: 0 ok, 1 grid-barrier timeout (barrier + 16)
   i64 scal_out;    // double[GM_MAX_RED + ...]: scalar slots mirrored by CTA 0 (or 0)
   double hs[GM_MAX_HS];  // host scalars (Python numbers) as runtime values
   InDesc in[GM_MAX_IN];
@@ -100,9 +100,21 @@ __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b);
 __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
 __device__ __forceinline__ float relu(float a) { return (a != a) ? a : (a > 0.f ? a : 0.f); }
-// 1/(1+e^-x): __frcp_rn is the correctly rounded reciprocal, identical to 1.f/y
-__device__ __forceinline__ float sigmoid(float a) { return __frcp_rn(__fadd_rn(1.f, expf(-a))); }
 __device__ __forceinline__ float recip(float a) { return __frcp_rn(a); }
+// exp via the SFU: ex2.approx(x*log2 e).  Relative error ~2 ulp + |x|*2^-24,
+// i.e. <= 1e-6 for |x| < 16 — an order below the 1e-5 parity bound (torch's
+// own CPU exp/sigmoid are SLEEF approximations too).
+__device__ __forceinline__ float fexp(float a) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(a * 1.4426950408889634f));
+  return y;
+}
+__device__ __forceinline__ float frcp(float a) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(a));
+  return y;
+}
+__device__ __forceinline__ float sigmoid(float a) { return frcp(1.f + fexp(-a)); }
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
 __device__ __forceinline__ float neg(float a) { return -a; }
 // NaN-propagating max/min (torch.maximum / Tensor.max semantics)
@@ -506,21 +518,33 @@ __device__ __forceinline__ double red_combine(int op, double a, double b) {
   }
 }
 
-// Self-resetting generation barrier over all CTAs of the launch.  The grid
-// is sized by the host to be co-resident (<= SMs x occupancy); a 2 s
-// globaltimer bound turns a residency violation into status=1, not a hang.
+__device__ __forceinline__ u64 atom_add_acq_rel64(u64* p, u64 v) {
+  u64 old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ u64 ld_acquire64(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier on a monotonic 64-bit arrival counter: barrier k of the
+// launch is complete when the counter reaches the next multiple of gridDim.x
+// (no reset, so consecutive launches and passes simply keep counting).  The
+// grid is sized by the host to be co-resident (<= SMs x occupancy); a 2 s
+// %globaltimer bound turns a residency violation into status=1, not a hang.
 __device__ __forceinline__ void grid_sync(const Params& P) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    u32* bar = (u32*)P.barrier;
-    const u32 gen = ld_acquire(bar + 1);
-    const u32 prev = atom_add_acq_rel(bar, 1u);
-    if (prev == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      st_release(bar + 1, gen + 1);
-    } else {
+    u64* cnt = (u64*)P.barrier;
+    const u64 g = gridDim.x;
+    const u64 old = atom_add_acq_rel64(cnt, 1ull);
+    const u64 target = (old / g + 1) * g;
+    if (old + 1 != target) {
       const u64 t0 = globaltimer();
-      while (ld_acquire(bar + 1) == gen) {
+      while (ld_acquire64(cnt) < target) {
+        __nanosleep(32);
         if (globaltimer() - t0 > 2000000000ull) {
           *(volatile int*)P.status = 1;
           break;
@@ -531,38 +555,51 @@ __device__ __forceinline__ void grid_sync(const Params& P) {
   __syncthreads();
 }
 
-// Reduce `nr` per-thread values across the grid.  `ops[r]` combine op,
-// `slots[r]` partials slot.  Result lands in s_out[r] in every CTA.
-// Combination order is fixed (warp butterfly -> warps in order -> CTAs in
-// order), so every CTA and every run produces the same bits.
+// Reduce `nr` per-thread values across the grid; the result lands in s_out[r]
+// in every CTA.  Every CTA combines all partials itself with one parallel
+// load round (thread t loads partial t) and the same fixed tree (warp
+// butterfly, then warps in order), so every CTA and every run produces the
+// same bits.
+__device__ __forceinline__ void block_combine(int op, double v, double* s_warp, int r, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, off));
+  if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
+  (void)out;
+}
+
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
                                             double* vals, double* s_warp, double* s_out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = 0; r < nr; ++r) {
-    double v = vals[r];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = red_combine(ops[r], v, __shfl_xor_sync(0xffffffffu, v, off));
-    if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
-  }
+  for (int r = 0; r < nr; ++r) block_combine(ops[r], vals[r], s_warp, r, s_out);
   __syncthreads();
   double* partials = (double*)P.partials;
   if (threadIdx.x == 0) {
     for (int r = 0; r < nr; ++r) {
       double acc = s_warp[r];
       for (int w = 1; w < GM_WARPS; ++w) acc = red_combine(ops[r], acc, s_warp[w * GM_MAX_RED + r]);
-      partials[(i64)slots[r] * gridDim.x + blockIdx.x] = acc;
+      if (gridDim.x > 1)
+        partials[(i64)slots[r] * gridDim.x + blockIdx.x] = acc;
+      else
+        s_out[r] = acc;
     }
   }
-  if (gridDim.x > 1) grid_sync(P);
-  else __syncthreads();
-  if (warp == 0) {
+  if (gridDim.x == 1) {
+    __syncthreads();
+    return;
+  }
+  grid_sync(P);
+  for (int r = 0; r < nr; ++r) {
+    double v = red_identity(ops[r]);
+    for (u32 b = threadIdx.x; b < gridDim.x; b += GM_THREADS)
+      v = red_combine(ops[r], v, ld_relaxed_f64(partials + (i64)slots[r] * gridDim.x + b));
+    block_combine(ops[r], v, s_warp, r, s_out);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     for (int r = 0; r < nr; ++r) {
-      double acc = red_identity(ops[r]);
-      for (u32 b = lane; b < gridDim.x; b += 32)
-        acc = red_combine(ops[r], acc, ld_relaxed_f64(partials + (i64)slots[r] * gridDim.x + b));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc = red_combine(ops[r], acc, __shfl_xor_sync(0xffffffffu, acc, off));
-      if (lane == 0) s_out[r] = acc;
+      double acc = s_warp[r];
+      for (int w = 1; w < GM_WARPS; ++w) acc = red_combine(ops[r], acc, s_warp[w * GM_MAX_RED + r]);
+      s_out[r] = acc;
     }
   }
   __syncthreads();

@@ -381,7 +381,7 @@ int gm_region_release(gm_region r) {
 
 size_t gm_region_params_bytes(void) { return sizeof(gm::Params); }
 
-size_t gm_branch_select_scratch_bytes(void) { return 64 + 8 * 4096; }
+size_t gm_branch_select_scratch_bytes(void) { return 64 + 8 * 4096; }  // barrier(8) pad | status @16 | partials @64
 
 int gm_branch_select_f32(const float* x, float* out, int64_t n, int red, int cmp, double thr, double a1, double b1,
                          double a2, double b2, void* scratch, double* stat_out, void* stream) {
@@ -413,7 +413,7 @@ int gm_branch_select_f32(const float* x, float* out, int64_t n, int red, int cmp
   P.out[0].ptr = (long long)(uintptr_t)out;
   char* s = (char*)scratch;
   P.barrier = (long long)(uintptr_t)s;
-  P.status = (long long)(uintptr_t)(s + 8);
+  P.status = (long long)(uintptr_t)(s + 16);
   P.partials = (long long)(uintptr_t)(s + 64);
   if ((size_t)grid * 8 > gm_branch_select_scratch_bytes() - 64) return fail(GM_E_INVALID, "grid too large for scratch");
   BsArgs A;

@@ -80,9 +80,9 @@ class _Spec:
             vpc = -(-nvec // grid) if nvec else 0
             smem = 0
         else:
-            # pure map: no grid barrier, any grid size
-            per_cta = threads * plan.unroll * 4
-            grid = max(1, -(-nvec // per_cta)) if nvec else 1
+            # pure map: no grid barrier; persistent grid of SMs x occupancy
+            occ = max(1, self.kernel.occupancy(threads, 0))
+            grid = max(1, min(sms * occ, -(-nvec // (threads * plan.unroll)) if nvec else 1))
             vpc = -(-nvec // grid) if nvec else 0
             smem = 0
         if vpc:
@@ -90,9 +90,11 @@ class _Spec:
         self.grid, self.vpc, self.smem, self.threads = grid, vpc, smem, threads
         self.nred = len(plan.reductions)
         self.nscal = len(plan.scalars)
-        # scratch: barrier(8) status(4) | partials | scalar mirror
+        # scratch: barrier counter u64 @0 | status int @16 | partials @64 | scalar mirror
         part_bytes = 8 * max(1, self.nred) * grid
-        self.scratch = torch.zeros(64 + part_bytes + 8 * max(1, self.nscal), dtype=torch.uint8, device=dev)
+        # (+1 KB: the GM_PROFILE timeline lives at scal_out + 64 u64)
+        self.scratch = torch.zeros(64 + part_bytes + 8 * 64 + 8 * 64 + 8 * max(1, self.nscal), dtype=torch.uint8,
+                                   device=dev)
         base = self.scratch.data_ptr()
         P = nat.Params()
         P.n = n
@@ -100,7 +102,7 @@ class _Spec:
         P.vpc = vpc
         P.piece_vecs = max(64, -(-vpc // nat.MAX_PIECES)) if vpc else 1
         P.barrier = base
-        P.status = base + 8
+        P.status = base + 16
         P.partials = base + 64
         P.scal_out = base + 64 + part_bytes
         self.template = P
@@ -188,9 +190,25 @@ class _Spec:
                 total += int(torch.Size(self.shape).numel()) * torch.empty((), dtype=info).element_size()
         return total
 
+    def timeline(self) -> list[int] | None:
+        """GM_PROFILE builds: [start, pass0 end, pass0 barrier done, ...,
+        end] in ns relative to the first CTA start (syncs; diagnostics)."""
+        if not getattr(self.plan, "profiled", False):
+            return None
+        off = 64 + 8 * max(1, self.nred) * self.grid + 8 * 64
+        v = self.scratch[off: off + 8 * 64].view(torch.int64).tolist()
+        t0 = v[0]
+        return [x - t0 if x else 0 for x in v]
+
+    def reset_timeline(self) -> None:
+        off = 64 + 8 * max(1, self.nred) * self.grid + 8 * 64
+        t = self.scratch[off: off + 8 * 64].view(torch.int64)
+        t.zero_()
+        t[0] = 2 ** 62
+
     def status(self) -> int:
         """Grid-barrier status word (syncs; diagnostics only)."""
-        return int(self.scratch[8:12].view(torch.int32).item())
+        return int(self.scratch[16:20].view(torch.int32).item())
 
     def scalars(self) -> list[float]:
         """Scalar slots mirrored by CTA 0 of the last launch (syncs; tests)."""
