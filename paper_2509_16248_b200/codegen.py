@@ -353,7 +353,9 @@ class Plan:
             dt = DT_CODE[ip.dtype]
             k = ip.slot
             if ip.mode == MODE_FULL:
-                return [f"gm::load8<{dt}>(P.in[{k}], sres{k}, e{u}, le{u}, nv{u}, n{node.uid}_{u});"]
+                if ip.resident:
+                    return [f"gm::load8_smem<{dt}>(sres{k}, le{u}, nv{u}, n{node.uid}_{u});"]
+                return [f"gm::load8_gmem<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
             if ip.mode == MODE_PERIODIC:
                 return [f"gm::load8_periodic<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
             if ip.mode == MODE_STRIDED:
@@ -586,6 +588,7 @@ class Plan:
         any_res = any(resident)
         w("  Stage st0, st1; st0.bars = s_bars; st1.bars = s_bars + GM_MAX_PIECES;")
         w("  st0.waited = st1.waited = 0; st0.npieces = st1.npieces = 0; st0.piece_vecs = st1.piece_vecs = 1;")
+        w("  st0.wend = st1.wend = 0;")
         if any_res:
             es = ", ".join(str(DT_SIZE[ip.dtype]) for ip in self.inputs)
             gs = ", ".join(str(g) for g in self.stage_group)

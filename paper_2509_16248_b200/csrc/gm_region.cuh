@@ -356,6 +356,30 @@ __device__ __forceinline__ void load8(const InDesc& d, u32 sres, i64 e, i64 le, 
   }
 }
 
+// Staged (shared-memory resident) input: `sres` + local element `le`.
+template <int DT>
+__device__ __forceinline__ void load8_smem(u32 sres, i64 le, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  if (nv == GM_VEC) {
+    E::lds8(sres + (u32)(le * E::ES), x);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::lds1(sres + (u32)((le + k) * E::ES)) : 0.f;
+  }
+}
+
+// Streamed input from global memory (128-bit ld.global.nc).
+template <int DT>
+__device__ __forceinline__ void load8_gmem(const InDesc& d, i64 e, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  if (nv == GM_VEC) {
+    E::ldg8((const char*)d.ptr + e * E::ES, x);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, e + k) : 0.f;
+  }
+}
+
 // Broadcast / strided input: element offsets decoded from the iteration index.
 template <int DT>
 __device__ __forceinline__ void load8_strided(const InDesc& d, i64 e, int nv, float (&x)[8]) {
@@ -427,6 +451,7 @@ struct Stage {
   int npieces;
   i64 piece_vecs;
   int waited;       // pieces this thread has already waited for (in order)
+  i64 wend;         // = waited * piece_vecs
 };
 
 __device__ __forceinline__ void stage_issue_group(const Params& P, unsigned char* smem, int nin, const int* es,
@@ -462,6 +487,7 @@ __device__ __forceinline__ void stage_issue(const Params& P, unsigned char* smem
     st[g]->piece_vecs = P.piece_vecs;
     st[g]->npieces = has[g] ? np : 0;
     st[g]->waited = 0;
+    st[g]->wend = 0;
   }
   if (threadIdx.x == 0) {
     for (int g = 0; g < 2; ++g)
@@ -475,12 +501,13 @@ __device__ __forceinline__ void stage_issue(const Params& P, unsigned char* smem
   }
 }
 
-// Wait (once, in order) for the piece holding local vector `lv`.
+// Wait (once, in order) for the piece holding local vector `lv` — no
+// division on the hot path: `waited` pieces cover local vectors < wend.
 __device__ __forceinline__ void stage_wait(Stage& st, i64 lv) {
-  const int p = (int)(lv / st.piece_vecs);
-  while (st.waited <= p) {
+  while (st.wend <= lv && st.waited < st.npieces) {
     mbar_wait(&st.bars[st.waited], 0);
     ++st.waited;
+    st.wend += st.piece_vecs;
   }
 }
 

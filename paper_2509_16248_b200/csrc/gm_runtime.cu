@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   const bool resident = P.in[0].smem_off >= 0;
   const u32 sres = resident ? smem_u32(smem + P.in[0].smem_off) : 0u;
   Stage st, st_unused;
+  st.wend = st_unused.wend = 0;
   st.bars = s_bars;
   st_unused.bars = s_bars + GM_MAX_PIECES;
   const int es[1] = {4};
