@@ -353,8 +353,11 @@ class Plan:
             dt = DT_CODE[ip.dtype]
             k = ip.slot
             if ip.mode == MODE_FULL:
-                if ip.resident:
-                    return [f"gm::load8_smem<{dt}>(sres{k}, le{u}, nv{u}, n{node.uid}_{u});"]
+                g = self.stage_group[k]
+                if g == 0 and self._cur_pass == 0:
+                    return [f"gm::load8_stash<{dt}>(P.in[{k}], sres{k}, e{u}, le{u}, nv{u}, n{node.uid}_{u});"]
+                if g >= 0:
+                    return [f"gm::load8_res<{dt}>(P.in[{k}], sres{k}, e{u}, le{u}, nv{u}, n{node.uid}_{u});"]
                 return [f"gm::load8_gmem<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
             if ip.mode == MODE_PERIODIC:
                 return [f"gm::load8_periodic<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
@@ -573,7 +576,7 @@ class Plan:
         w("GM_KERNEL_NAME(const __grid_constant__ gm::Params P) {")
         w("  using namespace gm;")
         w("  extern __shared__ __align__(128) unsigned char smem[];")
-        w("  __shared__ u64 s_bars[2 * GM_MAX_PIECES];")
+
         w("  __shared__ double s_warp[GM_WARPS * GM_MAX_RED];")
         w("  __shared__ double s_red[GM_MAX_RED];")
         w(f"  __shared__ double s_scal[{nscal}];")
@@ -584,22 +587,20 @@ class Plan:
             w("  if (threadIdx.x == 0) atomicMin(&prof_[0], gm::globaltimer());")
         w("  const i64 v0 = (i64)blockIdx.x * P.vpc;")
         w("  const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;")
-        w("  (void)v1; (void)s_bars; (void)s_warp; (void)s_red;")
+        w("  (void)v1; (void)s_warp; (void)s_red;")
         any_res = any(resident)
-        w("  Stage st0, st1; st0.bars = s_bars; st1.bars = s_bars + GM_MAX_PIECES;")
-        w("  st0.waited = st1.waited = 0; st0.npieces = st1.npieces = 0; st0.piece_vecs = st1.piece_vecs = 1;")
-        w("  st0.wend = st1.wend = 0;")
-        if any_res:
-            es = ", ".join(str(DT_SIZE[ip.dtype]) for ip in self.inputs)
-            gs = ", ".join(str(g) for g in self.stage_group)
-            w(f"  const int es_[{len(self.inputs)}] = {{{es}}};")
-            w(f"  const int grp_[{len(self.inputs)}] = {{{gs}}};")
-            w(f"  stage_issue(P, smem, {len(self.inputs)}, es_, grp_, v0, v1, st0, st1);")
+
+        any_res = any(resident)
         # first pass that reads a group-1 (prefetched) input
         g1_first = min([min(ip.passes) for ip in self.inputs if self.stage_group[ip.slot] == 1] or [-1])
         for ip, r in zip(self.inputs, resident):
             if ip.mode == MODE_FULL:
                 w(f"  const u32 sres{ip.slot} = {'smem_u32(smem + P.in[%d].smem_off)' % ip.slot if r else '0u'};")
+        for ip in self.inputs:
+            if self.stage_group[ip.slot] == 1:
+                w(f"  gm::prefetch_thread<{DT_CODE[ip.dtype]}>(P, P.in[{ip.slot}], sres{ip.slot}, v0, v1);")
+        if any(g == 1 for g in self.stage_group):
+            w("  gm::cp_async_commit();")
         # level-0 scalars
         self._emit_scalar_level(w, 0)
         red_slot = {r.uid: i for i, r in enumerate(self.reductions)}
@@ -632,11 +633,10 @@ class Plan:
             for k, r in enumerate(reds):
                 w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
             U = self.unroll
+            self._cur_pass = p
             waits = []
-            if p == 0 and any(g == 0 for g in self.stage_group):
-                waits.append("st0")
             if p == g1_first:
-                waits.append("st1")
+                w("    gm::cp_async_wait_all();  // this thread's prefetched stash slots")
             loads = [n for n in elem_nodes
                      if n.op == "free" and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))]
             # steady state: U full vectors per iteration, constant lane count
@@ -649,10 +649,7 @@ class Plan:
             w("    for (; vb < v1; vb += GM_THREADS) {")
             self._emit_body(w, p, elem_nodes, reds, outs, guards, loads, waits, 1, full=False)
             w("    }")
-            if p == 0 and any(g == 0 for g in self.stage_group):
-                w("    stage_finish(st0);")
-            if p == g1_first:
-                w("    stage_finish(st1);")
+
             if prof:
                 w("    __syncthreads();")
                 w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{1 + 2 * p}], gm::globaltimer());")
@@ -786,13 +783,13 @@ class Plan:
         self.stage_group = [-1] * len(self.inputs)
         flags = [False] * len(self.inputs)
         self.resident_flags = flags
-        if not self.reductions or not nvec:
+        if not self.reductions or not nvec or os.environ.get("GM_STAGING", "1") == "0":
             return flags
         stageable = [ip for ip in self.inputs
                      if ip.mode == MODE_FULL and ip.passes and DT_SIZE[ip.dtype] >= 2
                      and (self.n * DT_SIZE[ip.dtype]) % 16 == 0]
         multi = [ip for ip in stageable if len(ip.passes) >= 2]
-        first0 = [ip for ip in stageable if len(ip.passes) < 2 and 0 in ip.passes]
+        first0 = []  # read by pass 0 only: streaming is optimal, nothing to stash
         later = [ip for ip in stageable if len(ip.passes) < 2 and 0 not in ip.passes]
         per_sm = 233472  # B200 shared memory per SM (228 KB)
         for minb in (2, 1):

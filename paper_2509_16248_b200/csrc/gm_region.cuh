@@ -380,6 +380,73 @@ __device__ __forceinline__ void load8_gmem(const InDesc& d, i64 e, int nv, float
   }
 }
 
+// ---------------------------------------------------------------------------
+// thread-private staging.  Every pass maps local vector lv to thread
+// lv % GM_THREADS, so a thread only ever re-reads the stash slots it wrote:
+// no mbarrier, no __syncthreads.  Pass 0 streams an input it re-reads later
+// with 128-bit loads and stores the raw vector to shared memory on the way
+// (load8_stash); an input first read by a later pass is prefetched at kernel
+// start with cp.async (LDGSTS) and waited per thread (cp_async_wait_all).
+// The one partial tail vector of a tensor always reads global memory.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sts16(u32 s, u32 a, u32 b, u32 c, u32 d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(s), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void cp_async16(u32 s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int DT>
+__device__ __forceinline__ void load8_stash(const InDesc& d, u32 sres, i64 e, i64 le, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  if (nv != GM_VEC) {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, e + k) : 0.f;
+    return;
+  }
+  const char* g = (const char*)d.ptr + e * E::ES;
+  const u32 s = sres + (u32)(le * E::ES);
+  u32 a, b, c, w;
+  ldg16(g, a, b, c, w);
+  sts16(s, a, b, c, w);
+  if (E::ES == 4) {
+    u32 a2, b2, c2, w2;
+    ldg16(g + 16, a2, b2, c2, w2);
+    sts16(s + 16, a2, b2, c2, w2);
+    x[0] = __uint_as_float(a); x[1] = __uint_as_float(b); x[2] = __uint_as_float(c); x[3] = __uint_as_float(w);
+    x[4] = __uint_as_float(a2); x[5] = __uint_as_float(b2); x[6] = __uint_as_float(c2); x[7] = __uint_as_float(w2);
+  } else {
+    E::lds8(s, x);  // (re-read the stored vector: same thread, cheap; keeps one code path)
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void load8_res(const InDesc& d, u32 sres, i64 e, i64 le, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  if (nv == GM_VEC) {
+    E::lds8(sres + (u32)(le * E::ES), x);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, e + k) : 0.f;
+  }
+}
+
+// Prefetch this thread's full vectors of one input into its stash slots.
+template <int DT>
+__device__ __forceinline__ void prefetch_thread(const Params& P, const InDesc& d, u32 sres, i64 v0, i64 v1) {
+  typedef Elem<DT> E;
+  const i64 vfull = (P.n / GM_VEC < v1) ? P.n / GM_VEC : v1;
+  for (i64 v = v0 + threadIdx.x; v < vfull; v += GM_THREADS) {
+    const i64 e = v * GM_VEC, le = e - v0 * GM_VEC;
+    const char* g = (const char*)d.ptr + e * E::ES;
+    const u32 s = sres + (u32)(le * E::ES);
+#pragma unroll
+    for (int b = 0; b < GM_VEC * E::ES; b += 16) cp_async16(s + b, g + b);
+  }
+}
+
 // Broadcast / strided input: element offsets decoded from the iteration index.
 template <int DT>
 __device__ __forceinline__ void load8_strided(const InDesc& d, i64 e, int nv, float (&x)[8]) {

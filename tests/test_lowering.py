@@ -109,7 +109,8 @@ def test_uniform_select_guards_untaken_arm(programs):
     assert plan.npass == 2 and len(plan.reductions) == 1
     src = plan.source
     i = src.index("// ---- pass 1")
-    j = src.index("P.in[1]", i)
+    key = "sres1" if plan.stage_group[1] >= 0 else "P.in[1]"
+    j = src.index(key + ",", i) if key == "sres1" else src.index(key, i)
     assert "if ((!sb" in src[i:j]
     # q is read by both passes: staged once, waited in pass 0 (group 0);
     # hidden is read once by pass 1: prefetched behind pass 0 (group 1)
