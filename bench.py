@@ -292,7 +292,10 @@ def main():
     d2h = out_host.numel() * out_host.element_size()
 
     n_region_launch = len(fused)
-    gpu_launches = args.steps * (n_region_launch + 1)  # fused regions + log-ring commit per step
+    tmpl = getattr(entry, "template", None)
+    g = tmpl.gathers if tmpl is not None else 0
+    # our kernels per step: fused regions + log-ring gathers (+ slot commit when any)
+    gpu_launches = args.steps * (n_region_launch + g + (1 if g else 0))
     line = {
         "metric": METRIC,
         "value": value,

@@ -637,8 +637,9 @@ __device__ __forceinline__ void grid_sync(const Params& P) {
     const u64 target = (old / g + 1) * g;
     if (old + 1 != target) {
       const u64 t0 = globaltimer();
+      int spins = 0;
       while (ld_acquire64(cnt) < target) {
-        __nanosleep(32);
+        if (++spins > 64) __nanosleep(32);
         if (globaltimer() - t0 > 2000000000ull) {
           *(volatile int*)P.status = 1;
           break;
@@ -650,31 +651,36 @@ __device__ __forceinline__ void grid_sync(const Params& P) {
 }
 
 // Reduce `nr` per-thread values across the grid; the result lands in s_out[r]
-// in every CTA.  Every CTA combines all partials itself with one parallel
-// load round (thread t loads partial t) and the same fixed tree (warp
-// butterfly, then warps in order), so every CTA and every run produces the
-// same bits.
-__device__ __forceinline__ void block_combine(int op, double v, double* s_warp, int r, double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// in every CTA.  Both combine stages run in warp 0 with independent loads
+// (no serial chains of dependent loads): warp values of the CTA, then, after
+// the grid barrier, all CTA partials (8 in flight per lane per round).  The
+// tree is the same in every CTA and every run, so every CTA and every run
+// produces the same bits.
+__device__ __forceinline__ double warp_combine(int op, double v) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, off));
-  if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
-  (void)out;
+  return v;
 }
 
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
                                             double* vals, double* s_warp, double* s_out) {
-  for (int r = 0; r < nr; ++r) block_combine(ops[r], vals[r], s_warp, r, s_out);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = 0; r < nr; ++r) {
+    const double v = warp_combine(ops[r], vals[r]);
+    if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
+  }
   __syncthreads();
   double* partials = (double*)P.partials;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     for (int r = 0; r < nr; ++r) {
-      double acc = s_warp[r];
-      for (int w = 1; w < GM_WARPS; ++w) acc = red_combine(ops[r], acc, s_warp[w * GM_MAX_RED + r]);
-      if (gridDim.x > 1)
-        partials[(i64)slots[r] * gridDim.x + blockIdx.x] = acc;
-      else
-        s_out[r] = acc;
+      double v = lane < GM_WARPS ? s_warp[lane * GM_MAX_RED + r] : red_identity(ops[r]);
+      v = warp_combine(ops[r], v);
+      if (lane == 0) {
+        if (gridDim.x > 1)
+          partials[(i64)slots[r] * gridDim.x + blockIdx.x] = v;
+        else
+          s_out[r] = v;
+      }
     }
   }
   if (gridDim.x == 1) {
@@ -682,18 +688,22 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
     return;
   }
   grid_sync(P);
-  for (int r = 0; r < nr; ++r) {
-    double v = red_identity(ops[r]);
-    for (u32 b = threadIdx.x; b < gridDim.x; b += GM_THREADS)
-      v = red_combine(ops[r], v, ld_relaxed_f64(partials + (i64)slots[r] * gridDim.x + b));
-    block_combine(ops[r], v, s_warp, r, s_out);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     for (int r = 0; r < nr; ++r) {
-      double acc = s_warp[r];
-      for (int w = 1; w < GM_WARPS; ++w) acc = red_combine(ops[r], acc, s_warp[w * GM_MAX_RED + r]);
-      s_out[r] = acc;
+      const double* base = partials + (i64)slots[r] * gridDim.x;
+      double acc = red_identity(ops[r]);
+      for (u32 b0 = 0; b0 < gridDim.x; b0 += 32 * 8) {
+        double t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const u32 b = b0 + i * 32 + lane;
+          t[i] = b < gridDim.x ? ld_relaxed_f64(base + b) : red_identity(ops[r]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = red_combine(ops[r], acc, t[i]);
+      }
+      acc = warp_combine(ops[r], acc);
+      if (lane == 0) s_out[r] = acc;
     }
   }
   __syncthreads();

@@ -221,10 +221,11 @@ __global__ void gm_logring_gather_kernel(const __grid_constant__ GatherArgs A) {
   }
 }
 
+// Advance the slot counter after a step's gathers (stream ordered).  The
+// host learns completion from a CUDA event, so no system-scope fence here.
 __global__ void gm_logring_commit_kernel(unsigned long long* dstep, unsigned long long* dcommit) {
   const unsigned long long s = *dstep + 1;
   *dstep = s;
-  __threadfence_system();
   *(volatile unsigned long long*)dcommit = s;
 }
 

@@ -12,11 +12,13 @@ Here a replay inside an active step
     3 per dim when numel > threshold 1000, torch/_tensor_str.py) into a slot
     of a pinned, device-mapped host ring (gm_logring_gather);
   * records (callee, argument template) in the step's call list.
-At the end of the step a commit kernel publishes the step number to mapped
-host memory.  A host thread (or `flush()`) waits for the commit — it never
-synchronises the stream — rebuilds CPU tensors whose repr is identical to
-the original's, and calls the original callee in source order, so level
-checks happen at drain time exactly as if the call ran late.
+A step that gathered tensors then bumps the device slot counter
+(gm_logring_commit) and records a CUDA event behind itself; a host thread
+(or `flush()`) polls that event — it never synchronises the stream —
+rebuilds CPU tensors whose repr is identical to the original's, and calls
+the original callee in source order, so level checks happen at drain time
+exactly as if the call ran late.  A step whose deferred calls carry host
+constants only (the whole corpus) costs no device work at all.
 
 Outside a step (a plain call of the lowered function) replay is immediate,
 which is the reference's behaviour.
@@ -75,6 +77,7 @@ class TensorRef:
 class StepTemplate:
     calls: list = field(default_factory=list)   # (site, callee, [arg | TensorRef])
     discard: bool = False
+    gathers: int = 0                            # device gathers launched by the step
 
 
 class _TensorText:
@@ -132,8 +135,10 @@ class LogRing:
         self.host = nat.lib().gm_logring_host_ptr(h)
         self.lock = threading.RLock()
         self.pending: deque = deque()        # (step_number, template)
-        self.launched = 0                    # steps committed by launches (device counter target)
+        self.launched = 0                    # steps queued for the drain
         self.drained = 0
+        self.gather_steps = 0                # steps that advanced the device slot counter
+        self.drained_gather_steps = 0
         self._active: StepTemplate | None = None
         self._cursor = 0
         self.gathers = 0
@@ -173,6 +178,7 @@ class LogRing:
                     "gm_logring_gather",
                 )
                 self.gathers += 1
+                tmpl.gathers += 1
                 gf = a.grad_fn
                 out.append(TensorRef(off, a.dtype, shape, counts, heads,
                                      type(gf).__name__ if gf is not None else None, a.requires_grad))
@@ -183,10 +189,14 @@ class LogRing:
         tmpl.calls.append((site, callee, out))
 
     def end(self) -> StepTemplate:
+        """Close the step.  Only a step that gathered tensors advances the
+        device slot counter (gm_logring_commit); a step whose deferred calls
+        carry host constants only launches nothing at all."""
         tmpl = self._active
         self._active = None
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        nat.check(nat.lib().gm_logring_commit(self.handle, ctypes.c_void_p(stream)), "gm_logring_commit")
+        if tmpl.gathers:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            nat.check(nat.lib().gm_logring_commit(self.handle, ctypes.c_void_p(stream)), "gm_logring_commit")
         return tmpl
 
     @property
@@ -194,13 +204,26 @@ class LogRing:
         return self._active is not None
 
     def enqueue(self, tmpl: StepTemplate) -> None:
-        """Register one launched step (eager or graph replay) in order."""
+        """Register one launched step (eager or graph replay), in stream
+        order.  Completion is a CUDA event recorded behind the step (polled by
+        the drain, never waited on by the forward); steps with nothing to
+        deliver are not queued."""
+        if not tmpl.calls:
+            return
         with self.lock:
-            # back-pressure: never run more than n_slots-1 steps ahead of the drain
-            while self.launched - self.drained >= self.n_slots - 1:
-                self._drain_one(block=True)
+            slot = None
+            if tmpl.gathers:
+                # back-pressure: never run more than n_slots-1 gather steps ahead
+                while self.gather_steps - self.drained_gather_steps >= self.n_slots - 1:
+                    self._drain_one(block=True)
+                slot = self.gather_steps % self.n_slots
+                self.gather_steps += 1
+            ev = None
+            if tmpl.gathers:
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream(self.device))
             self.launched += 1
-            self.pending.append((self.launched, tmpl))
+            self.pending.append((self.launched, tmpl, ev, slot))
 
     # -- consumer side (host) -------------------------------------------------------
     def committed(self) -> int:
@@ -233,17 +256,19 @@ class LogRing:
         with self.lock:
             if not self.pending:
                 return False
-            step, tmpl = self.pending[0]
-            while self.committed() < step:
-                if not block:
-                    return False
-                time.sleep(20e-6)
+            step, tmpl, ev, slot = self.pending[0]
+            if ev is not None:
+                while not ev.query():
+                    if not block:
+                        return False
+                    time.sleep(20e-6)
             self.pending.popleft()
-            slot = (step - 1) % self.n_slots
             if not tmpl.discard:
                 for _site, callee, args in tmpl.calls:
                     real = [self._rebuild(a, slot) if isinstance(a, TensorRef) else a for a in args]
                     callee(*real)
+            if slot is not None:
+                self.drained_gather_steps += 1
             self.drained = step
             return True
 
