@@ -567,6 +567,8 @@ class Plan:
         w = out.append
         nscal = max(1, len(self.scalars))
         resident = self._plan_residency_flags()
+        if os.environ.get("GM_PROFILE"):
+            w("#define GM_PROF 1")
         w('#include "gm_region.cuh"')
         w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
         w("#define gm_trunc(x) ((double)(long long)(x))")
@@ -658,7 +660,7 @@ class Plan:
                 w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
                 w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
                 w(f"    const int slots_[{nr}] = {{{', '.join(str(red_slot[r.uid]) for r in reds)}}};")
-                w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red);")
+                w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red{', prof_ + ' + str(40 + 3 * p) if prof else ''});")
                 if prof:
                     w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{2 + 2 * p}], gm::globaltimer());")
                 w("    if (threadIdx.x == 0) {")

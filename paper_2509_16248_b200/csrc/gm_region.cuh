@@ -662,8 +662,15 @@ __device__ __forceinline__ double warp_combine(int op, double v) {
   return v;
 }
 
+// GM_PROF: optional timeline stamps (atomicMax over CTAs) for diagnostics
+#ifdef GM_PROF
+#define GM_STAMP(i) do { if (threadIdx.x == 0 && prof) atomicMax(&prof[i], globaltimer()); } while (0)
+#else
+#define GM_STAMP(i) do { (void)prof; } while (0)
+#endif
+
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
-                                            double* vals, double* s_warp, double* s_out) {
+                                            double* vals, double* s_warp, double* s_out, u64* prof = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r = 0; r < nr; ++r) {
     const double v = warp_combine(ops[r], vals[r]);
@@ -687,7 +694,9 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
     __syncthreads();
     return;
   }
+  GM_STAMP(0);
   grid_sync(P);
+  GM_STAMP(1);
   if (warp == 0) {
     for (int r = 0; r < nr; ++r) {
       const double* base = partials + (i64)slots[r] * gridDim.x;
@@ -707,6 +716,7 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
     }
   }
   __syncthreads();
+  GM_STAMP(2);
 }
 
 // Per-thread float accumulation of one 8-lane vector (masked to nv lanes).
