@@ -235,6 +235,16 @@ def main():
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     with ClockSampler(local) as clocks:
+        # keep the GPU busy (untimed replays) until nvidia-smi has sampled it
+        # under load, so the clock record covers the timed region
+        t_load = time.perf_counter()
+        while time.perf_counter() - t_load < 1.0 or len(clocks.rows) < 3:
+            for _ in range(200):
+                entry.run()
+            torch.cuda.synchronize(dev)
+            if time.perf_counter() - t_load > 5.0:
+                break
+        barrier()
         for i in range(args.steps):
             flush_buf.zero_()
             starts[i].record(stream)

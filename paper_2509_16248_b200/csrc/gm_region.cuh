@@ -82,7 +82,7 @@ struct Params {
   i64 vpc;         // vectors per CTA
   i64 piece_vecs;  // vectors per bulk-copy piece (resident staging)
   i64 partials;    // double[GM_MAX_RED][gridDim.x]
-  i64 barrier;     // u64 arrival counter, monotonic across launches (zeroed once)
+  i64 barrier;     // scratch: arrival counter, epoch flag, results (see grid_reduce)
   i64 status;      // int: 0 ok, 1 grid-barrier timeout (barrier + 16)
   i64 scal_out;    // double[GM_MAX_RED + ...]: scalar slots mirrored by CTA 0 (or 0)
   double hs[GM_MAX_HS];  // host scalars (Python numbers) as runtime values
@@ -623,44 +623,21 @@ __device__ __forceinline__ u64 ld_acquire64(const u64* p) {
   return v;
 }
 
-// Grid barrier on a monotonic 64-bit arrival counter: barrier k of the
-// launch is complete when the counter reaches the next multiple of gridDim.x
-// (no reset, so consecutive launches and passes simply keep counting).  The
-// grid is sized by the host to be co-resident (<= SMs x occupancy); a 2 s
-// %globaltimer bound turns a residency violation into status=1, not a hang.
-__device__ __forceinline__ void grid_sync(const Params& P) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    u64* cnt = (u64*)P.barrier;
-    const u64 g = gridDim.x;
-    const u64 old = atom_add_acq_rel64(cnt, 1ull);
-    const u64 target = (old / g + 1) * g;
-    if (old + 1 != target) {
-      const u64 t0 = globaltimer();
-      int spins = 0;
-      while (ld_acquire64(cnt) < target) {
-        if (++spins > 64) __nanosleep(32);
-        if (globaltimer() - t0 > 2000000000ull) {
-          *(volatile int*)P.status = 1;
-          break;
-        }
-      }
-    }
-  }
-  __syncthreads();
+__device__ __forceinline__ void st_release64(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Reduce `nr` per-thread values across the grid; the result lands in s_out[r]
-// in every CTA.  Both combine stages run in warp 0 with independent loads
-// (no serial chains of dependent loads): warp values of the CTA, then, after
-// the grid barrier, all CTA partials (8 in flight per lane per round).  The
-// tree is the same in every CTA and every run, so every CTA and every run
-// produces the same bits.
-__device__ __forceinline__ double warp_combine(int op, double v) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, off));
-  return v;
-}
+// Scratch layout behind P.barrier (zeroed once, reused by every launch); the
+// counter, the flag and the results sit on separate 128-byte lines so the
+// pollers never contend with the arrivals:
+//   +0    u64 arrival counter (monotonic across launches and passes)
+//   +16   int status (1 = barrier timeout)
+//   +128  u64 epoch flag: number of completed grid reductions
+//   +256  double results[GM_MAX_RED] published by the combining CTA
+// and P.partials = double[slot][gridDim.x] at +GM_SCRATCH_PARTIALS.
+#define GM_SCRATCH_FLAG 128
+#define GM_SCRATCH_RESULTS 256
+#define GM_SCRATCH_PARTIALS 384
 
 // GM_PROF: optional timeline stamps (atomicMax over CTAs) for diagnostics
 #ifdef GM_PROF
@@ -669,8 +646,28 @@ __device__ __forceinline__ double warp_combine(int op, double v) {
 #define GM_STAMP(i) do { (void)prof; } while (0)
 #endif
 
+__device__ __forceinline__ double warp_combine(int op, double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+// Reduce `nr` per-thread values across the grid; the results land in s_out[r]
+// in every CTA.
+//   1. CTA partial: warp butterfly, then warp 0 over the warps (fixed tree).
+//   2. Thread 0 stores the partials and arrives on the counter (acq_rel).
+//   3. The LAST arriving CTA combines all partials in CTA order (warp 0,
+//      8 independent loads per lane per round, then a fixed butterfly),
+//      publishes the results and bumps the epoch flag (release); every other
+//      CTA polls the flag (acquire) and reads the published results.
+// One combiner means no contention on the partial lines and one fixed
+// summation order: every CTA and every run sees the same bits.  The grid is
+// sized to be co-resident (<= SMs x occupancy); a 2 s %globaltimer bound
+// turns a residency violation into status=1, not a hang.
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
                                             double* vals, double* s_warp, double* s_out, u64* prof = nullptr) {
+  __shared__ int s_last;
+  __shared__ u64 s_epoch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r = 0; r < nr; ++r) {
     const double v = warp_combine(ops[r], vals[r]);
@@ -678,44 +675,74 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
   }
   __syncthreads();
   double* partials = (double*)P.partials;
+  const bool multi = gridDim.x > 1;
   if (warp == 0) {
     for (int r = 0; r < nr; ++r) {
       double v = lane < GM_WARPS ? s_warp[lane * GM_MAX_RED + r] : red_identity(ops[r]);
       v = warp_combine(ops[r], v);
       if (lane == 0) {
-        if (gridDim.x > 1)
+        if (multi)
           partials[(i64)slots[r] * gridDim.x + blockIdx.x] = v;
         else
           s_out[r] = v;
       }
     }
   }
-  if (gridDim.x == 1) {
+  if (!multi) {
     __syncthreads();
     return;
   }
   GM_STAMP(0);
-  grid_sync(P);
-  GM_STAMP(1);
-  if (warp == 0) {
-    for (int r = 0; r < nr; ++r) {
-      const double* base = partials + (i64)slots[r] * gridDim.x;
-      double acc = red_identity(ops[r]);
-      for (u32 b0 = 0; b0 < gridDim.x; b0 += 32 * 8) {
-        double t[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const u32 b = b0 + i * 32 + lane;
-          t[i] = b < gridDim.x ? ld_relaxed_f64(base + b) : red_identity(ops[r]);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc = red_combine(ops[r], acc, t[i]);
-      }
-      acc = warp_combine(ops[r], acc);
-      if (lane == 0) s_out[r] = acc;
-    }
+  u64* cnt = (u64*)P.barrier;
+  u64* flag = (u64*)((char*)P.barrier + GM_SCRATCH_FLAG);
+  double* results = (double*)((char*)P.barrier + GM_SCRATCH_RESULTS);
+  if (threadIdx.x == 0) {
+    const u64 g = gridDim.x;
+    const u64 old = atom_add_acq_rel64(cnt, 1ull);
+    s_epoch = old / g + 1;
+    s_last = (old + 1) % g == 0;
   }
   __syncthreads();
+  GM_STAMP(1);
+  if (s_last) {
+    if (warp == 0) {
+      for (int r = 0; r < nr; ++r) {
+        const double* base = partials + (i64)slots[r] * gridDim.x;
+        double acc = red_identity(ops[r]);
+        for (u32 b0 = 0; b0 < gridDim.x; b0 += 32 * 8) {
+          double t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const u32 b = b0 + i * 32 + lane;
+            t[i] = b < gridDim.x ? ld_relaxed_f64(base + b) : red_identity(ops[r]);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc = red_combine(ops[r], acc, t[i]);
+        }
+        acc = warp_combine(ops[r], acc);
+        if (lane == 0) {
+          s_out[r] = acc;
+          results[r] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release64(flag, s_epoch);
+  } else {
+    if (threadIdx.x == 0) {
+      const u64 t0 = globaltimer();
+      int spins = 0;
+      while (ld_acquire64(flag) < s_epoch) {
+        if (++spins > 64) __nanosleep(32);
+        if (globaltimer() - t0 > 2000000000ull) {
+          *(volatile int*)P.status = 1;
+          break;
+        }
+      }
+      for (int r = 0; r < nr; ++r) s_out[r] = ld_relaxed_f64(results + r);
+    }
+    __syncthreads();
+  }
   GM_STAMP(2);
 }
 

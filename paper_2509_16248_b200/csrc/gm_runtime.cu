@@ -383,7 +383,8 @@ int gm_region_release(gm_region r) {
 
 size_t gm_region_params_bytes(void) { return sizeof(gm::Params); }
 
-size_t gm_branch_select_scratch_bytes(void) { return 64 + 8 * 4096; }  // barrier(8) pad | status @16 | partials @64
+// barrier scratch (counter, epoch, status, results) | partials @ GM_SCRATCH_PARTIALS
+size_t gm_branch_select_scratch_bytes(void) { return GM_SCRATCH_PARTIALS + 8 * 4096; }
 
 int gm_branch_select_f32(const float* x, float* out, int64_t n, int red, int cmp, double thr, double a1, double b1,
                          double a2, double b2, void* scratch, double* stat_out, void* stream) {
@@ -416,8 +417,9 @@ int gm_branch_select_f32(const float* x, float* out, int64_t n, int red, int cmp
   char* s = (char*)scratch;
   P.barrier = (long long)(uintptr_t)s;
   P.status = (long long)(uintptr_t)(s + 16);
-  P.partials = (long long)(uintptr_t)(s + 64);
-  if ((size_t)grid * 8 > gm_branch_select_scratch_bytes() - 64) return fail(GM_E_INVALID, "grid too large for scratch");
+  P.partials = (long long)(uintptr_t)(s + GM_SCRATCH_PARTIALS);
+  if ((size_t)grid * 8 > gm_branch_select_scratch_bytes() - GM_SCRATCH_PARTIALS)
+    return fail(GM_E_INVALID, "grid too large for scratch");
   BsArgs A;
   A.red = red;
   A.cmp = cmp;

@@ -27,6 +27,7 @@ from . import _native as nat
 from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
 from .ir import Graph, Node, Unsupported
 
+SCRATCH_PARTIALS = 384  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
 _kernel_lock = threading.Lock()
 
@@ -90,11 +91,11 @@ class _Spec:
         self.grid, self.vpc, self.smem, self.threads = grid, vpc, smem, threads
         self.nred = len(plan.reductions)
         self.nscal = len(plan.scalars)
-        # scratch: barrier counter u64 @0 | status int @16 | partials @64 | scalar mirror
+        # scratch: counter/epoch/status/results (192 B, see gm_region.cuh) |
+        # partials | scalar mirror (+1 KB: the GM_PROFILE timeline at scal_out + 64 u64)
         part_bytes = 8 * max(1, self.nred) * grid
-        # (+1 KB: the GM_PROFILE timeline lives at scal_out + 64 u64)
-        self.scratch = torch.zeros(64 + part_bytes + 8 * 64 + 8 * 64 + 8 * max(1, self.nscal), dtype=torch.uint8,
-                                   device=dev)
+        self.scratch = torch.zeros(SCRATCH_PARTIALS + part_bytes + 8 * 64 + 8 * 64 + 8 * max(1, self.nscal),
+                                   dtype=torch.uint8, device=dev)
         base = self.scratch.data_ptr()
         P = nat.Params()
         P.n = n
@@ -103,8 +104,8 @@ class _Spec:
         P.piece_vecs = max(64, -(-vpc // nat.MAX_PIECES)) if vpc else 1
         P.barrier = base
         P.status = base + 16
-        P.partials = base + 64
-        P.scal_out = base + 64 + part_bytes
+        P.partials = base + SCRATCH_PARTIALS
+        P.scal_out = base + SCRATCH_PARTIALS + part_bytes
         self.template = P
         self.in_slots = []  # (slot, free_index, mode)
         for ip in plan.inputs:
@@ -195,13 +196,13 @@ class _Spec:
         end] in ns relative to the first CTA start (syncs; diagnostics)."""
         if not getattr(self.plan, "profiled", False):
             return None
-        off = 64 + 8 * max(1, self.nred) * self.grid + 8 * 64
+        off = SCRATCH_PARTIALS + 8 * max(1, self.nred) * self.grid + 8 * 64
         v = self.scratch[off: off + 8 * 64].view(torch.int64).tolist()
         t0 = v[0]
         return [x - t0 if x else 0 for x in v]
 
     def reset_timeline(self) -> None:
-        off = 64 + 8 * max(1, self.nred) * self.grid + 8 * 64
+        off = SCRATCH_PARTIALS + 8 * max(1, self.nred) * self.grid + 8 * 64
         t = self.scratch[off: off + 8 * 64].view(torch.int64)
         t.zero_()
         t[0] = 2 ** 62
@@ -212,7 +213,7 @@ class _Spec:
 
     def scalars(self) -> list[float]:
         """Scalar slots mirrored by CTA 0 of the last launch (syncs; tests)."""
-        off = 64 + 8 * max(1, self.nred) * self.grid
+        off = SCRATCH_PARTIALS + 8 * max(1, self.nred) * self.grid
         return self.scratch[off: off + 8 * self.nscal].view(torch.float64).tolist()
 
 
