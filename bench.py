@@ -277,21 +277,29 @@ def main():
                     "traffic": None, "kernel": dom["name"], "bytes_alg": dom["bytes"], "kernel_ms": dom["ms"],
                     "peak_kind": peak_kind, "share_of_step": dom["ms"] / statistics.mean(step_ms)}
 
-    # ---- end to end through the public API (pinned host in, host out)
-    out_host = None
-    e2e_ms = []
+    # ---- end to end through the public API, host buffers in and out:
+    # (a) single call latency: executor(*pinned host inputs) -> D2H into a
+    #     pinned host tensor, synchronised; (b) throughput: the executor's
+    #     double-buffered host pipeline (H2D / forward / D2H overlapped).
     h2d = sum(t.numel() * t.element_size() for t in x_host)
-    for _ in range(3):
+    out0 = ex(*x_host)
+    out_pinned = torch.empty(out0.shape, dtype=out0.dtype, pin_memory=True)
+    e2e_ms = []
+    for i in range(args.steps + 3):
+        e0 = time.perf_counter()
         out = ex(*x_host)
-        out_host = out.to("cpu", non_blocking=False)
+        out_pinned.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        if i >= 3:
+            e2e_ms.append(1e3 * (time.perf_counter() - e0))
+    ex.flush()
+    host_batches = [tuple(x_host)] * args.steps
+    outs = [torch.empty(out0.shape, dtype=out0.dtype, pin_memory=True) for _ in range(args.steps)]
+    ex.run_host_pipelined(host_batches[:4], out=outs[:4])  # build both slots, warm
     ex.flush()
     barrier()
     t_e2e = time.perf_counter()
-    for _ in range(args.steps):
-        e0 = time.perf_counter()
-        out = ex(*x_host)
-        out_host = out.to("cpu")
-        e2e_ms.append(1e3 * (time.perf_counter() - e0))
+    ex.run_host_pipelined(host_batches, out=outs)
     barrier()
     e2e_total = time.perf_counter() - t_e2e
     ex.flush()
@@ -299,7 +307,7 @@ def main():
         t = torch.tensor([e2e_total], device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e_total = float(t)
-    d2h = out_host.numel() * out_host.element_size()
+    d2h = out_pinned.numel() * out_pinned.element_size()
 
     n_region_launch = len(fused)
     tmpl = getattr(entry, "template", None)
@@ -326,7 +334,10 @@ def main():
         "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
                    "shape": list(x_host[0].shape), "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed (256 MB write) between timed steps"},
-        "e2e": {"value": ws * batch * args.steps / e2e_total, "unit": "samples/s", "p50_ms": statistics.median(e2e_ms),
+        "e2e": {"value": ws * batch * args.steps / e2e_total, "unit": "samples/s",
+                "how": "B200Executor.run_host_pipelined: pinned host inputs -> H2D -> graph replay -> D2H into "
+                       "pinned host outputs, double-buffered; wall clock, max over ranks",
+                "p50_ms_single_call": statistics.median(e2e_ms),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": gpu_launches,
         "roofline": roofline,

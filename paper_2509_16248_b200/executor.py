@@ -145,8 +145,11 @@ class B200Executor:
         if drain_thread:
             logring.ring_for(self.device).start_drain_thread()
 
-    def prepare(self, *args) -> _Entry:
-        key = _key(args)
+    def prepare(self, *args, slot: int = 0) -> _Entry:
+        """The captured entry for this input signature (built on first use).
+        `slot` selects an independent copy (own static buffers and graph),
+        used to double-buffer host-fed pipelines."""
+        key = _key(args) + (("slot", slot),)
         e = self.entries.get(key)
         if e is None:
             with torch.cuda.device(self.device):
@@ -158,6 +161,50 @@ class B200Executor:
         e = self.prepare(*args)
         e.load(args)
         return e.run()
+
+    def run_host_pipelined(self, batches, out=None):
+        """Throughput path for host-resident inputs: each batch (a tuple of
+        pinned CPU tensors) is copied H2D on a copy stream, replayed on the
+        compute stream and its output copied D2H into pinned host memory on a
+        second copy stream, double-buffered across two captured graphs so
+        the copies of batch k+1 / k-1 overlap the forward of batch k.
+        Returns the list of host outputs (pinned tensors), in order."""
+        batches = list(batches)
+        if not batches:
+            return []
+        dev = self.device
+        entries = [self.prepare(*[b.to(dev) for b in batches[0]], slot=s) for s in (0, 1)]
+        comp = torch.cuda.current_stream(dev)
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        free = [torch.cuda.Event() for _ in range(2)]      # slot's buffers reusable
+        loaded = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        results = []
+        outs_host = out or [None] * len(batches)
+        for k, batch in enumerate(batches):
+            s = k % 2
+            e = entries[s]
+            with torch.cuda.stream(h2d):
+                if k >= 2:
+                    h2d.wait_event(free[s])
+                for st, a in zip(e.static, batch):
+                    if torch.is_tensor(st):
+                        st.copy_(a, non_blocking=True)
+                loaded[s].record(h2d)
+            comp.wait_event(loaded[s])
+            if k >= 2:
+                comp.wait_event(free[s])
+            o = e.run()
+            done[s].record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done[s])
+                if outs_host[k] is None:
+                    outs_host[k] = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+                outs_host[k].copy_(o, non_blocking=True)
+                free[s].record(d2h)
+            results.append(outs_host[k])
+        d2h.synchronize()
+        return results
 
     def flush(self) -> None:
         """Deliver every deferred print/log of the calls made so far."""

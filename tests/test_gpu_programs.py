@@ -74,3 +74,20 @@ def test_workloads(programs, name, dtype):
     for idx in range(len(prog["inputs"])):
         prog, ref_out, ref_text, out, text, ex, low = _run(programs, name, idx, dtype)
         _check(prog, name, ref_out, ref_text, out, text, ex, low, dtype)
+
+
+@pytest.mark.gpu
+def test_host_pipeline_matches_single_calls(programs):
+    """B200Executor.run_host_pipelined (double-buffered H2D / replay / D2H)
+    returns, batch by batch, exactly what single calls return."""
+    prog = programs["bigbird_like"]
+    ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
+    batches = []
+    for spec in prog["inputs"]:
+        args = orc.make_args(spec["args"], spec["seed"], torch.bfloat16)
+        batches.append(tuple(a.pin_memory() for a in args))
+    singles = [ex(*b).cpu().clone() for b in batches]
+    outs = ex.run_host_pipelined(batches * 3)
+    ex.flush()
+    for k, o in enumerate(outs):
+        assert torch.equal(o, singles[k % len(batches)]), k
