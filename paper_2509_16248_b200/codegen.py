@@ -36,12 +36,12 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _native as nat
-from .ir import COMPARE, REDUCE, Graph, Node, Unsupported, infer, is_fusable_dtype, topo
+from .ir import COMPARE, INT_REDUCE, ITEM, NZSUM, REDUCE, Graph, Node, Unsupported, infer, is_fusable_dtype, topo
 
 DT_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2, torch.bool: 4}
 DT_SIZE = {torch.float32: 4, torch.bfloat16: 2, torch.float16: 2, torch.bool: 1}
-RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "amax": 1, "amin": 2, "prod": 3, "any": 4,
-          "all": 5}
+RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "nzsum": 0, "amax": 1, "amin": 2, "prod": 3,
+          "any": 4, "all": 5}
 
 MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strided", "scalar"
 
@@ -484,6 +484,9 @@ class Plan:
             return f"{dst} = (double)gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);"
         if node.op in REDUCE:
             raise AssertionError("reductions are finished by _finish_reduction")
+        if node.op == ITEM:
+            # the 0-d tensor's value as a Python number (exact in double)
+            return f"{dst} = {self._sv(node.args[0])};"
         R = _round_d(node.dtype) if node.kind == "dscalar" else ""
         a = node.args
         op = node.op
@@ -633,7 +636,10 @@ class Plan:
                 if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
                     w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
             for k, r in enumerate(reds):
-                w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
+                if self._exact_acc(r):
+                    w(f"    double acc{k} = 0.0;")
+                else:
+                    w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
             U = self.unroll
             self._cur_pass = p
             waits = []
@@ -732,7 +738,15 @@ class Plan:
             for k, r in enumerate(reds):
                 x = r.args[0]
                 src = f"n{x.uid}_{u}"
-                if r.op == "norm":
+                if r.op == NZSUM:
+                    w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
+                      f"if (l < nv{u} && {src}[l] != 0.f) t_ += (double)({self._coordsum(f'(e{u} + l)')});\n"
+                      f"{ind}acc{k} += t_; }}")
+                elif self._exact_acc(r):
+                    w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
+                      f"if (l < nv{u}) t_ += (double)({'(' + src + '[l] != 0.f ? 1.f : 0.f)' if r.op == 'count_nonzero' else src + '[l]'});\n"
+                      f"{ind}acc{k} += t_; }}")
+                elif r.op == "norm":
                     w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = gm::mul({src}[l], {src}[l]);\n{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, t_, nv{u}); }}")
                 elif r.op == "count_nonzero":
                     w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = {src}[l] != 0.f ? 1.f : 0.f;\n{ind}acc{k} = gm::acc8(0, acc{k}, t_, nv{u}); }}")
@@ -741,6 +755,23 @@ class Plan:
             for j, o in outs:
                 k = self._out_slot(j)
                 w(f"{ind}gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
+
+    def _exact_acc(self, r: Node) -> bool:
+        """Integer-valued reductions accumulate in fp64 (exact to 2^53)."""
+        return r.op in INT_REDUCE or (r.op == "sum" and not r.args[0].dtype.is_floating_point)
+
+    def _coordsum(self, idx: str) -> str:
+        """Sum of the coordinates of flat index `idx` in the iteration space."""
+        S = list(self.shape)
+        terms = []
+        stride = 1
+        for d in range(len(S) - 1, -1, -1):
+            t = f"({idx} / {stride}ll)" if stride != 1 else f"({idx})"
+            if d > 0:
+                t = f"({t} % {S[d]}ll)"
+            terms.append(t)
+            stride *= S[d]
+        return " + ".join(terms) if terms else "0"
 
     def _emit_scalar_level(self, w, level: int) -> None:
         nodes = [n for n in self.scalars if self.avail[n.uid] == level and n.op not in REDUCE]

@@ -30,6 +30,10 @@ class Unsupported(Exception):
     """The expression leaves the fusable subset."""
 
 
+# `.item()` (attr_table.cfg: dynamic) lowered to a device scalar with Python
+# number semantics — SURVEY §8f rank 2 (corpus/longformer_like/original.py:18-26).
+ITEM = "item"
+
 UNARY = {
     "neg", "pos", "abs", "relu", "sigmoid", "tanh", "exp", "log", "sqrt", "rsqrt", "sin", "cos",
     "silu", "square", "reciprocal", "logical_not",
@@ -37,7 +41,14 @@ UNARY = {
 BINARY = {"add", "sub", "mul", "div", "pow", "maximum", "minimum", "gt", "ge", "lt", "le", "eq", "ne",
           "logical_and", "logical_or"}
 COMPARE = {"gt", "ge", "lt", "le", "eq", "ne"}
-REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_nonzero"}
+REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_nonzero", "nzsum"}
+# reductions whose result is an integer count/sum: accumulated exactly in fp64
+INT_REDUCE = {"count_nonzero", "nzsum"}
+# `torch.nonzero(m).sum()` lowered to a reduction: the sum over the positions
+# where m holds of their coordinates (SURVEY §8f rank 1,
+# corpus/moe_minicpm_like/original.py:14-15)
+NZSUM = "nzsum"
+GM_RT_NAME = "__gm_rt__"
 
 # torch.<name>(...) / torch.nn.functional.<name>(...) spellings
 _TORCH_FUNCS = {
@@ -54,7 +65,7 @@ _TORCH_FUNCS = {
 }
 # Tensor.<name>(...) spellings (pure_ops.cfg plus the attr_table reductions)
 _METHODS = dict(_TORCH_FUNCS)
-_METHODS.update({"clamp_min": "clamp_min", "clamp_max": "clamp_max"})
+_METHODS.update({"clamp_min": "clamp_min", "clamp_max": "clamp_max", "item": ITEM})
 
 _BINOP = {ast.Add: "add", ast.Sub: "sub", ast.Mult: "mul", ast.Div: "div", ast.Pow: "pow"}
 _CMPOP = {ast.Gt: "gt", ast.GtE: "ge", ast.Lt: "lt", ast.LtE: "le", ast.Eq: "eq", ast.NotEq: "ne"}
@@ -180,6 +191,8 @@ class Builder:
         if not isinstance(func, ast.Attribute):
             raise Unsupported("call of a plain name")
         chain = attr_chain(func)
+        if chain == [GM_RT_NAME, "nonzero_sum"] and len(c.args) == 1 and not c.keywords:
+            return self.op(NZSUM, self.expr(c.args[0]))
         is_torch = chain is not None and (
             (len(chain) == 2 and chain[0] in self.torch_names)
             or (len(chain) == 2 and chain[0] in self.functional_names)
@@ -217,6 +230,10 @@ class Builder:
             if len(args) != 1 or kw:
                 raise Unsupported(f"{name} with arguments")
             return self.op(name, args[0])
+        if name == ITEM:
+            if len(args) != 1 or kw or not method:
+                raise Unsupported("item arguments")
+            return self.op(ITEM, args[0])
         if name in UNARY:
             if len(args) != 1 or kw:
                 raise Unsupported(f"{name} arguments")
@@ -306,7 +323,19 @@ META_FNS = {
     "any": lambda a: a.any(),
     "all": lambda a: a.all(),
     "count_nonzero": lambda a: torch.count_nonzero(a),
+    "nzsum": lambda a: torch.zeros((), dtype=torch.int64, device=a.device),
 }
+
+
+def _meta_item(a):
+    """Python-number stand-in with the type `Tensor.item()` would return."""
+    if not torch.is_tensor(a) or a.numel() != 1:
+        raise Unsupported("item of a non-scalar")
+    if a.dtype == torch.bool:
+        return False
+    if a.dtype.is_floating_point:
+        return 0.0
+    return 0
 
 
 def _meta_clamp(node: Node, vals):
@@ -344,6 +373,8 @@ def infer(graph: Graph, args: list, needed: list[Node]) -> None:
             try:
                 if node.op == "clamp":
                     v = _meta_clamp(node, vals)
+                elif node.op == ITEM:
+                    v = _meta_item(vals[0])
                 else:
                     if all(not torch.is_tensor(x) for x in vals) and node.op not in (
                         "add", "sub", "mul", "div", "pow", "neg", "pos", "abs", "gt", "ge", "lt", "le", "eq", "ne",

@@ -347,6 +347,32 @@ class ModuleRuntime:
         self.sites = lowered.sites
         self.immediate_replays = 0
 
+    # -- fixed-shape replacements of dynamic-shape ops whose
+    #    only consumer is a full sum (see lowering._lower_dynamic_shape)
+    @staticmethod
+    def nonzero_sum(mask):
+        """== torch.nonzero(mask).sum() (int64).  Inside a fused region this
+        is a coordinate-sum reduction; here (unfused) it is computed without
+        sizing a dynamic output: sum over dims of (coordinate * mask)."""
+        m = mask != 0
+        total = torch.zeros((), dtype=torch.int64, device=m.device)
+        for d, n in enumerate(m.shape):
+            shape = [1] * m.dim()
+            shape[d] = n
+            coord = torch.arange(n, device=m.device, dtype=torch.int64).view(shape)
+            total = total + (coord * m).sum()
+        return total
+
+    @staticmethod
+    def unique_sum(x):
+        """== x.unique().sum(): sort, keep the first of each run of equal
+        values, sum — fixed shapes throughout, so no host sync."""
+        s = x.reshape(-1).sort().values
+        keep = torch.ones_like(s, dtype=torch.bool)
+        if s.numel() > 1:
+            keep[1:] = s[1:] != s[:-1]
+        return torch.where(keep, s, torch.zeros((), dtype=s.dtype, device=s.device)).sum()
+
     def replay(self, site: int, callee, captured: tuple) -> None:
         ring = active_ring()
         if ring is None:

@@ -55,6 +55,7 @@ class Lowered:
     regions: list[Region] = field(default_factory=list)
     sites: list[ReplaySite] = field(default_factory=list)
     region_sources: list[str] = field(default_factory=list)
+    dynamic_shape_lowered: list = field(default_factory=list)
 
 
 def _torch_aliases(tree: ast.Module) -> tuple[set[str], set[str]]:
@@ -98,6 +99,29 @@ def _is_replay(stmt: ast.stmt) -> tuple[ast.expr, str] | None:
     if isinstance(inner, ast.Name) and inner.id.startswith("__gm_defer_"):
         return call.func, inner.id
     return None
+
+
+_DYN_OPS = {"nonzero", "unique", "masked_select"}   # data/dynamic_shape_ops.cfg
+
+
+def _dyn_def(stmt: ast.stmt, torch_names: set[str]):
+    """`V = torch.nonzero(M)` / `M.nonzero()` / `X.unique()` / `torch.unique(X)` /
+    `torch.masked_select(X, M)` / `X.masked_select(M)` -> (V, op, operand exprs)."""
+    if not (isinstance(stmt, ast.Assign) and len(stmt.targets) == 1 and isinstance(stmt.targets[0], ast.Name)
+            and isinstance(stmt.value, ast.Call) and not stmt.value.keywords):
+        return None
+    call = stmt.value
+    f = call.func
+    if not isinstance(f, ast.Attribute) or f.attr not in _DYN_OPS:
+        return None
+    if isinstance(f.value, ast.Name) and f.value.id in torch_names:
+        operands = list(call.args)
+    else:
+        operands = [f.value] + list(call.args)
+    want = {"nonzero": 1, "unique": 1, "masked_select": 2}[f.attr]
+    if len(operands) != want:
+        return None
+    return stmt.targets[0].id, f.attr, operands
 
 
 def _names_read(node: ast.AST) -> set[str]:
@@ -144,10 +168,67 @@ class _FunctionLowerer:
             return False
         return True
 
+    def _lower_dynamic_shape(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
+        """a dynamic-shape op whose only consumer is a full
+        `.sum()` is replaced by a fixed-shape reduction, so no host sync is
+        needed to size its output (the reference reports these sites
+        unfixable, data/dynamic_shape_ops.cfg; the counts stay the reference's):
+          nonzero(M).sum()          -> __gm_rt__.nonzero_sum(M)   (fused coordinate sum)
+          masked_select(X, M).sum() -> torch.where(M, X, 0).sum() (fused)
+          X.unique().sum()          -> __gm_rt__.unique_sum(X)    (sort + adjacent-distinct mask)
+        """
+        torch_name = sorted(self.owner.torch_names)[0]
+        out = list(stmts)
+        i = 0
+        while i < len(out):
+            d = _dyn_def(out[i], self.owner.torch_names)
+            if d is None:
+                i += 1
+                continue
+            var, op, operands = d
+            loads = [n for n in ast.walk(self.fn) if isinstance(n, ast.Name) and n.id == var]
+            stores = [n for n in loads if isinstance(n.ctx, ast.Store)]
+            uses = [n for n in loads if isinstance(n.ctx, ast.Load)]
+            if len(stores) != 1 or len(uses) != 1:
+                i += 1
+                continue
+            if op == "nonzero":
+                repl = ast.Call(ast.Attribute(ast.Name(GM_RT, ast.Load()), "nonzero_sum", ast.Load()),
+                                [operands[0]], [])
+            elif op == "unique":
+                repl = ast.Call(ast.Attribute(ast.Name(GM_RT, ast.Load()), "unique_sum", ast.Load()),
+                                [operands[0]], [])
+            else:
+                where = ast.Call(ast.Attribute(ast.Name(torch_name, ast.Load()), "where", ast.Load()),
+                                 [operands[1], operands[0], ast.Constant(0)], [])
+                repl = ast.Call(ast.Attribute(where, "sum", ast.Load()), [], [])
+            target = uses[0]
+
+            class _Sub(ast.NodeTransformer):
+                done = 0
+
+                def visit_Call(self, node):
+                    f = node.func
+                    if (isinstance(f, ast.Attribute) and f.attr == "sum" and f.value is target
+                            and not node.args and not node.keywords):
+                        _Sub.done += 1
+                        return ast.copy_location(copy.deepcopy(repl), node)
+                    return self.generic_visit(node)
+
+            new_tail = [_Sub().visit(s) for s in out[i + 1:]]
+            if _Sub.done != 1:
+                i += 1
+                continue
+            self.owner.dyn_lowered.append((var, op))
+            out = out[:i] + new_tail
+            ast.fix_missing_locations(self.fn)
+        return out
+
     def lower_block(self, stmts: list[ast.stmt], in_loop: bool) -> list[ast.stmt]:
         out: list[ast.stmt] = []
         run: list[ast.stmt] = []
         hoist: list[ast.stmt] = []
+        stmts = self._lower_dynamic_shape(stmts)
         for stmt in self._split_returns(stmts):
             cap = _is_capture(stmt)
             if cap is not None and run:
@@ -258,6 +339,7 @@ class _Lowerer:
         self.region_sources: list[str] = []
         self.sites: list[ReplaySite] = []
         self.fallback_defs: list[ast.FunctionDef] = []
+        self.dyn_lowered: list[tuple[str, str]] = []
 
     def next_ret(self) -> int:
         self._ret = getattr(self, "_ret", -1) + 1
@@ -316,7 +398,7 @@ class _Lowerer:
             fn.body = fl.lower_block(fn.body, in_loop=False)
         ast.fix_missing_locations(self.tree)
         source = ast.unparse(self.tree)
-        return Lowered(self.text, source, self.regions, self.sites, self.region_sources)
+        return Lowered(self.text, source, self.regions, self.sites, self.region_sources, list(self.dyn_lowered))
 
 
 def lower(text: str) -> tuple[Lowered, "_Lowerer"]:

@@ -33,10 +33,12 @@ def _check(prog, name, ref_out, ref_text, out, text, ex, low, dtype):
     if prog.get("compare_output_text", True):
         assert text == ref_text, (name, text, ref_text)
     info = ex.info()[0]
-    residual = prog["outcome"]["predicted_residual"]
-    if residual == 0:
-        assert info.mode == "graph", (name, info)
-        assert info.host_syncs == 0, (name, info)
+    # every corpus program and stand-in is sync-free on the B200 path — the
+    # 15 dynamic-shape sites of moe_minicpm_like and the 3 .item() reads of
+    # longformer_like included, although the
+    # reference reports them unfixable (its counts stay the parity target)
+    assert info.mode == "graph", (name, info)
+    assert info.host_syncs == 0, (name, info)
     # every region whose types are fusable ran the sm_100a kernel
     for r in low.regions:
         assert r.stats.launches + r.stats.fallbacks > 0
@@ -54,7 +56,7 @@ def test_corpus_manifest_shapes(programs, name):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
-@pytest.mark.parametrize("name", [c for c in CORPUS if c != "moe_minicpm_like"])
+@pytest.mark.parametrize("name", CORPUS)
 def test_corpus_baseline_shapes(programs, name, dtype):
     """Config 3/5: corpus programs with every tensor at the BASELINE shape."""
     prog = programs[name]

@@ -42,9 +42,23 @@ def test_capture_hoisted_not_splitting(programs):
     assert len(low.sites) == 2
 
 
-def test_longformer_item_reads_cut_regions(programs):
+def test_longformer_item_reads_become_device_scalars(programs):
+    """`w = t.item()` feeding only tensor arithmetic stays a
+    device scalar, so the three host reads vanish and the forward is one
+    3-pass region; the dead final read (`w2`) is dropped."""
     low, _ = lowering.lower(programs["longformer_like"]["transformed"])
-    assert [r.out_names for r in low.regions] == [["win", "span"], ["scaled", "peak"], ["shifted", "floor"]]
+    assert [r.out_names for r in low.regions] == [["shifted"]]
+    assert "item" not in low.source.split("def forward")[1].split("compiled_forward")[0]
+
+
+def test_moe_dynamic_shape_ops_lowered(programs):
+    """nonzero / unique / masked_select consumed only by
+    .sum() become fixed-shape reductions (no data-dependent output size)."""
+    low, _ = lowering.lower(programs["moe_minicpm_like"]["transformed"])
+    ops = [op for _, op in low.dynamic_shape_lowered]
+    assert ops.count("nonzero") == 5 and ops.count("unique") == 5 and ops.count("masked_select") == 5
+    body = low.source.split("def forward")[1].split("compiled_forward")[0]
+    assert "nonzero(" not in body and ".unique()" not in body and "masked_select" not in body
 
 
 def test_name_mangling_safe():
