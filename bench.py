@@ -95,6 +95,23 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def max_over_ranks(x: float, dist_mod, device=None) -> float:
+    """Max of a per-rank duration across replicas (all-reduce MAX on a 1-elem
+    tensor: plumbing for the timing, not a data-path collective)."""
+    if dist_mod is None or not dist_mod.is_initialized() or dist_mod.get_world_size() == 1:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=device or "cpu")
+    dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+    return float(t)
+
+
+def replica_value(batch: int, steps: int, world: int, max_seconds: float) -> float:
+    """Whole-job samples/s of `world` independent replicas."""
+    return world * batch * steps / max_seconds
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -253,12 +270,8 @@ def main():
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ex.flush()
-    total_ms = sum(step_ms)
-    if pg is not None:
-        t = torch.tensor([total_ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        total_ms = float(t)
-    value = ws * batch * args.steps / (total_ms / 1e3)
+    total_ms = max_over_ranks(sum(step_ms), pg, dev)
+    value = replica_value(batch, args.steps, ws, total_ms / 1e3)
 
     # ---- dominant fused kernel timed alone (same stream, L2 flushed)
     fused = [r for r in low.regions if r.last_spec is not None]
@@ -301,12 +314,8 @@ def main():
     t_e2e = time.perf_counter()
     ex.run_host_pipelined(host_batches, out=outs)
     barrier()
-    e2e_total = time.perf_counter() - t_e2e
+    e2e_total = max_over_ranks(time.perf_counter() - t_e2e, pg, dev)
     ex.flush()
-    if pg is not None:
-        t = torch.tensor([e2e_total], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        e2e_total = float(t)
     d2h = out_pinned.numel() * out_pinned.element_size()
 
     n_region_launch = len(fused)
@@ -334,7 +343,7 @@ def main():
         "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
                    "shape": list(x_host[0].shape), "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed (256 MB write) between timed steps"},
-        "e2e": {"value": ws * batch * args.steps / e2e_total, "unit": "samples/s",
+        "e2e": {"value": replica_value(batch, args.steps, ws, e2e_total), "unit": "samples/s",
                 "how": "B200Executor.run_host_pipelined: pinned host inputs -> H2D -> graph replay -> D2H into "
                        "pinned host outputs, double-buffered; wall clock, max over ranks",
                 "p50_ms_single_call": statistics.median(e2e_ms),
