@@ -756,6 +756,10 @@ class Plan:
                 k = self._out_slot(j)
                 w(f"{ind}gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
 
+    def _unguarded_in(self, ip: InputPlan, p: int) -> bool:
+        dnf = self._guards(p).get(ip.node.uid, frozenset({frozenset()}))
+        return any(len(c) == 0 for c in dnf)
+
     def _exact_acc(self, r: Node) -> bool:
         """Integer-valued reductions accumulate in fp64 (exact to 2^53)."""
         return r.op in INT_REDUCE or (r.op == "sum" and not r.args[0].dtype.is_floating_point)
@@ -823,7 +827,10 @@ class Plan:
                      and (self.n * DT_SIZE[ip.dtype]) % 16 == 0]
         multi = [ip for ip in stageable if len(ip.passes) >= 2]
         first0 = []  # read by pass 0 only: streaming is optimal, nothing to stash
-        later = [ip for ip in stageable if len(ip.passes) < 2 and 0 not in ip.passes]
+        # prefetch only inputs a later pass reads unconditionally: an input
+        # that only an untaken arm reads must cost no HBM traffic at all
+        later = [ip for ip in stageable if len(ip.passes) < 2 and 0 not in ip.passes
+                 and self._unguarded_in(ip, min(ip.passes))]
         per_sm = 233472  # B200 shared memory per SM (228 KB)
         for minb in (2, 1):
             grid0 = max(1, min(minb * sms, -(-nvec // (nat.THREADS * self.unroll))))

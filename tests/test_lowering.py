@@ -126,6 +126,7 @@ def test_uniform_select_guards_untaken_arm(programs):
     key = "sres1" if plan.stage_group[1] >= 0 else "P.in[1]"
     j = src.index(key + ",", i) if key == "sres1" else src.index(key, i)
     assert "if ((!sb" in src[i:j]
-    # q is read by both passes: staged once, waited in pass 0 (group 0);
-    # hidden is read once by pass 1: prefetched behind pass 0 (group 1)
-    assert plan.stage_group == [0, 1]
+    # q is read by both passes: stashed by pass 0 (group 0); hidden is read
+    # only by the else arm of pass 1, so it is not prefetched (an untaken arm
+    # must cost no HBM traffic) and loads lazily under the guard
+    assert plan.stage_group == [0, -1]
