@@ -106,6 +106,9 @@ class Plan:
         self.name = name
         infer(graph, args, outputs)
         self.order = topo(outputs)
+        # host scalars exactly representable in bf16 (part of the region key)
+        self.host_exact = {n.uid: self._bf16_exact(args[n.value]) for n in self.order
+                           if n.op == "free" and n.kind == "host"}
         self._classify(args)
         self._passes()
         self._inputs(args)
@@ -632,6 +635,8 @@ class Plan:
             for s in used_scal:
                 w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
                 w(f"    const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
+                if s.op == "free" and s.kind == "host":
+                    w(f"    const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
             for ip in self.inputs:
                 if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
                     w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
@@ -699,6 +704,11 @@ class Plan:
         return "\n".join(out) + "\n"
 
     def _emit_body(self, w, p, elem_nodes, reds, outs, guards, loads, waits, U, full):
+        if full and not os.environ.get("GM_NO_PACKED"):
+            pref = self._packed_plan(elem_nodes)
+            if any(v == "P" for v in pref.values()):
+                self._emit_body_packed(w, elem_nodes, reds, outs, guards, loads, U, pref)
+                return
         ind = "      "
         for u in range(U):
             w(f"{ind}const i64 e{u} = (vb + {u} * GM_THREADS) * GM_VEC;")
@@ -735,25 +745,175 @@ class Plan:
                     w(ind + "  " + line.replace("\n", "\n" + ind + "  "))
             if open_block:
                 w(f"{ind}}}")
-            for k, r in enumerate(reds):
-                x = r.args[0]
-                src = f"n{x.uid}_{u}"
-                if r.op == NZSUM:
-                    w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
-                      f"if (l < nv{u} && {src}[l] != 0.f) t_ += (double)({self._coordsum(f'(e{u} + l)')});\n"
-                      f"{ind}acc{k} += t_; }}")
-                elif self._exact_acc(r):
-                    w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
-                      f"if (l < nv{u}) t_ += (double)({'(' + src + '[l] != 0.f ? 1.f : 0.f)' if r.op == 'count_nonzero' else src + '[l]'});\n"
-                      f"{ind}acc{k} += t_; }}")
-                elif r.op == "norm":
-                    w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = gm::mul({src}[l], {src}[l]);\n{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, t_, nv{u}); }}")
-                elif r.op == "count_nonzero":
-                    w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = {src}[l] != 0.f ? 1.f : 0.f;\n{ind}acc{k} = gm::acc8(0, acc{k}, t_, nv{u}); }}")
+            self._emit_reds_outs(w, ind, reds, outs, u)
+
+    # -- packed bf16x2 path ------------------------------------------------------
+    @staticmethod
+    def _bf16_exact(v) -> bool:
+        f = torch.tensor(float(v), dtype=torch.float32)
+        return bool(f.to(torch.bfloat16).to(torch.float32) == f)
+
+    @staticmethod
+    def _bf16_bits(v) -> int:
+        return int(torch.tensor(float(v), dtype=torch.float32).to(torch.bfloat16).view(torch.int16).item()) & 0xFFFF
+
+    def _scalar_packable(self, s: Node, op: str) -> bool:
+        """May scalar `s` enter a packed bf16 op `op` without changing the
+        result?  add/sub/compare round the scalar to bf16 in torch anyway;
+        mul keeps it in fp32, so it must be bf16-exact."""
+        if s.op == "const":
+            return op in ("add", "sub") or self._bf16_exact(s.value)
+        if s.op == "free" and s.kind == "host":
+            return op in ("add", "sub") or self.host_exact.get(s.uid, False)
+        return False
+
+    def _packed_plan(self, elem_nodes: list[Node]) -> dict[int, str]:
+        pref: dict[int, str] = {}
+        bf = torch.bfloat16
+        for n in elem_nodes:
+            r = "F"
+            if n.dtype == bf:
+                if n.op == "free":
+                    ip = self.in_by_uid[n.uid]
+                    if ip.mode == MODE_FULL and ip.dtype == bf:
+                        r = "P"
+                elif n.op in ("add", "sub", "mul"):
+                    ok = True
+                    for a in n.args:
+                        if a.kind == "elem":
+                            ok &= a.dtype == bf
+                        else:
+                            ok &= self._scalar_packable(a, n.op)
+                    if ok and any(a.kind == "elem" for a in n.args):
+                        r = "P"
+                elif n.op in ("neg", "pos", "abs"):
+                    if n.args[0].kind == "elem" and n.args[0].dtype == bf:
+                        r = "P"
+                elif n.op == "where" and n.args[0].kind != "elem":
+                    if all(a.kind == "elem" and a.dtype == bf for a in n.args[1:]):
+                        r = "P"
+            pref[n.uid] = r
+        return pref
+
+    def _packed_scalar(self, s: Node) -> str:
+        if s.op == "const":
+            b = self._bf16_bits(s.value)
+            return f"0x{(b << 16) | b:08x}u"
+        return f"spk{s.uid}"
+
+    def _emit_body_packed(self, w, elem_nodes, reds, outs, guards, loads, U, pref):
+        """Steady-state body (U full vectors) with packed bf16 nodes."""
+        ind = "      "
+        needs: dict[int, set] = {n.uid: {pref[n.uid]} for n in elem_nodes}
+        for n in elem_nodes:
+            for a in n.args:
+                if a.kind == "elem":
+                    needs[a.uid].add(pref[n.uid] if (pref[n.uid] == "P" and not (n.op == "where" and a is n.args[0]))
+                                     else "F")
+        for r in reds:
+            needs[r.args[0].uid].add("F")
+        for u in range(U):
+            w(f"{ind}const i64 e{u} = (vb + {u} * GM_THREADS) * GM_VEC;")
+            w(f"{ind}const int nv{u} = GM_VEC; (void)nv{u};")
+            w(f"{ind}const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
+        for u in range(U):
+            for n in elem_nodes:
+                if "F" in needs[n.uid]:
+                    w(f"{ind}float n{n.uid}_{u}[GM_VEC];")
+                if "P" in needs[n.uid]:
+                    w(f"{ind}u32 p{n.uid}_{u}[4];")
+
+        def convert(n: Node, u: int) -> list[str]:
+            out = []
+            if pref[n.uid] == "P" and "F" in needs[n.uid]:
+                out.append(f"gm::unpack8(p{n.uid}_{u}, n{n.uid}_{u});")
+            if pref[n.uid] == "F" and "P" in needs[n.uid]:
+                out.append(f"gm::pack8(n{n.uid}_{u}, p{n.uid}_{u});")
+            return out
+
+        def node_code(n: Node, u: int) -> list[str]:
+            if pref[n.uid] == "F":
+                return self._elem_code(n, u) + convert(n, u)
+            dst = f"p{n.uid}_{u}"
+            if n.op == "free":
+                ip = self.in_by_uid[n.uid]
+                k = ip.slot
+                g = self.stage_group[k]
+                if g == 0 and self._cur_pass == 0:
+                    code = f"gm::stash_raw(P.in[{k}], sres{k}, e{u}, le{u}, {dst});"
+                elif g >= 0:
+                    code = f"gm::lds_raw(sres{k}, le{u}, {dst});"
                 else:
-                    w(f"{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, {src}, nv{u});")
-            for j, o in outs:
-                k = self._out_slot(j)
+                    code = f"gm::ldg_raw(P.in[{k}], e{u}, {dst});"
+                return [code] + convert(n, u)
+
+            def pv(a: Node) -> str:
+                return f"p{a.uid}_{u}[j]" if a.kind == "elem" else self._packed_scalar(a)
+
+            a = n.args
+            if n.op in ("add", "sub", "mul"):
+                fn = {"add": "gm::hadd2", "sub": "gm::hsub2", "mul": "gm::hmul2"}[n.op]
+                body = f"{fn}({pv(a[0])}, {pv(a[1])})"
+            elif n.op == "neg":
+                body = f"({pv(a[0])} ^ 0x80008000u)"
+            elif n.op == "abs":
+                body = f"({pv(a[0])} & 0x7fff7fffu)"
+            elif n.op == "pos":
+                body = pv(a[0])
+            elif n.op == "where":
+                c = a[0]
+                return [f"if (sb{c.uid}) {{\n#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = p{a[1].uid}_{u}[j];\n}} "
+                        f"else {{\n#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = p{a[2].uid}_{u}[j];\n}}"] + convert(n, u)
+            else:
+                raise AssertionError(n.op)
+            return [f"#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = {body};"] + convert(n, u)
+
+        for u in range(U):
+            for n in loads:
+                for line in node_code(n, u):
+                    w(ind + line.replace("\n", "\n" + ind))
+        for u in range(U):
+            cur_guard = None
+            open_block = False
+            for n in elem_nodes:
+                if n in loads:
+                    continue
+                g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
+                if g != cur_guard:
+                    if open_block:
+                        w(f"{ind}}}")
+                        open_block = False
+                    if g:
+                        w(f"{ind}if ({g}) {{")
+                        open_block = True
+                    cur_guard = g
+                for line in node_code(n, u):
+                    w(ind + "  " + line.replace("\n", "\n" + ind + "  "))
+            if open_block:
+                w(f"{ind}}}")
+            self._emit_reds_outs(w, ind, reds, outs, u, pref)
+
+    def _emit_reds_outs(self, w, ind, reds, outs, u, pref=None):
+        for k, r in enumerate(reds):
+            x = r.args[0]
+            src = f"n{x.uid}_{u}"
+            if r.op == NZSUM:
+                w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
+                  f"if (l < nv{u} && {src}[l] != 0.f) t_ += (double)({self._coordsum(f'(e{u} + l)')});\n"
+                  f"{ind}acc{k} += t_; }}")
+            elif self._exact_acc(r):
+                w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
+                  f"if (l < nv{u}) t_ += (double)({'(' + src + '[l] != 0.f ? 1.f : 0.f)' if r.op == 'count_nonzero' else src + '[l]'});\n"
+                  f"{ind}acc{k} += t_; }}")
+            elif r.op == "norm":
+                w(f"{ind}{{ float t_[GM_VEC];\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) t_[l] = gm::mul({src}[l], {src}[l]);\n{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, t_, nv{u}); }}")
+            else:
+                w(f"{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, {src}, nv{u});")
+        for j, o in outs:
+            k = self._out_slot(j)
+            if pref is not None and pref.get(o.uid) == "P":
+                w(f"{ind}gm::stg_raw(P.out[{k}], e{u}, p{o.uid}_{u});")
+            else:
                 w(f"{ind}gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
 
     def _unguarded_in(self, ip: InputPlan, p: int) -> bool:

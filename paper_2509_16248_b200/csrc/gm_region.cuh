@@ -381,6 +381,52 @@ __device__ __forceinline__ void load8_gmem(const InDesc& d, i64 e, int nv, float
 }
 
 // ---------------------------------------------------------------------------
+// packed bf16x2 arithmetic.  For bf16 operands `op.rn.bf16x2` is the exact
+// result rounded once to bf16 — what torch's CPU kernels produce by
+// computing in fp32 and rounding the fp32 result (the fp32 add/sub/mul of two
+// bf16 values is exact or below half a bf16 ulp).  Chains of such ops then
+// need no unpack/round/pack per op.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 hadd2(u32 a, u32 b) {
+  u32 d;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ u32 hsub2(u32 a, u32 b) {
+  u32 d;
+  asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ u32 hmul2(u32 a, u32 b) {
+  u32 d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ void unpack_bf2(u32 p, float& lo, float& hi) {
+  lo = __uint_as_float(p << 16);
+  hi = __uint_as_float(p & 0xffff0000u);
+}
+__device__ __forceinline__ void unpack8(const u32 (&p)[4], float (&x)[8]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) unpack_bf2(p[j], x[2 * j], x[2 * j + 1]);
+}
+__device__ __forceinline__ void pack8(const float (&x)[8], u32 (&p)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) p[j] = f2bf2(x[2 * j], x[2 * j + 1]);
+}
+// raw 16-byte (8 x bf16) vector access for the packed path
+__device__ __forceinline__ void ldg_raw(const InDesc& d, i64 e, u32 (&p)[4]) {
+  ldg16((const char*)d.ptr + e * 2, p[0], p[1], p[2], p[3]);
+}
+__device__ __forceinline__ void lds_raw(u32 sres, i64 le, u32 (&p)[4]) {
+  lds16(sres + (u32)(le * 2), p[0], p[1], p[2], p[3]);
+}
+__device__ __forceinline__ void stash_raw(const InDesc& d, u32 sres, i64 e, i64 le, u32 (&p)[4]);
+__device__ __forceinline__ void stg_raw(const OutDesc& o, i64 e, const u32 (&p)[4]) {
+  stg16((char*)o.ptr + e * 2, p[0], p[1], p[2], p[3]);
+}
+
+// ---------------------------------------------------------------------------
 // thread-private staging.  Every pass maps local vector lv to thread
 // lv % GM_THREADS, so a thread only ever re-reads the stash slots it wrote:
 // no mbarrier, no __syncthreads.  Pass 0 streams an input it re-reads later
@@ -420,6 +466,11 @@ __device__ __forceinline__ void load8_stash(const InDesc& d, u32 sres, i64 e, i6
   } else {
     E::lds8(s, x);  // (re-read the stored vector: same thread, cheap; keeps one code path)
   }
+}
+
+__device__ __forceinline__ void stash_raw(const InDesc& d, u32 sres, i64 e, i64 le, u32 (&p)[4]) {
+  ldg16((const char*)d.ptr + e * 2, p[0], p[1], p[2], p[3]);
+  sts16(sres + (u32)(le * 2), p[0], p[1], p[2], p[3]);
 }
 
 template <int DT>

@@ -46,7 +46,9 @@ def arg_key(a) -> tuple:
         return ("t", a.dtype, tuple(a.shape), tuple(a.stride()), a.device.type, a.device.index,
                 a.data_ptr() % 16 == 0)
     if isinstance(a, (bool, int, float)):
-        return ("h", type(a))
+        # bf16-exactness of a host scalar selects the packed bf16 code path
+        f = torch.tensor(float(a), dtype=torch.float32)
+        return ("h", type(a), bool(f.to(torch.bfloat16).float() == f))
     return ("o", type(a))
 
 
