@@ -36,7 +36,8 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _native as nat
-from .ir import COMPARE, INT_REDUCE, ITEM, NZSUM, REDUCE, Graph, Node, Unsupported, infer, is_fusable_dtype, topo
+from .ir import (BOOL_AND, BOOL_NOT, BOOL_OR, COMPARE, INT_REDUCE, ITEM, NZSUM, REDUCE, Graph, Node, Unsupported,
+                 infer, is_fusable_dtype, topo)
 
 DT_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2, torch.bool: 4}
 DT_SIZE = {torch.float32: 4, torch.bfloat16: 2, torch.float16: 2, torch.bool: 1}
@@ -522,11 +523,11 @@ class Plan:
         if op in ("maximum", "minimum"):
             fn = "gm::dmax" if op == "maximum" else "gm::dmin"
             return f"{dst} = {R}({fn}({sv(a[0])}, {sv(a[1])}));"
-        if op == "logical_and":
+        if op in ("logical_and", BOOL_AND):
             return f"{dst} = ({sv(a[0])} != 0.0 && {sv(a[1])} != 0.0) ? 1.0 : 0.0;"
-        if op == "logical_or":
+        if op in ("logical_or", BOOL_OR):
             return f"{dst} = ({sv(a[0])} != 0.0 || {sv(a[1])} != 0.0) ? 1.0 : 0.0;"
-        if op == "logical_not":
+        if op in ("logical_not", BOOL_NOT):
             return f"{dst} = ({sv(a[0])} == 0.0) ? 1.0 : 0.0;"
         if op == "clamp":
             has_lo, has_hi = node.value

@@ -49,6 +49,7 @@ INT_REDUCE = {"count_nonzero", "nzsum"}
 # corpus/moe_minicpm_like/original.py:14-15)
 NZSUM = "nzsum"
 GM_RT_NAME = "__gm_rt__"
+BOOL_AND, BOOL_OR, BOOL_NOT = "bool_and", "bool_or", "bool_not"
 
 # torch.<name>(...) / torch.nn.functional.<name>(...) spellings
 _TORCH_FUNCS = {
@@ -174,7 +175,19 @@ class Builder:
                 return self.op("neg", self.expr(e.operand))
             if isinstance(e.op, ast.UAdd):
                 return self.op("pos", self.expr(e.operand))
+            if isinstance(e.op, ast.Not):
+                return self.op(BOOL_NOT, self.expr(e.operand))
             raise Unsupported(f"unary {type(e.op).__name__}")
+        if isinstance(e, ast.BoolOp):
+            # `p and q` / `p or q` / `not p` on 0-d bool
+            # tensors (the reference copies predicates verbatim,
+            # transform.py:386-388, so these reach the runtime and sync via
+            # Tensor.__bool__ or, for `not`, hand torch.where a Python bool)
+            name = BOOL_AND if isinstance(e.op, ast.And) else BOOL_OR
+            node = self.expr(e.values[0])
+            for v in e.values[1:]:
+                node = self.op(name, node, self.expr(v))
+            return node
         if isinstance(e, ast.Compare):
             if len(e.ops) != 1:
                 raise Unsupported("chained comparison")
@@ -327,6 +340,19 @@ META_FNS = {
 }
 
 
+def _meta_bool(op: str, vals):
+    """Python and/or/not.  On host values: Python semantics.  On 0-d bool
+    tensors (predicates): the value Python would return is the logical
+    and/or/not, computed on the device instead of through __bool__."""
+    if all(not torch.is_tensor(v) for v in vals):
+        if op == BOOL_NOT:
+            return not vals[0]
+        return (vals[0] and vals[1]) if op == BOOL_AND else (vals[0] or vals[1])
+    if not all(torch.is_tensor(v) and v.dim() == 0 and v.dtype == torch.bool for v in vals):
+        raise Unsupported(f"{op} needs 0-d bool tensors")
+    return torch.empty((), dtype=torch.bool, device=vals[0].device)
+
+
 def _meta_item(a):
     """Python-number stand-in with the type `Tensor.item()` would return."""
     if not torch.is_tensor(a) or a.numel() != 1:
@@ -375,6 +401,8 @@ def infer(graph: Graph, args: list, needed: list[Node]) -> None:
                     v = _meta_clamp(node, vals)
                 elif node.op == ITEM:
                     v = _meta_item(vals[0])
+                elif node.op in (BOOL_AND, BOOL_OR, BOOL_NOT):
+                    v = _meta_bool(node.op, vals)
                 else:
                     if all(not torch.is_tensor(x) for x in vals) and node.op not in (
                         "add", "sub", "mul", "div", "pow", "neg", "pos", "abs", "gt", "ge", "lt", "le", "eq", "ne",

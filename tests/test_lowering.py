@@ -130,3 +130,17 @@ def test_uniform_select_guards_untaken_arm(programs):
     # only by the else arm of pass 1, so it is not prefetched (an untaken arm
     # must cost no HBM traffic) and loads lazily under the guard
     assert plan.stage_group == [0, -1]
+
+
+def test_boolean_predicates_lowered():
+    """and/or/not of 0-d bool predicates become device logical ops
+     — the whole transformed forward is one region."""
+    src = ("import torch\n\ndef f(x):\n    h = x * 2\n    __gm_pred_0 = (h.sum() > 0) and (h.max() < 5)\n"
+           "    __gm_then_y_0 = h + 1\n    __gm_else_y_0 = h - 1\n"
+           "    y = torch.where(__gm_pred_0, __gm_then_y_0, __gm_else_y_0)\n"
+           "    __gm_pred_1 = not (y.mean() > 0)\n    z = torch.where(__gm_pred_1, y * 3, y)\n    return z\n")
+    low, _ = lowering.lower(src)
+    assert [r.out_names for r in low.regions] == [["z"]]
+    plan = codegen.Plan(low.regions[0].graph, low.regions[0].out_nodes, [torch.randn(4096)], "f", allow_cpu=True)
+    assert plan.npass == 3
+    nat.compile_cubin(plan.source, (10, 0))
