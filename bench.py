@@ -112,6 +112,24 @@ def replica_value(batch: int, steps: int, world: int, max_seconds: float) -> flo
     return world * batch * steps / max_seconds
 
 
+def _ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary
+    (profiles/*_ncu_regions.json, one `ncu --set full` capture), or None."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_regions.json"))):
+        try:
+            with open(path) as fh:
+                rows = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        vals = [r["traffic_bytes"] for r in rows if r.get("kernel") == kernel and "traffic_bytes" in r]
+        if vals:
+            best = sum(vals) / len(vals)
+    return best
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -287,7 +305,8 @@ def main():
     if dom:
         achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": dom["name"], "bytes_alg": dom["bytes"], "kernel_ms": dom["ms"],
+                    "traffic": _ncu_traffic(dom["name"].split(" ")[0]), "kernel": dom["name"],
+                    "bytes_alg": dom["bytes"], "kernel_ms": dom["ms"],
                     "peak_kind": peak_kind, "share_of_step": dom["ms"] / statistics.mean(step_ms)}
 
     # ---- end to end through the public API, host buffers in and out:
