@@ -22,7 +22,8 @@ KEYS = {
     "launch__grid_size": "grid",
     "smsp__inst_executed.sum": "warp_instructions",
 }
-UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3,
+              "msecond": 1e6, "ms": 1e6}
 
 
 def main(rep, out):
