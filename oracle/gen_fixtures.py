@@ -110,6 +110,18 @@ def main() -> None:
             "transformed": new_text,
             "outcome": _outcome(outcome),
         }
+    # the reference's unit fixtures (pkg/tests/fixtures/units/*.py): the
+    # rewrite shapes its own tests pin (test_transform.py), run through the
+    # B200 path by tests/test_gpu_units.py on branch-forcing inputs
+    for up in sorted((REF / "tests" / "fixtures" / "units").glob("*.py")):
+        text = up.read_text()
+        new_text, outcome = fix_file(SourceModule.from_text(f"units/{up.name}", text))
+        programs[f"unit:{up.stem}"] = {
+            "kind": "unit",
+            "original": text,
+            "transformed": new_text,
+            "outcome": _outcome(outcome),
+        }
     GOLDEN.mkdir(parents=True, exist_ok=True)
     (GOLDEN / "programs.json").write_text(json.dumps(programs, indent=1, sort_keys=True) + "\n")
 

@@ -25,6 +25,9 @@ This is the B200 counterpart of the harness call `fn(*clones)`
 
 from __future__ import annotations
 
+import contextlib
+import io
+import logging
 import time
 import warnings
 from dataclasses import dataclass
@@ -48,6 +51,35 @@ def count_syncs(fn, *args):
         torch.cuda.set_sync_debug_mode(prev)
     n = sum(1 for w in rec if _SYNC_MSG in str(w.message))
     return out, n
+
+
+class _SideEffects(logging.Handler):
+    """Counts host side effects a forward performs outside the log ring
+    (prints / log records the rewrite did not defer).  Such a forward cannot
+    be replayed from a CUDA graph without losing them, so it stays eager."""
+
+    def __init__(self):
+        super().__init__(level=logging.DEBUG)
+        self.records = 0
+
+    def emit(self, record):
+        self.records += 1
+
+
+@contextlib.contextmanager
+def _watch_side_effects():
+    h = _SideEffects()
+    root = logging.getLogger()
+    old = root.level
+    root.addHandler(h)
+    root.setLevel(logging.DEBUG)
+    buf = io.StringIO()
+    try:
+        with contextlib.redirect_stdout(buf):
+            yield h, buf
+    finally:
+        root.removeHandler(h)
+        root.setLevel(old)
 
 
 def _key(args) -> tuple:
@@ -81,22 +113,26 @@ class _Entry:
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         syncs = 0
-        with torch.cuda.stream(side):
+        # warm-up runs: their deferred calls are discarded, and any immediate
+        # print/log output (sites the reference did not defer) is swallowed
+        # and counted
+        with torch.cuda.stream(side), _watch_side_effects() as (se, buf):
             for _ in range(ex.warmup):
                 with logring.step(dev, discard=True) as st:
                     _, n = count_syncs(ex.fn, *self.static)
                 ring.enqueue(st.template)
                 syncs = max(syncs, n)
+        side_effects = se.records + len(buf.getvalue())
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize(dev)
         ring.flush()
         self.graph = None
         self.outputs = None
         reason = ""
-        if ex.use_graphs and syncs == 0:
+        if ex.use_graphs and syncs == 0 and not side_effects:
             g = torch.cuda.CUDAGraph()
             try:
-                with torch.cuda.graph(g, pool=ex.pool):
+                with torch.cuda.graph(g, pool=ex.pool), _watch_side_effects():
                     with logring.step(dev, discard=False) as st:
                         self.outputs = ex.fn(*self.static)
                 self.template = st.template
@@ -108,6 +144,8 @@ class _Entry:
                 self.graph = None
         elif syncs:
             reason = f"{syncs} host sync(s) in the forward"
+        elif side_effects:
+            reason = "immediate host side effects (prints/logs not deferred by the rewrite)"
         elif not ex.use_graphs:
             reason = "graphs disabled"
         torch.cuda.synchronize(dev)
