@@ -116,6 +116,9 @@ def reference_callable(text: str, callable_name: str, dtype: torch.dtype | None 
     `dtype` (modules are cast; functions take the cast inputs)."""
     mod = load_program(text, callable_name)
     fn = getattr(mod, callable_name)
+    # a `@torch.compile`-decorated entry runs eagerly here, as the reference's
+    # own equivalence tests do when Inductor is unavailable (TORCHDYNAMO_DISABLE)
+    fn = getattr(fn, "_torchdynamo_orig_callable", fn)
     if dtype is not None and isinstance(fn, torch.nn.Module):
         fn.to(dtype)
     return fn

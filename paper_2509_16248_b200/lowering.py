@@ -391,9 +391,17 @@ class _Lowerer:
 
         return call
 
+    def _is_compile_decorator(self, d: ast.expr) -> bool:
+        target = d.func if isinstance(d, ast.Call) else d
+        chain = attr_chain(target)
+        return chain is not None and len(chain) == 2 and chain[0] in self.torch_names and chain[1] == "compile"
+
     def run(self) -> Lowered:
         fns = [n for n in ast.walk(self.tree) if isinstance(n, (ast.FunctionDef, ast.AsyncFunctionDef))]
         for fn in fns:
+            # `@torch.compile` entry points (analysis.py entry mechanisms) are
+            # executed by the B200 path itself: drop the Dynamo wrapper
+            fn.decorator_list = [d for d in fn.decorator_list if not self._is_compile_decorator(d)]
             fl = _FunctionLowerer(self, fn)
             fn.body = fl.lower_block(fn.body, in_loop=False)
         ast.fix_missing_locations(self.tree)
