@@ -78,6 +78,8 @@ _SIGNATURES = [
     ("gm_free", None, [ctypes.c_void_p]),
     ("gm_region_compile", ctypes.c_int,
      [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p, ctypes.c_size_t]),
+    ("gm_region_load", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     ("gm_region_set_smem", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("gm_region_occupancy", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
@@ -172,16 +174,23 @@ def compile_cubin(src: str, cc: tuple[int, int] = (10, 0)) -> bytes:
 
 
 class CompiledRegion:
-    """Owner of one gm_region handle (a loaded, NVRTC-compiled kernel)."""
+    """Owner of one gm_region handle (a loaded region kernel): NVRTC-compiled
+    from `src`, or loaded from an ahead-of-time `cubin`."""
 
-    def __init__(self, src: str, kernel: str):
+    def __init__(self, src: str, kernel: str, cubin: bytes | None = None):
         h = ctypes.c_void_p()
-        log = ctypes.create_string_buffer(1 << 16)
-        check(lib().gm_region_compile(src.encode(), kernel.encode(), ctypes.byref(h), log, len(log)),
-              f"gm_region_compile({kernel})")
+        if cubin is not None:
+            check(lib().gm_region_load(cubin, len(cubin), kernel.encode(), ctypes.byref(h)),
+                  f"gm_region_load({kernel})")
+            self.log = "aot"
+        else:
+            log = ctypes.create_string_buffer(1 << 16)
+            check(lib().gm_region_compile(src.encode(), kernel.encode(), ctypes.byref(h), log, len(log)),
+                  f"gm_region_compile({kernel})")
+            self.log = log.value.decode(errors="replace")
         self.handle = h
         self.kernel = kernel
-        self.log = log.value.decode(errors="replace")
+        self.from_cache = cubin is not None
         self._smem_set = 0
 
     def occupancy(self, threads: int, smem: int) -> int:

@@ -347,6 +347,29 @@ int gm_region_compile(const char* cuda_src, const char* kernel_name, gm_region* 
   return GM_OK;
 }
 
+int gm_region_load(const void* cubin, size_t cubin_bytes, const char* kernel_name, gm_region* out) {
+  if (!cubin || !cubin_bytes || !kernel_name || !out) return fail(GM_E_INVALID, "gm_region_load: null argument");
+  if (g_device < 0) return fail(GM_E_INVALID, "gm_region_load: gm_init not called");
+  int r = ensure_ctx();
+  if (r) return r;
+  gm_region_s* reg = new gm_region_s();
+  CUresult cr = g_drv.ModuleLoadData(&reg->mod, cubin);
+  if (cr != CUDA_SUCCESS) {
+    delete reg;
+    const char* s = nullptr;
+    g_drv.GetErrorString(cr, &s);
+    return fail(GM_E_CUDA, "cuModuleLoadData(cached cubin): %s", s ? s : "?");
+  }
+  cr = g_drv.ModuleGetFunction(&reg->fn, reg->mod, kernel_name);
+  if (cr != CUDA_SUCCESS) {
+    g_drv.ModuleUnload(reg->mod);
+    delete reg;
+    return fail(GM_E_CUDA, "cuModuleGetFunction(%s) failed", kernel_name);
+  }
+  *out = reg;
+  return GM_OK;
+}
+
 int gm_region_set_smem(gm_region r, int smem_bytes) {
   if (!r) return fail(GM_E_INVALID, "gm_region_set_smem: null region");
   GM_CU(g_drv.FuncSetAttribute(r->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem_bytes));

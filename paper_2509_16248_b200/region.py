@@ -18,6 +18,8 @@ NativeError propagates.
 from __future__ import annotations
 
 import ctypes
+import hashlib
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -32,13 +34,40 @@ _kernel_cache: dict[str, nat.CompiledRegion] = {}
 _kernel_lock = threading.Lock()
 
 
+KCACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_kcache")
+
+
+def kcache_path(source: str, arch: str = "sm100a") -> str:
+    return os.path.join(KCACHE_DIR, f"{hashlib.sha1(source.encode()).hexdigest()}_{arch}.cubin")
+
+
 def compiled_kernel(source: str, kernel: str) -> nat.CompiledRegion:
+    """In-process cache, then the ahead-of-time cubin cache (filled by
+    __graft_entry__.build() for the known workloads), then NVRTC."""
     with _kernel_lock:
         k = _kernel_cache.get(source)
         if k is None:
-            k = nat.CompiledRegion(source, kernel)
+            path = kcache_path(source)
+            cubin = None
+            if os.path.exists(path):
+                with open(path, "rb") as fh:
+                    cubin = fh.read()
+            k = nat.CompiledRegion(source, kernel, cubin=cubin)
             _kernel_cache[source] = k
         return k
+
+
+def aot_compile(source: str) -> str:
+    """NVRTC-compile `source` for sm_100a into the cubin cache (no GPU)."""
+    path = kcache_path(source)
+    if not os.path.exists(path):
+        os.makedirs(KCACHE_DIR, exist_ok=True)
+        cubin = nat.compile_cubin(source, (10, 0))
+        tmp = path + ".tmp"
+        with open(tmp, "wb") as fh:
+            fh.write(cubin)
+        os.replace(tmp, path)
+    return path
 
 
 def arg_key(a) -> tuple:
@@ -235,8 +264,16 @@ class Region:
         self.stats = RegionStats()
         self.last_spec: _Spec | None = None
         self.last_args: tuple | None = None
+        # aot.py: when a list, every call's arguments are recorded here
+        self.trace = None
+        # optional (start, end) torch.cuda.Event(external=True) pair recorded
+        # around the kernel launch; captured into a CUDA graph they time the
+        # kernel inside every replay (bench.py's roofline measurement)
+        self.probe = None
 
     def __call__(self, *args):
+        if self.trace is not None:
+            self.trace.append(args)
         key = tuple(arg_key(a) for a in args)
         spec = self.specs.get(key)
         if spec is None:
@@ -248,7 +285,11 @@ class Region:
         self.stats.launches += 1
         self.last_spec = spec
         self.last_args = args
+        if self.probe is not None:
+            self.probe[0].record()
         outs = spec.run(list(args))
+        if self.probe is not None:
+            self.probe[1].record()
         return outs[0] if len(outs) == 1 else tuple(outs)
 
     def _specialise(self, args: list):

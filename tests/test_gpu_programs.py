@@ -93,3 +93,22 @@ def test_host_pipeline_matches_single_calls(programs):
     ex.flush()
     for k, o in enumerate(outs):
         assert torch.equal(o, singles[k % len(batches)]), k
+
+
+@pytest.mark.gpu
+def test_aot_cubins_are_used(programs):
+    """build() precompiled the BASELINE workloads' regions: the GPU run finds
+    the same specialisations in the cubin cache (no NVRTC at first call)."""
+    import os
+
+    from paper_2509_16248_b200 import region as reg
+
+    prog = programs["bigbird_like"]
+    spec = prog["inputs"][0]
+    args = orc.make_args(spec["args"], spec["seed"], torch.bfloat16)
+    if not any(os.path.exists(p) for p in [reg.KCACHE_DIR]):
+        pytest.skip("no AOT cache (build() not run)")
+    ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
+    ex(*[a.cuda() for a in args])
+    for r in low.regions:
+        assert r.last_spec is not None and r.last_spec.kernel.from_cache, r.name
