@@ -298,9 +298,10 @@ def main():
     # around every fused-region launch (event nodes perturb the step, so the
     # timed loop above replays the probe-free graph).
     fused = [r for r in low.regions if r.last_spec is not None]
+    probes = {}
     for r in fused:
-        r.probe = (torch.cuda.Event(enable_timing=True, external=True),
-                   torch.cuda.Event(enable_timing=True, external=True))
+        r.probe = probes[r.rid] = (torch.cuda.Event(enable_timing=True, external=True),
+                                   torch.cuda.Event(enable_timing=True, external=True))
     probed = ex.prepare(*[t.to(dev) for t in x_host], slot=7)
     probed.load([t.to(dev) for t in x_host])
     for r in fused:
@@ -311,7 +312,7 @@ def main():
         probed.run()
         torch.cuda.synchronize(dev)
         for r in fused:
-            probe_ms[r.rid].append(r.probe[0].elapsed_time(r.probe[1]))
+            probe_ms[r.rid].append(probes[r.rid][0].elapsed_time(probes[r.rid][1]))
     ex.flush()
     kernels = []
     for r in fused:
