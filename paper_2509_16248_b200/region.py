@@ -37,8 +37,20 @@ _kernel_lock = threading.Lock()
 KCACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_kcache")
 
 
+def _skeleton_digest() -> str:
+    """The cubin depends on the generated source AND on the skeleton header
+    NVRTC includes, so both key the cache."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc", "gm_region.cuh")
+    with open(path, "rb") as fh:
+        return hashlib.sha1(fh.read()).hexdigest()
+
+
+_SKELETON = _skeleton_digest()
+
+
 def kcache_path(source: str, arch: str = "sm100a") -> str:
-    return os.path.join(KCACHE_DIR, f"{hashlib.sha1(source.encode()).hexdigest()}_{arch}.cubin")
+    key = hashlib.sha1((_SKELETON + "\n" + source).encode()).hexdigest()
+    return os.path.join(KCACHE_DIR, f"{key}_{arch}.cubin")
 
 
 def compiled_kernel(source: str, kernel: str) -> nat.CompiledRegion:
