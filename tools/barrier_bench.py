@@ -1,7 +1,7 @@
 """Micro-benchmark of the grid-wide reduce + broadcast used between region
 passes: K back-to-back reduces (no other work) at the region grid, per-call
 time from CUDA events over one launch.  Variants of the protocol are defined
-here (V0 = gm::grid_reduce as shipped) to pick the fastest on B200.
+here (V0 = gm::grid_reduce as shipped (the V3 protocol)) to pick the fastest on B200.
 
     python tools/barrier_bench.py
 """
@@ -15,13 +15,10 @@ SRC = r'''
 #include "gm_region.cuh"
 using namespace gm;
 
-__device__ __forceinline__ u64 ld_relaxed64(const u64* p) {
-  u64 v; asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory"); return v;
-}
 __device__ __forceinline__ void red_release_add64(u64* p, u64 v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel() { fence_acq_rel_gpu(); }
 
 // V = variant: 1 relaxed polling + fence; 2 = 1 without nanosleep;
 // 3 = all CTAs poll the arrival counter, CTA 0 combines (red.release arrivals)
