@@ -37,6 +37,10 @@ WORKLOADS = {
     "qwen_audio_like": ("config 5: corpus qwen_audio_like at [8,1024,768]", [[8, 1024, 768]]),
     "longformer_like": ("config 3: corpus longformer_like at [4,4096,768]", [[4, 4096, 768]]),
     "biogpt_like": ("config 5: corpus biogpt_like at [8,1024,768]", [[8, 1024, 768]] * 2),
+    "blenderbot_like": ("config 5: corpus blenderbot_like at [8,1024,768]", [[8, 1024, 768]]),
+    "flan_t5_like": ("config 5: corpus flan_t5_like, [8192,768] @ [768,768]", [[8192, 768], [768, 768]]),
+    "pegasus_like": ("config 5: corpus pegasus_like at [8,1024,768]", [[8, 1024, 768]]),
+    "moe_minicpm_like": ("config 5: corpus moe_minicpm_like at [8,1024,768]", [[8, 1024, 768]]),
 }
 
 
