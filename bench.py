@@ -259,6 +259,14 @@ def main():
     entry.load([t.to(dev) for t in x_host])
     info = entry.info
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    flush_rd = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.int64, device=dev)
+
+    def flush_l2():
+        """Write 256 MB (evicts everything), then read another 256 MB so the
+        L2 holds only clean lines of the flush buffers: the next step starts
+        cold and does not pay the flush's write-backs."""
+        flush_buf.zero_()
+        flush_rd.sum()
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -285,7 +293,7 @@ def main():
                 break
         barrier()
         for i in range(args.steps):
-            flush_buf.zero_()
+            flush_l2()
             starts[i].record(stream)
             entry.run()
             ends[i].record(stream)
@@ -302,11 +310,16 @@ def main():
     kernels = []
     for r in fused:
         spec = r.last_spec
-        ms = _time_kernel_flushed(spec, list(r.last_args), flush_buf, dev)
-        kernels.append({"name": f"{spec.plan.kernel} ({r.name})", "ms": ms,
-                        "bytes": spec.bytes_alg(list(r.last_args)), "grid": spec.grid, "smem": spec.smem,
-                        "passes": spec.plan.npass,
-                        "how": "graph of 20 x (256 MB L2 flush + launch) minus 20 x flush; cold L2"})
+        ms = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev)
+        k = {"name": f"{spec.plan.kernel} ({r.name})", "ms": ms,
+             "bytes": spec.bytes_alg(list(r.last_args)), "grid": spec.grid, "smem": spec.smem,
+             "passes": spec.plan.npass, "speculative": spec.plan.spec,
+             "how": "graph of 20 x (L2 flush + launch) minus 20 x flush; cold L2"}
+        if spec.plan.spec:
+            launches, misses = spec.spec_stats()
+            k["spec_launches"], k["spec_misses"] = launches, misses
+            k["ms_mispredicted"] = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev, mispredict=True)
+        kernels.append(k)
     dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
     peak, peak_kind = _peaks()
     roofline = None
@@ -369,7 +382,7 @@ def main():
         "data": "synthetic inputs (manifest seed/dist at the BASELINE shape), random-init weights (seed 0)",
         "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
                    "shape": list(x_host[0].shape), "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2": "flushed (256 MB write) between timed steps"},
+                   "l2": "flushed between timed steps: 256 MB write, then 256 MB read (cold, clean L2)"},
         "e2e": {"value": replica_value(batch, args.steps, ws, e2e_total), "unit": "samples/s",
                 "how": "B200Executor.run_host_pipelined: pinned host inputs -> H2D -> graph replay -> D2H into "
                        "pinned host outputs, double-buffered; wall clock, max over ranks",
@@ -388,9 +401,19 @@ def main():
         pg.destroy_process_group()
 
 
-def _time_kernel_flushed(spec, args, flush_buf, dev, reps: int = 20, trials: int = 5) -> float:
-    """Average duration (ms) of one region launch with a cold L2."""
+def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5, mispredict: bool = False) -> float:
+    """Average duration (ms) of one region launch with a cold L2.  With
+    `mispredict`, every launch of a speculative region is handed the wrong
+    predictions (the exact fallback path runs)."""
     import torch
+
+    nd = len(spec.plan.decisions) if spec.plan.spec else 0
+    pred = spec.scratch[256: 256 + 4 * nd].view(torch.int32) if nd else None
+    wrong = None
+    if mispredict and nd:
+        vals = spec.scalars()
+        wrong = torch.tensor([0 if vals[spec.plan.slot[d.uid]] != 0.0 else 1 for d in spec.plan.decisions],
+                             dtype=torch.int32, device=dev)
 
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
@@ -402,11 +425,15 @@ def _time_kernel_flushed(spec, args, flush_buf, dev, reps: int = 20, trials: int
     keep = []
     with torch.cuda.graph(g_both):
         for _ in range(reps):
-            flush_buf.zero_()
+            flush()
+            if wrong is not None:
+                pred.copy_(wrong)
             keep.append(spec.run(args))
     with torch.cuda.graph(g_flush):
         for _ in range(reps):
-            flush_buf.zero_()
+            flush()
+            if wrong is not None:
+                pred.copy_(wrong)
 
     def t(g):
         g.replay()

@@ -46,8 +46,10 @@ RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "nzsum": 0, "amax"
 
 MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strided", "scalar"
 
-UNROLL = 2
 STATIC_SMEM_RESERVE = 8 * 1024
+DATA_REGS = 40          # raw-vector registers per thread: register stage + one block's loads
+VEC_REGS = {torch.float32: 8, torch.bfloat16: 4, torch.float16: 4, torch.bool: 2}
+MAX_DECISIONS = 32      # predicted decisions per speculative region (scratch ints at barrier + 256)
 
 
 def _round_f(dtype) -> str:
@@ -242,8 +244,14 @@ class Plan:
         return [o for _, o in self.pass_outputs[p]] + [r.args[0] for r in self.pass_reds[p]]
 
     def _pass_nodes(self, p: int) -> list[Node]:
-        """Elementwise nodes pass p evaluates (scalars come from s_scal, so
-        the traversal stops at them)."""
+        return self._nodes(self._pass_roots(p))
+
+    def _guards(self, p: int) -> dict[int, frozenset]:
+        return self._guards_roots(self._pass_roots(p))
+
+    def _nodes(self, roots: list[Node]) -> list[Node]:
+        """Elementwise nodes a sweep over `roots` evaluates (scalars come
+        from s_scal, so the traversal stops at them)."""
         seen: set[int] = set()
         order: list[Node] = []
 
@@ -255,13 +263,13 @@ class Plan:
                 visit(a)
             order.append(n)
 
-        for r in self._pass_roots(p):
+        for r in roots:
             visit(r)
         return order
 
-    def _guards(self, p: int) -> dict[int, frozenset]:
-        """DNF guard per elementwise node of pass p: a set of conjunctions of
-        (scalar-node uid, polarity) literals."""
+    def _guards_roots(self, roots: list[Node]) -> dict[int, frozenset]:
+        """DNF guard per elementwise node of a sweep over `roots`: a set of
+        conjunctions of (scalar-node uid, polarity) literals."""
         TRUE = frozenset()
         dnf: dict[int, set] = {}
 
@@ -291,7 +299,7 @@ class Plan:
                         break
             return True
 
-        work = [(r, TRUE) for r in self._pass_roots(p)]
+        work = [(r, TRUE) for r in roots]
         while work:
             node, conj = work.pop()
             if node.kind != "elem":
@@ -341,6 +349,8 @@ class Plan:
         L = "l"
         dst = f"n{node.uid}_{u}[{L}]"
         R = _round_f(node.dtype) if node.dtype != torch.bool else ""
+        if getattr(self, "_no_round", False):
+            R = ""
         a = node.args
         op = node.op
 
@@ -357,12 +367,10 @@ class Plan:
             dt = DT_CODE[ip.dtype]
             k = ip.slot
             if ip.mode == MODE_FULL:
-                g = self.stage_group[k]
-                if g == 0 and self._cur_pass == 0:
-                    return [f"gm::load8_stash<{dt}>(P.in[{k}], sres{k}, e{u}, le{u}, nv{u}, n{node.uid}_{u});"]
-                if g >= 0:
-                    return [f"gm::load8_res<{dt}>(P.in[{k}], sres{k}, e{u}, le{u}, nv{u}, n{node.uid}_{u});"]
-                return [f"gm::load8_gmem<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
+                if self._tail:
+                    return [f"gm::load8_gmem<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
+                pre, raw = self._raw_for(ip, u)
+                return pre + [f"gm::rcvt<{dt}>({raw}, n{node.uid}_{u});"]
             if ip.mode == MODE_PERIODIC:
                 return [f"gm::load8_periodic<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
             if ip.mode == MODE_STRIDED:
@@ -569,184 +577,534 @@ class Plan:
             return f"{dst} = {x};"
         return f"{dst} = {R}({x});" if R else f"{dst} = {x};"
 
+    # -- contexts ----------------------------------------------------------------
+    # A context is one sweep over the iteration space: exact pass p (an int),
+    # or "spec" — the speculative single pass that evaluates every pass's
+    # roots under predicted decisions.
+    def _ctx_roots(self, ctx) -> list[Node]:
+        if ctx == "spec":
+            roots: list[Node] = []
+            for p in range(self.npass):
+                roots += self._pass_roots(p)
+            return roots
+        return self._pass_roots(ctx)
+
+    def _used_scalars(self, elem_nodes: list[Node], guards: dict) -> list[Node]:
+        used: list[Node] = []
+        for n in elem_nodes:
+            for a in n.args:
+                if a.kind != "elem" and a.op != "const" and a not in used:
+                    used.append(a)
+        for conj_set in guards.values():
+            for conj in conj_set:
+                for uid, _ in conj:
+                    node = self.graph.nodes[uid]
+                    if node not in used:
+                        used.append(node)
+        return used
+
+    def _decisions(self) -> list[Node]:
+        """Scalars computed from reductions (level >= 1) that elementwise code
+        reads: the branch decisions a speculative pass predicts."""
+        out: list[Node] = []
+        for p in range(self.npass):
+            roots = self._pass_roots(p)
+            for s in self._used_scalars(self._nodes(roots), self._guards_roots(roots)):
+                if self.avail.get(s.uid, 0) >= 1 and s not in out:
+                    out.append(s)
+        return out
+
+    def _spec_ok(self) -> bool:
+        if os.environ.get("GM_SPEC", "1") == "0":
+            return False
+        if not self.reductions or self.npass < 2 or not self.decisions or len(self.decisions) > MAX_DECISIONS:
+            return False
+        return all(d.dtype == torch.bool for d in self.decisions)
+
+    # -- launch layout and staging ---------------------------------------------------
+    def _plan_layout(self) -> None:
+        """Grid, vectors per thread and staging, decided from the shape and
+        the device so the kernel source is a function of the plan key.
+
+        Every region runs 2 CTAs x 512 threads per SM (co-resident, so the
+        grid barrier is safe) over a grid-stride vector map: vector v is the
+        k = v // T-th vector of thread v % T (T = grid x 512), so at every
+        moment the whole grid sweeps one contiguous stretch of HBM.  A thread
+        issues the loads of all its vectors of a register block before any
+        arithmetic (K x 16-32 B in flight per input).
+
+        Exact multi-pass kernels keep an input a later pass re-reads in
+        registers across the grid barrier when the whole pass is one block
+        and the budget allows, else in its thread-private shared-memory slots
+        (stashed by the first pass, or prefetched with cp.async at kernel
+        start when only later passes read it).  Speculative kernels stage
+        nothing: their exact fallback re-reads (from L2 in practice)."""
+        sms, smem_optin = self.device_info
+        self.vfull = self.n // nat.VEC
+        self.minb = 2
+        self.grid = max(1, min(2 * sms, -(-max(self.vfull, 1) // nat.THREADS)))
+        self.T = self.grid * nat.THREADS
+        self.K = -(-self.vfull // self.T) if self.vfull else 0
+        self.stage = {ip.slot: "none" for ip in self.inputs}
+        self.load_pass: dict[int, int] = {}
+        self.prefetch: set[int] = set()
+        self.smem_off: dict[int, int] = {}
+        self.smem_bytes = 0
+        self.decisions = self._decisions()
+        self.spec = self._spec_ok()
+        if self.spec or not self.reductions or self.npass < 2 or not self.K \
+                or os.environ.get("GM_STAGING", "1") == "0":
+            return
+        full = [ip for ip in self.inputs if ip.mode == MODE_FULL and ip.passes]
+        multi = [ip for ip in full if len(ip.passes) >= 2 and self._unguarded_in(ip, min(ip.passes))]
+        # prefetch only inputs a later pass reads unconditionally: an input
+        # that only an untaken arm reads must cost no HBM traffic at all
+        later = [ip for ip in full if len(ip.passes) == 1 and min(ip.passes) > 0
+                 and self._unguarded_in(ip, min(ip.passes))]
+
+        def fits_regs(staged: list[InputPlan]) -> bool:
+            live = sum(self.K * VEC_REGS[ip.dtype] for ip in staged)
+            for p in range(self.npass):
+                tmp = sum(VEC_REGS[ip.dtype] for ip in self._preload_inputs(p) if ip not in staged)
+                if live + self.K * tmp > DATA_REGS:
+                    return False
+            return True
+
+        staged: list[InputPlan] = []
+        if fits_regs([]):
+            for ip in multi + later:
+                if fits_regs(staged + [ip]):
+                    staged.append(ip)
+        for ip in staged:
+            self.stage[ip.slot] = "reg"
+            self.load_pass[ip.slot] = 0 if ip in later else min(ip.passes)
+        budget = 233472 // self.minb - STATIC_SMEM_RESERVE
+        used = 0
+        for ip in multi + later:
+            if ip in staged or DT_SIZE[ip.dtype] < 2:
+                continue
+            b = (self.K * nat.THREADS * nat.VEC * DT_SIZE[ip.dtype] + 127) // 128 * 128
+            if used + b <= min(budget, smem_optin - STATIC_SMEM_RESERVE):
+                self.stage[ip.slot] = "smem"
+                self.smem_off[ip.slot] = used
+                used += b
+                if ip in later:
+                    self.prefetch.add(ip.slot)
+        self.smem_bytes = used
+
+    def _preload_inputs(self, ctx) -> list[InputPlan]:
+        """Full-size inputs a context reads unconditionally (loaded at the
+        top of each register block)."""
+        roots = self._ctx_roots(ctx)
+        nodes = self._nodes(roots)
+        guards = self._guards_roots(roots)
+        out = []
+        for n in nodes:
+            if n.op == "free" and n.kind == "elem":
+                ip = self.in_by_uid[n.uid]
+                if ip.mode == MODE_FULL and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()}))):
+                    out.append(ip)
+        return out
+
+    def _block_loads(self, ctx) -> list[tuple[InputPlan, str]]:
+        """(input, action) issued at the top of each register block of `ctx`:
+        'rs' = load into the kernel-scope register stage, 'ld' = load,
+        'ldst' = load and stash to shared memory after use, 'lds' = read the
+        stash."""
+        acts = []
+        for ip in self._preload_inputs(ctx):
+            st = self.stage[ip.slot]
+            if st == "reg":
+                if ctx == self.load_pass[ip.slot]:
+                    acts.append((ip, "rs"))
+            elif st == "smem":
+                if ip.slot in self.prefetch or ctx != min(ip.passes):
+                    acts.append((ip, "lds"))
+                else:
+                    acts.append((ip, "ldst"))
+            else:
+                acts.append((ip, "ld"))
+        if ctx == 0:
+            for ip in self.inputs:
+                if self.stage[ip.slot] == "reg" and self.load_pass[ip.slot] == 0 and min(ip.passes) > 0:
+                    acts.append((ip, "rs"))
+        return acts
+
+    def _raw_for(self, ip: InputPlan, u: int) -> tuple[list[str], str]:
+        """Statements + name of the raw vector `u` of input `ip` in the
+        current block (preloaded, register-staged, or loaded here)."""
+        k = ip.slot
+        dt = DT_CODE[ip.dtype]
+        if k in self._preloaded:
+            return [], self._preloaded[k].format(u=u)
+        if self.stage[k] == "reg":
+            return [], f"rs{k}_{u}"
+        name = f"rl{k}_{u}"
+        if self.stage[k] == "smem":
+            return [f"gm::Raw<{dt}> {name};",
+                    f"gm::rlds<{dt}>(sres{k} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), {name});"], name
+        return [f"gm::Raw<{dt}> {name};", f"gm::rload<{dt}>(P.in[{k}], e{u}, {name});"], name
+
+    # -- emission ---------------------------------------------------------------------
     def _emit(self) -> str:
         out: list[str] = []
         w = out.append
         nscal = max(1, len(self.scalars))
-        resident = self._plan_residency_flags()
-        if os.environ.get("GM_PROFILE"):
+        self._plan_layout()
+        self._tail = False
+        self._preloaded: dict[int, str] = {}
+        prof = bool(os.environ.get("GM_PROFILE"))
+        self.profiled = prof
+        if prof:
             w("#define GM_PROF 1")
         w('#include "gm_region.cuh"')
         w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
         w("#define gm_trunc(x) ((double)(long long)(x))")
         w(f"// region {self.name}: shape {list(self.shape)}, {self.npass} pass(es), "
-          f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s)")
+          f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s); grid {self.grid} x {nat.THREADS}, "
+          f"{self.K} vector(s)/thread{', speculative' if self.spec else ''}")
         w(f'extern "C" __global__ void __launch_bounds__(GM_THREADS, {self.minb})')
         w("GM_KERNEL_NAME(const __grid_constant__ gm::Params P) {")
         w("  using namespace gm;")
         w("  extern __shared__ __align__(128) unsigned char smem[];")
-
         w("  __shared__ double s_warp[GM_WARPS * GM_MAX_RED];")
         w("  __shared__ double s_red[GM_MAX_RED];")
         w(f"  __shared__ double s_scal[{nscal}];")
-        prof = bool(os.environ.get("GM_PROFILE"))
-        self.profiled = prof
+        w("  (void)s_warp; (void)s_red; (void)smem;")
         if prof:
             w("  u64* prof_ = (u64*)P.scal_out + 64;")
             w("  if (threadIdx.x == 0) atomicMin(&prof_[0], gm::globaltimer());")
-        w("  const i64 v0 = (i64)blockIdx.x * P.vpc;")
-        w("  const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;")
-        w("  (void)v1; (void)s_warp; (void)s_red;")
-        any_res = any(resident)
-
-        any_res = any(resident)
-        # first pass that reads a group-1 (prefetched) input
-        g1_first = min([min(ip.passes) for ip in self.inputs if self.stage_group[ip.slot] == 1] or [-1])
-        for ip, r in zip(self.inputs, resident):
-            if ip.mode == MODE_FULL:
-                w(f"  const u32 sres{ip.slot} = {'smem_u32(smem + P.in[%d].smem_off)' % ip.slot if r else '0u'};")
+        w(f"  const i64 T_ = {self.T}ll;  // grid threads: vector v belongs to thread v % T_")
+        w(f"  const i64 VF_ = {self.vfull}ll;  // full 8-element vectors")
+        w("  const i64 t0_ = (i64)blockIdx.x * GM_THREADS + threadIdx.x;")
+        w("  (void)T_; (void)VF_; (void)t0_;")
         for ip in self.inputs:
-            if self.stage_group[ip.slot] == 1:
-                w(f"  gm::prefetch_thread<{DT_CODE[ip.dtype]}>(P, P.in[{ip.slot}], sres{ip.slot}, v0, v1);")
-        if any(g == 1 for g in self.stage_group):
+            if ip.mode == MODE_FULL and self.stage[ip.slot] == "smem":
+                w(f"  const u32 sres{ip.slot} = smem_u32(smem + {self.smem_off[ip.slot]});")
+        for ip in self.inputs:
+            if self.stage[ip.slot] == "reg":
+                for u in range(self.K):
+                    w(f"  gm::Raw<{DT_CODE[ip.dtype]}> rs{ip.slot}_{u};")
+        if self.prefetch:
+            # cp.async of every vector a later pass reads into its stash slot
+            for slot in sorted(self.prefetch):
+                ip = self.inputs[slot]
+                dt = DT_CODE[ip.dtype]
+                w(f"  for (int k = 0; k < {self.K}; ++k) {{")
+                w("    const i64 v = t0_ + (i64)k * T_;")
+                w(f"    if (v < VF_) gm::rprefetch<{dt}>(sres{slot} + (u32)(((i64)k * GM_THREADS + threadIdx.x) * "
+                  f"GM_VEC * {DT_SIZE[ip.dtype]}), P.in[{slot}], v * GM_VEC);")
+                w("  }")
             w("  gm::cp_async_commit();")
-        # level-0 scalars
         self._emit_scalar_level(w, 0)
-        red_slot = {r.uid: i for i, r in enumerate(self.reductions)}
-        for p in range(self.npass):
-            elem_nodes = self._pass_nodes(p)
-            reds = self.pass_reds[p]
-            outs = self.pass_outputs[p]
-            if not elem_nodes and not reds and not outs:
-                continue
-            w(f"  {{ // ---- pass {p}")
-            guards = self._guards(p)
-            # uniform locals: scalars used by this pass's elementwise code
-            used_scal = []
-            for n in elem_nodes:
-                for a in n.args:
-                    if a.kind != "elem" and a.op != "const" and a not in used_scal:
-                        used_scal.append(a)
-            for conj_set in guards.values():
-                for conj in conj_set:
-                    for uid, _ in conj:
-                        node = self.graph.nodes[uid]
-                        if node not in used_scal:
-                            used_scal.append(node)
-            for s in used_scal:
-                w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
-                w(f"    const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
-                if s.op == "free" and s.kind == "host":
-                    w(f"    const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
-            for ip in self.inputs:
-                if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
-                    w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
-            for k, r in enumerate(reds):
-                if self._exact_acc(r):
-                    w(f"    double acc{k} = 0.0;")
-                else:
-                    w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
-            U = self.unroll
-            self._cur_pass = p
-            waits = []
-            if p == g1_first:
-                w("    gm::cp_async_wait_all();  // this thread's prefetched stash slots")
-            loads = [n for n in elem_nodes
-                     if n.op == "free" and not self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))]
-            # steady state: U full vectors per iteration, constant lane count
-            w("    const i64 vfull_ = (P.n / GM_VEC < v1) ? P.n / GM_VEC : v1;")
-            w("    i64 vb = v0 + threadIdx.x;")
-            w(f"    for (; vb + {U - 1} * GM_THREADS < vfull_; vb += {U} * GM_THREADS) {{")
-            self._emit_body(w, p, elem_nodes, reds, outs, guards, loads, waits, U, full=True)
-            w("    }")
-            # remainder: one vector at a time (partial last vector included)
-            w("    for (; vb < v1; vb += GM_THREADS) {")
-            self._emit_body(w, p, elem_nodes, reds, outs, guards, loads, waits, 1, full=False)
-            w("    }")
-
-            if prof:
-                w("    __syncthreads();")
-                w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{1 + 2 * p}], gm::globaltimer());")
-            if reds:
-                nr = len(reds)
-                w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
-                w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
-                w(f"    const int slots_[{nr}] = {{{', '.join(str(red_slot[r.uid]) for r in reds)}}};")
-                w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red{', prof_ + ' + str(40 + 3 * p) if prof else ''});")
-                if prof:
-                    w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{2 + 2 * p}], gm::globaltimer());")
-                w("    if (threadIdx.x == 0) {")
-                for k, r in enumerate(reds):
-                    w("      " + self._finish_reduction(r, k))
-                w("    }")
-                w("    __syncthreads();")
-                self._emit_scalar_level(w, p + 1)
+        self.red_index = {r.uid: i for i, r in enumerate(self.reductions)}
+        if self.spec:
+            nd = len(self.decisions)
+            w(f"  __shared__ int s_pred[{nd}];")
+            w("  __shared__ int s_miss;")
+            w("  int* pred_ = (int*)(P.barrier + 256);  // predicted decisions (last launch's)")
+            w("  if (threadIdx.x == 0) {")
+            w(f"    for (int j = 0; j < {nd}; ++j) s_pred[j] = ((volatile int*)pred_)[j];")
             w("  }")
+            w("  __syncthreads();")
+            self._emit_ctx(w, "spec")
+            w("  if (!s_miss) {")
+            self._emit_epilogue(w, "    ", miss=False)
+            w("    return;")
+            w("  }")
+            w("  // misprediction: the exact multi-pass path (inputs re-read)")
+        for p in range(self.npass):
+            self._emit_ctx(w, p)
         if prof:
             w("  __syncthreads();")
             w("  if (threadIdx.x == 0) atomicMax(&prof_[63], gm::globaltimer());")
-        # scalar outputs and the debug mirror
-        w("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
+        self._emit_epilogue(w, "  ", miss=self.spec)
+        w("}")
+        return "\n".join(out) + "\n"
+
+    def _emit_epilogue(self, w, ind: str, miss: bool) -> None:
+        """Scalar outputs, the debug mirror and (speculative kernels) the
+        prediction update + hit/miss counters, by CTA 0 thread 0."""
+        w(f"{ind}if (blockIdx.x == 0 && threadIdx.x == 0) {{")
         for j, o in enumerate(self.outputs):
             if o.kind == "dscalar":
                 k = self._out_slot(j)
                 val = self._sv(o)
                 if o.dtype == torch.int64:
-                    w(f"    *(long long*)P.out[{k}].ptr = (long long){val};")
+                    w(f"{ind}  *(long long*)P.out[{k}].ptr = (long long){val};")
                 elif o.dtype == torch.int32:
-                    w(f"    *(int*)P.out[{k}].ptr = (int){val};")
+                    w(f"{ind}  *(int*)P.out[{k}].ptr = (int){val};")
                 else:
-                    w(f"    gm::store_scalar<{DT_CODE[o.dtype]}>(P.out[{k}], {val});")
-        w("    if (P.scal_out) {")
-        w(f"      for (int i = 0; i < {len(self.scalars)}; ++i) ((double*)P.scal_out)[i] = s_scal[i];")
-        w("    }")
-        w("  }")
-        w("}")
-        return "\n".join(out) + "\n"
+                    w(f"{ind}  gm::store_scalar<{DT_CODE[o.dtype]}>(P.out[{k}], {val});")
+        w(f"{ind}  if (P.scal_out) {{")
+        w(f"{ind}    for (int i = 0; i < {len(self.scalars)}; ++i) ((double*)P.scal_out)[i] = s_scal[i];")
+        w(f"{ind}  }}")
+        if self.spec:
+            w(f"{ind}  u64* st_ = (u64*)(P.barrier + 128);  // [launches, mispredictions]")
+            w(f"{ind}  st_[0] += 1;")
+            if miss:
+                w(f"{ind}  st_[1] += 1;")
+                for j, d in enumerate(self.decisions):
+                    w(f"{ind}  pred_[{j}] = (s_scal[{self.slot[d.uid]}] != 0.0) ? 1 : 0;")
+        w(f"{ind}}}")
 
-    def _emit_body(self, w, p, elem_nodes, reds, outs, guards, loads, waits, U, full):
-        if full and not os.environ.get("GM_NO_PACKED"):
-            pref = self._packed_plan(elem_nodes)
-            if any(v == "P" for v in pref.values()):
-                self._emit_body_packed(w, elem_nodes, reds, outs, guards, loads, U, pref)
-                return
+    def _emit_ctx(self, w, ctx) -> None:
+        spec = ctx == "spec"
+        roots = self._ctx_roots(ctx)
+        elem_nodes = self._nodes(roots)
+        guards = self._guards_roots(roots)
+        if spec:
+            reds = list(self.reductions)
+            outs = [jo for p in range(self.npass) for jo in self.pass_outputs[p]]
+        else:
+            reds = self.pass_reds[ctx]
+            outs = self.pass_outputs[ctx]
+        if not elem_nodes and not reds and not outs:
+            return
+        w(f"  {{ // ---- {'speculative pass (every pass under predicted decisions)' if spec else f'pass {ctx}'}")
+        for s in self._used_scalars(elem_nodes, guards):
+            if spec and self.avail.get(s.uid, 0) >= 1:
+                j = self.decisions.index(s)
+                w(f"    const float sf{s.uid} = s_pred[{j}] ? 1.f : 0.f; (void)sf{s.uid};")
+                w(f"    const bool sb{s.uid} = s_pred[{j}] != 0; (void)sb{s.uid};")
+            else:
+                w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
+                w(f"    const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
+            if s.op == "free" and s.kind == "host":
+                w(f"    const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
+        for ip in self.inputs:
+            if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
+                w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
+        for k, r in enumerate(reds):
+            if self._exact_acc(r):
+                w(f"    double acc{k} = 0.0;")
+            else:
+                w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
+        if self.prefetch and not spec and ctx == min(min(self.inputs[s].passes) for s in self.prefetch):
+            w("    gm::cp_async_wait_all();  // this thread's prefetched stash slots")
+        loads = self._block_loads(ctx)
+        if self.K:
+            tmp = sum(VEC_REGS[ip.dtype] for ip, a in loads if a != "rs")
+            if any(st == "reg" for st in self.stage.values()):
+                kb = self.K                      # register staging: one block by construction
+            else:
+                kb = self.K if self.K * tmp <= DATA_REGS else max(1, DATA_REGS // max(1, tmp))
+                nblk = -(-self.K // kb)
+                kb = -(-self.K // nblk)
+            pref = None
+            if not os.environ.get("GM_NO_PACKED"):
+                pp = self._packed_plan(elem_nodes)
+                if any(v == "P" for v in pp.values()):
+                    pref = pp
+            if kb >= self.K:
+                w("    {")
+                self._emit_block(w, "0", self.K, elem_nodes, reds, outs, guards, loads, pref)
+                w("    }")
+            else:
+                w(f"    for (int kb = 0; kb < {self.K}; kb += {kb}) {{")
+                self._emit_block(w, "kb", kb, elem_nodes, reds, outs, guards, loads, pref)
+                w("    }")
+        if self.n % nat.VEC:
+            self._emit_tail(w, elem_nodes, reds, outs, guards)
+        prof = self.profiled
+        if prof:
+            w("    __syncthreads();")
+            idx = 1 + 2 * (self.npass if spec else ctx)
+            w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{idx}], gm::globaltimer());")
+        if reds:
+            nr = len(reds)
+            w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
+            w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
+            w(f"    const int slots_[{nr}] = {{{', '.join(str(self.red_index[r.uid]) for r in reds)}}};")
+            w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red);")
+            if prof:
+                idx = 2 + 2 * (self.npass if spec else ctx)
+                w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{idx}], gm::globaltimer());")
+            if spec:
+                # replay the scalar levels in order with the exact statistics
+                # and compare every predicted decision
+                w("    if (threadIdx.x == 0) {")
+                for p in range(self.npass):
+                    for r in self.pass_reds[p]:
+                        w("      " + self._finish_reduction(r, self.red_index[r.uid]))
+                    for n in self.scalars:
+                        if self.avail[n.uid] == p + 1 and n.op not in REDUCE:
+                            w("      " + self._scalar_code(n))
+                w("      int miss_ = 0;")
+                for j, d in enumerate(self.decisions):
+                    w(f"      miss_ |= ((s_scal[{self.slot[d.uid]}] != 0.0) != (s_pred[{j}] != 0)) ? 1 : 0;")
+                w("      s_miss = miss_;")
+                w("    }")
+                w("    __syncthreads();")
+            else:
+                w("    if (threadIdx.x == 0) {")
+                for k, r in enumerate(reds):
+                    w("      " + self._finish_reduction(r, k))
+                w("    }")
+                w("    __syncthreads();")
+                self._emit_scalar_level(w, ctx + 1)
+        w("  }")
+
+    def _emit_block(self, w, kb: str, U: int, elem_nodes, reds, outs, guards, loads, pref) -> None:
+        """One register block: U vectors per thread, every load issued first."""
         ind = "      "
         for u in range(U):
-            w(f"{ind}const i64 e{u} = (vb + {u} * GM_THREADS) * GM_VEC;")
-            if full:
-                w(f"{ind}const int nv{u} = GM_VEC;")
+            k = f"({kb} + {u})" if kb != "0" else f"{u}"
+            w(f"{ind}const i64 v{u} = t0_ + (i64){k} * T_;")
+            if kb == "0" and (u + 1) * self.T <= self.vfull:
+                w(f"{ind}const bool ok{u} = true;  // t0_ < T_: every thread has its vector {u}")
             else:
-                w(f"{ind}const int nv{u} = (int)((P.n - e{u}) < GM_VEC ? (P.n - e{u}) : GM_VEC);")
-            w(f"{ind}const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
-        for st in waits:
-            w(f"{ind}stage_wait({st}, vb + {U - 1} * GM_THREADS - v0);")
+                w(f"{ind}const bool ok{u} = v{u} < VF_;")
+            w(f"{ind}const i64 e{u} = v{u} * GM_VEC;")
+            w(f"{ind}const int nv{u} = GM_VEC; (void)nv{u};")
+            w(f"{ind}const i64 le{u} = ((i64){k} * GM_THREADS + threadIdx.x) * GM_VEC; (void)le{u};")
+        self._preloaded = {}
+        for ip, act in loads:
+            dt = DT_CODE[ip.dtype]
+            k = ip.slot
+            if act == "rs":
+                self._preloaded[k] = f"rs{k}_{{u}}"
+                continue
+            self._preloaded[k] = f"r{k}_{{u}}"
+            for u in range(U):
+                w(f"{ind}gm::Raw<{dt}> r{k}_{u};")
         for u in range(U):
+            for ip, act in loads:
+                dt = DT_CODE[ip.dtype]
+                k = ip.slot
+                if act in ("rs", "ld", "ldst"):
+                    dst = f"rs{k}_{u}" if act == "rs" else f"r{k}_{u}"
+                    w(f"{ind}if (ok{u}) gm::rload<{dt}>(P.in[{k}], e{u}, {dst});")
+                else:
+                    w(f"{ind}if (ok{u}) gm::rlds<{dt}>(sres{k} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), r{k}_{u});")
+        if pref is None:
+            pref = {n.uid: "F" for n in elem_nodes}
+        needs: dict[int, set] = {n.uid: {pref[n.uid]} for n in elem_nodes}
+        for n in elem_nodes:
+            for a in n.args:
+                if a.kind == "elem":
+                    needs[a.uid].add(pref[n.uid] if (pref[n.uid] == "P" and not (n.op == "where" and a is n.args[0]))
+                                     else "F")
+        for r in reds:
+            needs[r.args[0].uid].add("F")
+        for _, o in outs:
+            needs[o.uid].add(pref[o.uid])
+        # nodes some consumer reads unpacked (float lanes)
+        self._f_consumers = {}
+        for n in elem_nodes:
+            for a in n.args:
+                if a.kind == "elem" and (pref[n.uid] == "F" or (n.op == "where" and a is n.args[0])):
+                    self._f_consumers[a.uid] = True
+        for r in reds:
+            self._f_consumers[r.args[0].uid] = True
+        for _, o in outs:
+            if pref[o.uid] == "F":
+                self._f_consumers[o.uid] = True
+        for u in range(U):
+            w(f"{ind}if (ok{u}) {{")
             for n in elem_nodes:
-                w(f"{ind}float n{n.uid}_{u}[GM_VEC];")
-        for u in range(U):
-            for n in loads:
-                for line in self._elem_code(n, u):
-                    w(ind + line.replace("\n", "\n" + ind))
-        for u in range(U):
+                if "F" in needs[n.uid]:
+                    w(f"{ind}  float n{n.uid}_{u}[GM_VEC];")
+                if "P" in needs[n.uid]:
+                    w(f"{ind}  u32 p{n.uid}_{u}[4];")
             cur_guard = None
             open_block = False
             for n in elem_nodes:
-                if n in loads:
-                    continue
                 g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
                 if g != cur_guard:
                     if open_block:
-                        w(f"{ind}}}")
+                        w(f"{ind}  }}")
                         open_block = False
                     if g:
-                        w(f"{ind}if ({g}) {{")
+                        w(f"{ind}  if ({g}) {{")
                         open_block = True
                     cur_guard = g
-                for line in self._elem_code(n, u):
-                    w(ind + "  " + line.replace("\n", "\n" + ind + "  "))
+                for line in self._node_code(n, u, pref, needs):
+                    w(ind + "    " + line.replace("\n", "\n" + ind + "    "))
             if open_block:
-                w(f"{ind}}}")
-            self._emit_reds_outs(w, ind, reds, outs, u)
+                w(f"{ind}  }}")
+            self._emit_reds_outs(w, ind + "  ", reds, outs, u, pref)
+            for ip, act in loads:
+                if act == "ldst":
+                    w(f"{ind}  gm::rstash<{DT_CODE[ip.dtype]}>(sres{ip.slot} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), "
+                      f"r{ip.slot}_{u});")
+            w(f"{ind}}}")
+        self._preloaded = {}
+
+    def _emit_tail(self, w, elem_nodes, reds, outs, guards) -> None:
+        """The partial last vector (n % 8 lanes), owned by thread VF_ % T_;
+        per-lane global loads and stores."""
+        ind = "      "
+        w("    if (t0_ == VF_ % T_) {")
+        w(f"{ind}const i64 e0 = VF_ * GM_VEC;")
+        w(f"{ind}const int nv0 = (int)({self.n}ll - e0);")
+        w(f"{ind}const i64 le0 = 0; (void)le0;")
+        self._tail = True
+        for n in elem_nodes:
+            w(f"{ind}float n{n.uid}_0[GM_VEC];")
+        cur_guard = None
+        open_block = False
+        for n in elem_nodes:
+            g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
+            if g != cur_guard:
+                if open_block:
+                    w(f"{ind}}}")
+                    open_block = False
+                if g:
+                    w(f"{ind}if ({g}) {{")
+                    open_block = True
+                cur_guard = g
+            for line in self._elem_code(n, 0):
+                w(ind + "  " + line.replace("\n", "\n" + ind + "  "))
+        if open_block:
+            w(f"{ind}}}")
+        self._emit_reds_outs(w, ind, reds, outs, 0)
+        self._tail = False
+        w("    }")
+
+    def _node_code(self, n: Node, u: int, pref: dict, needs: dict) -> list[str]:
+        def convert() -> list[str]:
+            out = []
+            if pref[n.uid] == "P" and "F" in needs[n.uid]:
+                out.append(f"gm::unpack8(p{n.uid}_{u}, n{n.uid}_{u});")
+            if pref[n.uid] == "F" and "P" in needs[n.uid]:
+                out.append(f"gm::pack8(n{n.uid}_{u}, p{n.uid}_{u});")
+            return out
+
+        if pref[n.uid] == "F":
+            # a bf16 node only read packed: pack8's RN conversion is its rounding
+            self._no_round = (n.dtype == torch.bfloat16 and "P" in needs[n.uid]
+                              and not self._f_consumers.get(n.uid))
+            try:
+                return self._elem_code(n, u) + convert()
+            finally:
+                self._no_round = False
+        dst = f"p{n.uid}_{u}"
+        if n.op == "free":
+            pre, raw = self._raw_for(self.in_by_uid[n.uid], u)
+            return pre + [f"#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = {raw}.w[j];"] + convert()
+
+        def pv(a: Node) -> str:
+            return f"p{a.uid}_{u}[j]" if a.kind == "elem" else self._packed_scalar(a)
+
+        a = n.args
+        if n.op in ("add", "sub", "mul"):
+            fn = {"add": "gm::hadd2", "sub": "gm::hsub2", "mul": "gm::hmul2"}[n.op]
+            body = f"{fn}({pv(a[0])}, {pv(a[1])})"
+        elif n.op == "neg":
+            body = f"({pv(a[0])} ^ 0x80008000u)"
+        elif n.op == "abs":
+            body = f"({pv(a[0])} & 0x7fff7fffu)"
+        elif n.op == "pos":
+            body = pv(a[0])
+        elif n.op == "where":
+            c = a[0]
+            return [f"if (sb{c.uid}) {{\n#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = p{a[1].uid}_{u}[j];\n}} "
+                    f"else {{\n#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = p{a[2].uid}_{u}[j];\n}}"] + convert()
+        else:
+            raise AssertionError(n.op)
+        return [f"#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = {body};"] + convert()
+
 
     # -- packed bf16x2 path ------------------------------------------------------
     @staticmethod
@@ -801,98 +1159,6 @@ class Plan:
             b = self._bf16_bits(s.value)
             return f"0x{(b << 16) | b:08x}u"
         return f"spk{s.uid}"
-
-    def _emit_body_packed(self, w, elem_nodes, reds, outs, guards, loads, U, pref):
-        """Steady-state body (U full vectors) with packed bf16 nodes."""
-        ind = "      "
-        needs: dict[int, set] = {n.uid: {pref[n.uid]} for n in elem_nodes}
-        for n in elem_nodes:
-            for a in n.args:
-                if a.kind == "elem":
-                    needs[a.uid].add(pref[n.uid] if (pref[n.uid] == "P" and not (n.op == "where" and a is n.args[0]))
-                                     else "F")
-        for r in reds:
-            needs[r.args[0].uid].add("F")
-        for u in range(U):
-            w(f"{ind}const i64 e{u} = (vb + {u} * GM_THREADS) * GM_VEC;")
-            w(f"{ind}const int nv{u} = GM_VEC; (void)nv{u};")
-            w(f"{ind}const i64 le{u} = e{u} - v0 * GM_VEC; (void)le{u};")
-        for u in range(U):
-            for n in elem_nodes:
-                if "F" in needs[n.uid]:
-                    w(f"{ind}float n{n.uid}_{u}[GM_VEC];")
-                if "P" in needs[n.uid]:
-                    w(f"{ind}u32 p{n.uid}_{u}[4];")
-
-        def convert(n: Node, u: int) -> list[str]:
-            out = []
-            if pref[n.uid] == "P" and "F" in needs[n.uid]:
-                out.append(f"gm::unpack8(p{n.uid}_{u}, n{n.uid}_{u});")
-            if pref[n.uid] == "F" and "P" in needs[n.uid]:
-                out.append(f"gm::pack8(n{n.uid}_{u}, p{n.uid}_{u});")
-            return out
-
-        def node_code(n: Node, u: int) -> list[str]:
-            if pref[n.uid] == "F":
-                return self._elem_code(n, u) + convert(n, u)
-            dst = f"p{n.uid}_{u}"
-            if n.op == "free":
-                ip = self.in_by_uid[n.uid]
-                k = ip.slot
-                g = self.stage_group[k]
-                if g == 0 and self._cur_pass == 0:
-                    code = f"gm::stash_raw(P.in[{k}], sres{k}, e{u}, le{u}, {dst});"
-                elif g >= 0:
-                    code = f"gm::lds_raw(sres{k}, le{u}, {dst});"
-                else:
-                    code = f"gm::ldg_raw(P.in[{k}], e{u}, {dst});"
-                return [code] + convert(n, u)
-
-            def pv(a: Node) -> str:
-                return f"p{a.uid}_{u}[j]" if a.kind == "elem" else self._packed_scalar(a)
-
-            a = n.args
-            if n.op in ("add", "sub", "mul"):
-                fn = {"add": "gm::hadd2", "sub": "gm::hsub2", "mul": "gm::hmul2"}[n.op]
-                body = f"{fn}({pv(a[0])}, {pv(a[1])})"
-            elif n.op == "neg":
-                body = f"({pv(a[0])} ^ 0x80008000u)"
-            elif n.op == "abs":
-                body = f"({pv(a[0])} & 0x7fff7fffu)"
-            elif n.op == "pos":
-                body = pv(a[0])
-            elif n.op == "where":
-                c = a[0]
-                return [f"if (sb{c.uid}) {{\n#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = p{a[1].uid}_{u}[j];\n}} "
-                        f"else {{\n#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = p{a[2].uid}_{u}[j];\n}}"] + convert(n, u)
-            else:
-                raise AssertionError(n.op)
-            return [f"#pragma unroll\nfor (int j = 0; j < 4; ++j) {dst}[j] = {body};"] + convert(n, u)
-
-        for u in range(U):
-            for n in loads:
-                for line in node_code(n, u):
-                    w(ind + line.replace("\n", "\n" + ind))
-        for u in range(U):
-            cur_guard = None
-            open_block = False
-            for n in elem_nodes:
-                if n in loads:
-                    continue
-                g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
-                if g != cur_guard:
-                    if open_block:
-                        w(f"{ind}}}")
-                        open_block = False
-                    if g:
-                        w(f"{ind}if ({g}) {{")
-                        open_block = True
-                    cur_guard = g
-                for line in node_code(n, u):
-                    w(ind + "  " + line.replace("\n", "\n" + ind + "  "))
-            if open_block:
-                w(f"{ind}}}")
-            self._emit_reds_outs(w, ind, reds, outs, u, pref)
 
     def _emit_reds_outs(self, w, ind, reds, outs, u, pref=None):
         for k, r in enumerate(reds):
@@ -961,64 +1227,3 @@ class Plan:
                 return k
             k += 1
         raise AssertionError(j)
-
-    # -- residency --------------------------------------------------------------
-    def _plan_residency_flags(self) -> list[bool]:
-        """Launch shape and shared-memory staging, decided from the shape and
-        the device so the kernel source is a function of the plan key.
-
-        Multi-pass regions stage every input some pass re-reads (read from
-        HBM once) and, space permitting, prefetch the inputs later passes
-        read once (their HBM reads then overlap pass 0 and the grid barrier).
-        Two CTAs per SM (32 warps) when the staged chunks fit in half the SM's
-        shared memory, else one.  Single-pass regions stream (no staging)."""
-        nvec = -(-self.n // nat.VEC) if self.n else 0
-        sms, smem_optin = self.device_info
-        self.unroll = UNROLL if self.reductions else 4
-        self.minb = 2 if self.reductions else 1
-        self.smem_off = {}
-        self.res_grid, self.res_vpc, self.res_smem = None, None, 0
-        self.stage_group = [-1] * len(self.inputs)
-        flags = [False] * len(self.inputs)
-        self.resident_flags = flags
-        if not self.reductions or not nvec or os.environ.get("GM_STAGING", "1") == "0":
-            return flags
-        stageable = [ip for ip in self.inputs
-                     if ip.mode == MODE_FULL and ip.passes and DT_SIZE[ip.dtype] >= 2
-                     and (self.n * DT_SIZE[ip.dtype]) % 16 == 0]
-        multi = [ip for ip in stageable if len(ip.passes) >= 2]
-        first0 = []  # read by pass 0 only: streaming is optimal, nothing to stash
-        # prefetch only inputs a later pass reads unconditionally: an input
-        # that only an untaken arm reads must cost no HBM traffic at all
-        later = [ip for ip in stageable if len(ip.passes) < 2 and 0 not in ip.passes
-                 and self._unguarded_in(ip, min(ip.passes))]
-        per_sm = 233472  # B200 shared memory per SM (228 KB)
-        for minb in (2, 1):
-            grid0 = max(1, min(minb * sms, -(-nvec // (nat.THREADS * self.unroll))))
-            vpc0 = -(-nvec // grid0)
-            budget = (per_sm // minb - STATIC_SMEM_RESERVE) if minb > 1 else smem_optin - STATIC_SMEM_RESERVE
-
-            def nbytes(ip):
-                return (vpc0 * nat.VEC * DT_SIZE[ip.dtype] + 127) // 128 * 128
-
-            if sum(nbytes(ip) for ip in multi) > budget and minb > 1:
-                continue
-            used = 0
-            chosen = []
-            for ip in multi + first0 + later:
-                b = nbytes(ip)
-                if used + b <= budget:
-                    chosen.append((ip, used))
-                    used += b
-            if not chosen:
-                break
-            self.minb = minb
-            for ip, off in chosen:
-                self.smem_off[ip.slot] = off
-                flags[ip.slot] = True
-                ip.resident = True
-                self.stage_group[ip.slot] = 0 if 0 in ip.passes else 1
-            self.res_grid, self.res_vpc, self.res_smem = grid0, vpc0, used
-            break
-        self.resident_flags = flags
-        return flags

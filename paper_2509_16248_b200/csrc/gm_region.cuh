@@ -114,7 +114,14 @@ __device__ __forceinline__ float frcp(float a) {
   asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(a));
   return y;
 }
-__device__ __forceinline__ float sigmoid(float a) { return frcp(1.f + fexp(-a)); }
+// sigmoid: ex2 / rcp on the SFU with flush-to-zero (1 + 2^y reads a denormal
+// 2^y as 1 anyway; only results below 1.2e-38 flush) — 2 MUFU, no fix-ups
+__device__ __forceinline__ float sigmoid(float a) {
+  float e, y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(a * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(1.f + e));
+  return y;
+}
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
 __device__ __forceinline__ float neg(float a) { return -a; }
 // NaN-propagating max/min (torch.maximum / Tensor.max semantics)
@@ -495,6 +502,73 @@ __device__ __forceinline__ void prefetch_thread(const Params& P, const InDesc& d
     const u32 s = sres + (u32)(le * E::ES);
 #pragma unroll
     for (int b = 0; b < GM_VEC * E::ES; b += 16) cp_async16(s + b, g + b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// raw vectors.  The generated loops issue every load of a register block
+// (one 8-element vector per input per k) before any arithmetic, so a thread
+// keeps K x 16-32 bytes per input in flight; the raw 32-bit words are kept
+// as loaded and converted (or used packed) where a node reads them.
+// Vector v of the iteration space belongs to thread v % T (T = grid x
+// GM_THREADS) as its k = v / T-th vector; its thread-private shared-memory
+// slot is (k * GM_THREADS + threadIdx.x) — the `le` element index below.
+// ---------------------------------------------------------------------------
+template <int DT> struct Raw;
+template <> struct Raw<GM_DT_F32> { u32 w[8]; };
+template <> struct Raw<GM_DT_BF16> { u32 w[4]; };
+template <> struct Raw<GM_DT_F16> { u32 w[4]; };
+template <> struct Raw<GM_DT_BOOL> { u32 w[2]; };
+
+template <int DT>
+__device__ __forceinline__ void rload(const InDesc& d, i64 e, Raw<DT>& r) {
+  const char* g = (const char*)d.ptr + e * Elem<DT>::ES;
+  if (DT == GM_DT_BOOL) {
+    ldg8b(g, r.w[0], r.w[1]);
+  } else {
+#pragma unroll
+    for (int b = 0; b < (int)(sizeof(Raw<DT>) / 16); ++b) ldg16(g + 16 * b, r.w[4 * b], r.w[4 * b + 1], r.w[4 * b + 2], r.w[4 * b + 3]);
+  }
+}
+template <int DT>
+__device__ __forceinline__ void rstash(u32 s, const Raw<DT>& r) {
+  if (DT == GM_DT_BOOL) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(s), "r"(r.w[0]), "r"(r.w[1]) : "memory");
+  } else {
+#pragma unroll
+    for (int b = 0; b < (int)(sizeof(Raw<DT>) / 16); ++b) sts16(s + 16 * b, r.w[4 * b], r.w[4 * b + 1], r.w[4 * b + 2], r.w[4 * b + 3]);
+  }
+}
+template <int DT>
+__device__ __forceinline__ void rlds(u32 s, Raw<DT>& r) {
+  if (DT == GM_DT_BOOL) {
+    lds8b(s, r.w[0], r.w[1]);
+  } else {
+#pragma unroll
+    for (int b = 0; b < (int)(sizeof(Raw<DT>) / 16); ++b) lds16(s + 16 * b, r.w[4 * b], r.w[4 * b + 1], r.w[4 * b + 2], r.w[4 * b + 3]);
+  }
+}
+// cp.async (LDGSTS) of one vector into its stash slot (16-byte types only)
+template <int DT>
+__device__ __forceinline__ void rprefetch(u32 s, const InDesc& d, i64 e) {
+  const char* g = (const char*)d.ptr + e * Elem<DT>::ES;
+#pragma unroll
+  for (int b = 0; b < (int)(sizeof(Raw<DT>) / 16); ++b) cp_async16(s + 16 * b, g + 16 * b);
+}
+template <int DT>
+__device__ __forceinline__ void rcvt(const Raw<DT>& r, float (&x)[8]) {
+  if (DT == GM_DT_F32) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __uint_as_float(r.w[k]);
+  } else if (DT == GM_DT_BOOL) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[k] = ((r.w[0] >> (8 * k)) & 0xffu) ? 1.f : 0.f;
+      x[4 + k] = ((r.w[1] >> (8 * k)) & 0xffu) ? 1.f : 0.f;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Elem16<DT>::unpack(r.w[j], x[2 * j], x[2 * j + 1]);
   }
 }
 

@@ -113,24 +113,14 @@ class _Spec:
         n = plan.n
         nvec = -(-n // nat.VEC) if n else 0
         threads = nat.THREADS
-        if plan.res_grid is not None:
-            grid, vpc, smem = plan.res_grid, plan.res_vpc, plan.res_smem
+        grid, smem = plan.grid, plan.smem_bytes
+        vpc = plan.K
+        if plan.reductions and grid > 1:
+            # the grid barrier needs every CTA resident at once
             occ = self.kernel.occupancy(threads, smem)
-            if occ < 1:
-                raise nat.NativeError(f"region {region.name}: resident plan does not fit ({smem} B smem)")
-        elif plan.reductions:
-            occ = max(1, self.kernel.occupancy(threads, 0))
-            grid = max(1, min(sms * occ, -(-nvec // (threads * plan.unroll)) if nvec else 1))
-            vpc = -(-nvec // grid) if nvec else 0
-            smem = 0
-        else:
-            # pure map: no grid barrier; persistent grid of SMs x occupancy
-            occ = max(1, self.kernel.occupancy(threads, 0))
-            grid = max(1, min(sms * occ, -(-nvec // (threads * plan.unroll)) if nvec else 1))
-            vpc = -(-nvec // grid) if nvec else 0
-            smem = 0
-        if vpc:
-            grid = max(1, -(-nvec // vpc))
+            if occ * sms < grid:
+                raise nat.NativeError(f"region {region.name}: {grid} CTAs not co-resident "
+                                      f"({occ}/SM at {smem} B smem, {sms} SMs)")
         self.grid, self.vpc, self.smem, self.threads = grid, vpc, smem, threads
         self.nred = len(plan.reductions)
         self.nscal = len(plan.scalars)
@@ -153,7 +143,7 @@ class _Spec:
         self.in_slots = []  # (slot, free_index, mode)
         for ip in plan.inputs:
             d = P.inp[ip.slot]
-            d.smem_off = plan.smem_off.get(ip.slot, -1) if plan.res_grid is not None else -1
+            d.smem_off = plan.smem_off.get(ip.slot, -1)
             if ip.mode == MODE_PERIODIC:
                 t = args[ip.free_index]
                 d.size[0] = t.numel()
@@ -249,6 +239,12 @@ class _Spec:
         t = self.scratch[off: off + 8 * 64].view(torch.int64)
         t.zero_()
         t[0] = 2 ** 62
+
+    def spec_stats(self) -> tuple[int, int]:
+        """(launches, mispredictions) of a speculative region (syncs; tests
+        and bench)."""
+        v = self.scratch[128:144].view(torch.int64).tolist()
+        return int(v[0]), int(v[1])
 
     def status(self) -> int:
         """Grid-barrier status word (syncs; diagnostics only)."""

@@ -110,5 +110,6 @@ def test_aot_cubins_are_used(programs):
         pytest.skip("no AOT cache (build() not run)")
     ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
     ex(*[a.cuda() for a in args])
+    ex.flush()
     for r in low.regions:
         assert r.last_spec is not None and r.last_spec.kernel.from_cache, r.name

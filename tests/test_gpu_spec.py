@@ -1,0 +1,72 @@
+"""Speculative regions on the B200 (codegen.Plan.spec): a region whose later
+passes depend on its reductions only through boolean branch decisions runs
+one pass under the decisions of the previous launch, verifies them after one
+grid-wide reduction, and falls back to the exact multi-pass path in the same
+launch on a misprediction.  Results must not depend on the prediction: the
+same CUDA graph is replayed over inputs whose branch decisions alternate, and
+every output is compared with the reference's CPU eager run."""
+
+import pytest
+import torch
+
+from oracle import executor as orc
+from paper_2509_16248_b200 import harness
+from parity import assert_parity
+
+CASES = [
+    # (program, dtype, shapes): decisions differ across the manifest inputs
+    ("bigbird_like", torch.bfloat16, None),
+    ("bigbird_like", torch.float32, None),
+    ("phi4_like", torch.float32, [[8, 1024, 768]]),
+    ("qwen_audio_like", torch.bfloat16, [[8, 1024, 768]]),
+    ("phi4_like", torch.float32, None),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,dtype,shapes", CASES,
+                         ids=[f"{c[0]}-{str(c[1])[6:]}-{'big' if c[2] else 'own'}" for c in CASES])
+def test_alternating_decisions_one_graph(programs, name, dtype, shapes):
+    prog = programs[name]
+    inputs = [orc.make_args(s["args"], s["seed"], dtype, shapes) for s in prog["inputs"]]
+    refs = [orc.run_reference(prog["transformed"], prog["callable"], a, dtype) for a in inputs]
+    ex, mod, low, _ = harness.b200_program(name, dtype=dtype)
+    order = list(range(len(inputs))) * 2 + list(reversed(range(len(inputs))))
+    for i in order:
+        out, text = harness.call_captured(ex, [a.cuda() for a in inputs[i]])
+        ref_out, ref_text = refs[i]
+        assert_parity(out, ref_out, dtype, what=f"{name} input {i}")
+        assert text == ref_text
+    assert len(ex.info()) == 1 and ex.info()[0].mode == "graph"
+    spec = [r.last_spec for r in low.regions if r.last_spec is not None and r.last_spec.plan.spec]
+    assert spec, "no speculative region"
+    launches = sum(s.spec_stats()[0] for s in spec)
+    misses = sum(s.spec_stats()[1] for s in spec)
+    assert launches >= len(order)
+    # the manifest inputs force different arms, so some launches mispredict
+    # (exact fallback ran) and replays of a repeated input hit
+    assert 0 < misses < launches, (launches, misses)
+
+
+@pytest.mark.gpu
+def test_forced_mispredictions_match_hits(programs):
+    """Same inputs, predictions overwritten with the wrong decisions before
+    every launch: the exact fallback's outputs equal the speculative ones."""
+    prog = programs["bigbird_like"]
+    s = prog["inputs"][0]
+    args = [a.cuda() for a in orc.make_args(s["args"], s["seed"], torch.bfloat16)]
+    ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
+    hit = ex(*args).clone()
+    ex.flush()
+    for r in low.regions:
+        sp = r.last_spec
+        nd = len(sp.plan.decisions)
+        vals = sp.scalars()
+        wrong = [0 if vals[sp.plan.slot[d.uid]] != 0.0 else 1 for d in sp.plan.decisions]
+        sp.scratch[256: 256 + 4 * nd].view(torch.int32).copy_(torch.tensor(wrong, dtype=torch.int32))
+    before = [r.last_spec.spec_stats()[1] for r in low.regions]
+    miss = ex(*args).clone()
+    ex.flush()
+    after = [r.last_spec.spec_stats()[1] for r in low.regions]
+    assert all(a == b + 1 for a, b in zip(after, before)), (before, after)
+    assert torch.equal(hit, miss)

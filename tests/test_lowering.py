@@ -112,24 +112,34 @@ def test_region_codegen_compiles_for_sm100a(programs, name, dtype):
         assert cubin[:4] == b"\x7fELF"
 
 
-def test_uniform_select_guards_untaken_arm(programs):
+def test_uniform_select_guards_untaken_arm(programs, monkeypatch):
     """bigbird region 0: `hidden` is read only by the else arm, so its load
     sits under the negated predicate and never happens when the then arm is
-    selected (the reference evaluates both arms, transform.py:404-412)."""
+    selected (the reference evaluates both arms, transform.py:404-412) — in
+    the speculative pass and in the exact fallback passes alike."""
     mod, low = lowering.load(programs["bigbird_like"]["transformed"])
     r = low.regions[0]
     args = [torch.randn(8, 64, 768), 0.125, torch.randn(8, 64, 768)]
     plan = codegen.Plan(r.graph, r.out_nodes, args, r.name, allow_cpu=True)
     assert plan.npass == 2 and len(plan.reductions) == 1
+    assert plan.spec and len(plan.decisions) == 1
+    src = plan.source
+    for marker in ("// ---- speculative pass", "// ---- pass 1"):
+        i = src.index(marker)
+        j = src.index("P.in[1]", i)
+        assert "if ((!sb" in src[i:j], marker
+    # exact (non-speculative) specialisation: q is read by both passes and
+    # stays in registers across the grid barrier; hidden is read only by the
+    # else arm of pass 1, so it is not prefetched (an untaken arm must cost
+    # no HBM traffic) and loads lazily under the guard
+    monkeypatch.setenv("GM_SPEC", "0")
+    plan = codegen.Plan(r.graph, r.out_nodes, args, r.name, allow_cpu=True)
+    assert not plan.spec
+    assert plan.stage == {0: "reg", 1: "none"}
     src = plan.source
     i = src.index("// ---- pass 1")
-    key = "sres1" if plan.stage_group[1] >= 0 else "P.in[1]"
-    j = src.index(key + ",", i) if key == "sres1" else src.index(key, i)
+    j = src.index("P.in[1]", i)
     assert "if ((!sb" in src[i:j]
-    # q is read by both passes: stashed by pass 0 (group 0); hidden is read
-    # only by the else arm of pass 1, so it is not prefetched (an untaken arm
-    # must cost no HBM traffic) and loads lazily under the guard
-    assert plan.stage_group == [0, -1]
 
 
 def test_boolean_predicates_lowered():
