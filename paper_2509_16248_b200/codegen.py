@@ -910,7 +910,8 @@ class Plan:
         if prof:
             w("    __syncthreads();")
             idx = 1 + 2 * (self.npass if spec else ctx)
-            w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{idx}], gm::globaltimer());")
+            w(f"    if (threadIdx.x == 0) {{ const u64 t_ = gm::globaltimer(); atomicMax(&prof_[{idx}], t_); "
+              f"atomicMin(&prof_[{32 + idx}], t_); }}")
         if reds:
             nr = len(reds)
             w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")

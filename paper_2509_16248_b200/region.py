@@ -232,13 +232,14 @@ class _Spec:
         off = SCRATCH_PARTIALS + 8 * max(1, self.nred) * self.grid + 8 * 64
         v = self.scratch[off: off + 8 * 64].view(torch.int64).tolist()
         t0 = v[0]
-        return [x - t0 if x else 0 for x in v]
+        return [x - t0 if x and x < 2 ** 62 else 0 for x in v]
 
     def reset_timeline(self) -> None:
         off = SCRATCH_PARTIALS + 8 * max(1, self.nred) * self.grid + 8 * 64
         t = self.scratch[off: off + 8 * 64].view(torch.int64)
         t.zero_()
         t[0] = 2 ** 62
+        t[32:40] = 2 ** 62   # per-pass earliest CTA finish (atomicMin)
 
     def spec_stats(self) -> tuple[int, int]:
         """(launches, mispredictions) of a speculative region (syncs; tests
