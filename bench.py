@@ -408,7 +408,9 @@ def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5
     import torch
 
     nd = len(spec.plan.decisions) if spec.plan.spec else 0
-    pred = spec.scratch[256: 256 + 4 * nd].view(torch.int32) if nd else None
+    from paper_2509_16248_b200.region import SCRATCH_PRED
+
+    pred = spec.scratch[SCRATCH_PRED: SCRATCH_PRED + 4 * nd].view(torch.int32) if nd else None
     wrong = None
     if mispredict and nd:
         vals = spec.scalars()
@@ -418,7 +420,7 @@ def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(side):
-        spec.run(args)  # warm (allocator, module)
+        spec.run(args, pdl=False)  # warm (allocator, module)
     torch.cuda.current_stream(dev).wait_stream(side)
     torch.cuda.synchronize(dev)
     g_both, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -428,7 +430,7 @@ def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5
             flush()
             if wrong is not None:
                 pred.copy_(wrong)
-            keep.append(spec.run(args))
+            keep.append(spec.run(args, pdl=False))  # the kernel's own duration
     with torch.cuda.graph(g_flush):
         for _ in range(reps):
             flush()

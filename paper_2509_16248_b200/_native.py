@@ -26,6 +26,7 @@ MAX_DIMS = 6
 MAX_PIECES = 16
 THREADS = 512
 VEC = 8
+LAUNCH_PDL = 1   # GM_LAUNCH_PDL
 
 
 class NativeError(RuntimeError):
@@ -86,6 +87,9 @@ _SIGNATURES = [
     ("gm_region_launch", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int,
       ctypes.c_void_p]),
+    ("gm_region_launch_ex", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+      ctypes.c_void_p, ctypes.c_int]),
     ("gm_region_release", ctypes.c_int, [ctypes.c_void_p]),
     ("gm_region_params_bytes", ctypes.c_size_t, []),
     ("gm_branch_select_scratch_bytes", ctypes.c_size_t, []),
@@ -201,11 +205,11 @@ class CompiledRegion:
         check(lib().gm_region_occupancy(self.handle, threads, smem, ctypes.byref(n)), "gm_region_occupancy")
         return n.value
 
-    def launch(self, params: Params, grid: int, threads: int, smem: int, stream: int) -> None:
+    def launch(self, params: Params, grid: int, threads: int, smem: int, stream: int, pdl: bool = False) -> None:
         check(
-            lib().gm_region_launch(self.handle, ctypes.byref(params), ctypes.sizeof(params), grid, threads, smem,
-                                   ctypes.c_void_p(stream)),
-            f"gm_region_launch({self.kernel})",
+            lib().gm_region_launch_ex(self.handle, ctypes.byref(params), ctypes.sizeof(params), grid, threads, smem,
+                                      ctypes.c_void_p(stream), LAUNCH_PDL if pdl else 0),
+            f"gm_region_launch_ex({self.kernel})",
         )
 
     def __del__(self):

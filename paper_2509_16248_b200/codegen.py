@@ -49,7 +49,7 @@ MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strid
 STATIC_SMEM_RESERVE = 8 * 1024
 DATA_REGS = 40          # raw-vector registers per thread: register stage + one block's loads
 VEC_REGS = {torch.float32: 8, torch.bfloat16: 4, torch.float16: 4, torch.bool: 2}
-MAX_DECISIONS = 32      # predicted decisions per speculative region (scratch ints at barrier + 256)
+MAX_DECISIONS = 24      # predicted decisions per speculative region (scratch ints at barrier + 288)
 
 
 def _round_f(dtype) -> str:
@@ -778,6 +778,9 @@ class Plan:
         w(f"  const i64 VF_ = {self.vfull}ll;  // full 8-element vectors")
         w("  const i64 t0_ = (i64)blockIdx.x * GM_THREADS + threadIdx.x;")
         w("  (void)T_; (void)VF_; (void)t0_;")
+        # programmatic dependent launch: wait for the previous kernel's
+        # results before the first global read (a no-op without PDL)
+        w('  asm volatile("griddepcontrol.wait;" ::: "memory");')
         for ip in self.inputs:
             if ip.mode == MODE_FULL and self.stage[ip.slot] == "smem":
                 w(f"  const u32 sres{ip.slot} = smem_u32(smem + {self.smem_off[ip.slot]});")
@@ -802,7 +805,7 @@ class Plan:
             nd = len(self.decisions)
             w(f"  __shared__ int s_pred[{nd}];")
             w("  __shared__ int s_miss;")
-            w("  int* pred_ = (int*)(P.barrier + 256);  // predicted decisions (last launch's)")
+            w("  int* pred_ = (int*)(P.barrier + GM_SCRATCH_PRED);  // predicted decisions (last launch's)")
             w("  if (threadIdx.x == 0) {")
             w(f"    for (int j = 0; j < {nd}; ++j) s_pred[j] = ((volatile int*)pred_)[j];")
             w("  }")
@@ -840,7 +843,7 @@ class Plan:
         w(f"{ind}    for (int i = 0; i < {len(self.scalars)}; ++i) ((double*)P.scal_out)[i] = s_scal[i];")
         w(f"{ind}  }}")
         if self.spec:
-            w(f"{ind}  u64* st_ = (u64*)(P.barrier + 128);  // [launches, mispredictions]")
+            w(f"{ind}  u64* st_ = (u64*)(P.barrier + GM_SCRATCH_STATS);  // [launches, mispredictions]")
             w(f"{ind}  st_[0] += 1;")
             if miss:
                 w(f"{ind}  st_[1] += 1;")

@@ -753,15 +753,16 @@ __device__ __forceinline__ void st_release64(u64* p, u64 v) {
 }
 
 // Scratch layout behind P.barrier (zeroed once, reused by every launch); the
-// counter, the flag and the results sit on separate 128-byte lines so the
-// pollers never contend with the arrivals:
+// arrivals and the broadcast sit on separate 128-byte lines:
 //   +0    u64 arrival counter (monotonic across launches and passes)
 //   +16   int status (1 = barrier timeout)
-//   +128  u64 epoch flag: number of completed grid reductions
-//   +256  double results[GM_MAX_RED] published by the combining CTA
+//   +32   u64 [speculative launches, mispredictions] (CTA 0, kernel end)
+//   +288  int predicted decisions of a speculative region
 // and P.partials = double[slot][gridDim.x] at +GM_SCRATCH_PARTIALS.
-#define GM_SCRATCH_FLAG 128
-#define GM_SCRATCH_RESULTS 256
+#define GM_SCRATCH_STATS 32     // u64 [speculative launches, mispredictions]
+#define GM_SCRATCH_FLAG 128     // (free: tools/barrier_bench.py protocol variants)
+#define GM_SCRATCH_RESULTS 136
+#define GM_SCRATCH_PRED 288     // int[24] predicted decisions (speculative regions)
 #define GM_SCRATCH_PARTIALS 384
 
 // GM_PROF: optional timeline stamps (atomicMax over CTAs) for diagnostics

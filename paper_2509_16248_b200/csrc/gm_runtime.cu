@@ -64,6 +64,7 @@ struct DriverApi {
   CUresult (*ModuleUnload)(CUmodule) = nullptr;
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            CUstream, void**, void**) = nullptr;
+  CUresult (*LaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
   CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
@@ -80,6 +81,7 @@ int load_driver() {
   GM_SYM(ModuleGetFunction, "cuModuleGetFunction");
   GM_SYM(ModuleUnload, "cuModuleUnload");
   GM_SYM(LaunchKernel, "cuLaunchKernel");
+  GM_SYM(LaunchKernelEx, "cuLaunchKernelEx");
   GM_SYM(FuncSetAttribute, "cuFuncSetAttribute");
   GM_SYM(OccupancyMaxActiveBlocksPerMultiprocessor, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
   GM_SYM(CtxGetCurrent, "cuCtxGetCurrent");
@@ -394,6 +396,35 @@ int gm_region_launch(gm_region r, const void* params, size_t params_bytes, int g
   }
   void* args[1] = {const_cast<void*>(params)};
   GM_CU(g_drv.LaunchKernel(r->fn, grid, 1, 1, threads, 1, 1, smem_bytes, (CUstream)stream, args, nullptr));
+  return GM_OK;
+}
+
+int gm_region_launch_ex(gm_region r, const void* params, size_t params_bytes, int grid, int threads, int smem_bytes,
+                        void* stream, int flags) {
+  if (!(flags & GM_LAUNCH_PDL)) return gm_region_launch(r, params, params_bytes, grid, threads, smem_bytes, stream);
+  if (!r || !params) return fail(GM_E_INVALID, "gm_region_launch_ex: null argument");
+  if (params_bytes != sizeof(gm::Params))
+    return fail(GM_E_INVALID, "gm_region_launch_ex: params %zu bytes, expected %zu", params_bytes, sizeof(gm::Params));
+  if (smem_bytes > r->smem) {
+    int e = gm_region_set_smem(r, smem_bytes);
+    if (e) return e;
+  }
+  CUlaunchAttribute attr[1];
+  memset(attr, 0, sizeof(attr));
+  attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr[0].value.programmaticStreamSerializationAllowed = 1;
+  CUlaunchConfig cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDimX = grid;
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = threads;
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = smem_bytes;
+  cfg.hStream = (CUstream)stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[1] = {const_cast<void*>(params)};
+  GM_CU(g_drv.LaunchKernelEx(&cfg, r->fn, args, nullptr));
   return GM_OK;
 }
 

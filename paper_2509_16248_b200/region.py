@@ -30,10 +30,13 @@ from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
 from .ir import Graph, Node, Unsupported
 
 SCRATCH_PARTIALS = 384  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
+SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [speculative launches, mispredictions]
+SCRATCH_PRED = 288      # GM_SCRATCH_PRED: int predicted decisions
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
 _kernel_lock = threading.Lock()
 
 
+PDL = os.environ.get("GM_PDL", "1") != "0"
 KCACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_kcache")
 
 
@@ -173,7 +176,11 @@ class _Spec:
                 k += 1
         self.shape = tuple(plan.shape)
 
-    def run(self, args: list):
+    def run(self, args: list, pdl: bool | None = None):
+        """Launch on the current stream.  `pdl` (default: GM_PDL, on) makes it
+        a programmatic dependent launch: the CTAs become resident while the
+        previous kernel drains and wait (griddepcontrol.wait) for its results
+        before reading anything."""
         P = nat.Params()
         ctypes.memmove(ctypes.byref(P), ctypes.byref(self.template), ctypes.sizeof(P))
         for slot, fi in self.in_slots:
@@ -193,7 +200,7 @@ class _Spec:
                 P.out[k].ptr = t.data_ptr()
                 outs[j] = t
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        self.kernel.launch(P, self.grid, self.threads, self.smem, stream)
+        self.kernel.launch(P, self.grid, self.threads, self.smem, stream, PDL if pdl is None else pdl)
         return outs
 
     def bytes_alg(self, args: list) -> int:
@@ -244,7 +251,7 @@ class _Spec:
     def spec_stats(self) -> tuple[int, int]:
         """(launches, mispredictions) of a speculative region (syncs; tests
         and bench)."""
-        v = self.scratch[128:144].view(torch.int64).tolist()
+        v = self.scratch[SCRATCH_STATS:SCRATCH_STATS + 16].view(torch.int64).tolist()
         return int(v[0]), int(v[1])
 
     def status(self) -> int:

@@ -11,6 +11,7 @@ import torch
 
 from oracle import executor as orc
 from paper_2509_16248_b200 import harness
+from paper_2509_16248_b200 import region as reg
 from parity import assert_parity
 
 CASES = [
@@ -63,7 +64,7 @@ def test_forced_mispredictions_match_hits(programs):
         nd = len(sp.plan.decisions)
         vals = sp.scalars()
         wrong = [0 if vals[sp.plan.slot[d.uid]] != 0.0 else 1 for d in sp.plan.decisions]
-        sp.scratch[256: 256 + 4 * nd].view(torch.int32).copy_(torch.tensor(wrong, dtype=torch.int32))
+        sp.scratch[reg.SCRATCH_PRED: reg.SCRATCH_PRED + 4 * nd].view(torch.int32).copy_(torch.tensor(wrong, dtype=torch.int32))
     before = [r.last_spec.spec_stats()[1] for r in low.regions]
     miss = ex(*args).clone()
     ex.flush()
