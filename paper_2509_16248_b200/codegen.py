@@ -806,10 +806,6 @@ class Plan:
             w(f"  __shared__ int s_pred[{nd}];")
             w("  __shared__ int s_miss;")
             w("  int* pred_ = (int*)(P.barrier + GM_SCRATCH_PRED);  // predicted decisions (last launch's)")
-            w("  if (threadIdx.x == 0) {")
-            w(f"    for (int j = 0; j < {nd}; ++j) s_pred[j] = ((volatile int*)pred_)[j];")
-            w("  }")
-            w("  __syncthreads();")
             self._emit_ctx(w, "spec")
             w("  if (!s_miss) {")
             self._emit_epilogue(w, "    ", miss=False)
@@ -865,11 +861,15 @@ class Plan:
         if not elem_nodes and not reds and not outs:
             return
         w(f"  {{ // ---- {'speculative pass (every pass under predicted decisions)' if spec else f'pass {ctx}'}")
+        # values read from global memory are loaded after the first block's
+        # data loads are issued (`late`), so their round trip overlaps them
+        late: list[str] = []
         for s in self._used_scalars(elem_nodes, guards):
             if spec and self.avail.get(s.uid, 0) >= 1:
                 j = self.decisions.index(s)
-                w(f"    const float sf{s.uid} = s_pred[{j}] ? 1.f : 0.f; (void)sf{s.uid};")
-                w(f"    const bool sb{s.uid} = s_pred[{j}] != 0; (void)sb{s.uid};")
+                w(f"    float sf{s.uid} = 0.f; bool sb{s.uid} = false; (void)sf{s.uid}; (void)sb{s.uid};")
+                late.append(f"{{ int pd_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(pd_) : \"l\"(pred_ + {j})); "
+                            f"sf{s.uid} = pd_ ? 1.f : 0.f; sb{s.uid} = pd_ != 0; if (threadIdx.x == 0) s_pred[{j}] = pd_; }}")
             else:
                 w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
                 w(f"    const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
@@ -877,7 +877,9 @@ class Plan:
                 w(f"    const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
         for ip in self.inputs:
             if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
-                w(f"    const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
+                w(f"    float sin{ip.slot} = 0.f;")
+                late.append(f"sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
+        self._late = late
         for k, r in enumerate(reds):
             if self._exact_acc(r):
                 w(f"    double acc{k} = 0.0;")
@@ -886,6 +888,27 @@ class Plan:
         if self.prefetch and not spec and ctx == min(min(self.inputs[s].passes) for s in self.prefetch):
             w("    gm::cp_async_wait_all();  // this thread's prefetched stash slots")
         loads = self._block_loads(ctx)
+        prof = self.profiled
+        nr = len(reds)
+        pidx = self.npass if spec else ctx
+        pargs = f", prof_ + 40 + 4 * {pidx}" if prof else ""
+        if reds:
+            w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
+            w(f"    const int slots_[{nr}] = {{{', '.join(str(self.red_index[r.uid]) for r in reds)}}};")
+            w("    u64 tgt_ = 0; (void)tgt_;")
+
+        def stamp_loop_end():
+            if prof:
+                idx = 1 + 2 * pidx
+                w("    __syncthreads();")
+                w(f"    if (threadIdx.x == 0) {{ const u64 t_ = gm::globaltimer(); atomicMax(&prof_[{idx}], t_); "
+                  f"atomicMin(&prof_[{32 + idx}], t_); }}")
+
+        def arrive():
+            w(f"    {{ double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
+            w(f"      tgt_ = grid_arrive(P, {nr}, ops_, slots_, vals_, s_warp, s_red{pargs}); }}")
+
+        deferred = False
         if self.K:
             tmp = sum(VEC_REGS[ip.dtype] for ip, a in loads if a != "rs")
             if any(st == "reg" for st in self.stage.values()):
@@ -900,29 +923,36 @@ class Plan:
                 if any(v == "P" for v in pp.values()):
                     pref = pp
             if kb >= self.K:
+                # one block: with reductions, the block's output stores are
+                # issued after the grid arrival (held in registers until then)
+                deferred = bool(reds) and bool(outs) and os.environ.get("GM_DEFER_STORES", "1") != "0"
                 w("    {")
-                self._emit_block(w, "0", self.K, elem_nodes, reds, outs, guards, loads, pref)
+                self._emit_block(w, "0", self.K, elem_nodes, reds, outs, guards, loads, pref, defer=deferred)
+                if deferred:
+                    if self.n % nat.VEC:
+                        w("    {")
+                        self._emit_tail(w, elem_nodes, reds, outs, guards)
+                        w("    }")
+                    stamp_loop_end()
+                    arrive()
+                    self._emit_deferred_stores(w, "      ", outs, self.K, pref)
                 w("    }")
             else:
                 w(f"    for (int kb = 0; kb < {self.K}; kb += {kb}) {{")
                 self._emit_block(w, "kb", kb, elem_nodes, reds, outs, guards, loads, pref)
                 w("    }")
-        if self.n % nat.VEC:
-            self._emit_tail(w, elem_nodes, reds, outs, guards)
-        prof = self.profiled
-        if prof:
-            w("    __syncthreads();")
-            idx = 1 + 2 * (self.npass if spec else ctx)
-            w(f"    if (threadIdx.x == 0) {{ const u64 t_ = gm::globaltimer(); atomicMax(&prof_[{idx}], t_); "
-              f"atomicMin(&prof_[{32 + idx}], t_); }}")
+        if not deferred:
+            if self.n % nat.VEC:
+                for line in self._late:
+                    w("    " + line)
+                self._emit_tail(w, elem_nodes, reds, outs, guards)
+            stamp_loop_end()
+            if reds:
+                arrive()
         if reds:
-            nr = len(reds)
-            w(f"    double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
-            w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
-            w(f"    const int slots_[{nr}] = {{{', '.join(str(self.red_index[r.uid]) for r in reds)}}};")
-            w(f"    grid_reduce(P, {nr}, ops_, slots_, vals_, s_warp, s_red);")
+            w(f"    grid_wait(P, {nr}, ops_, slots_, tgt_, s_red{pargs});")
             if prof:
-                idx = 2 + 2 * (self.npass if spec else ctx)
+                idx = 2 + 2 * pidx
                 w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{idx}], gm::globaltimer());")
             if spec:
                 # replay the scalar levels in order with the exact statistics
@@ -949,8 +979,10 @@ class Plan:
                 self._emit_scalar_level(w, ctx + 1)
         w("  }")
 
-    def _emit_block(self, w, kb: str, U: int, elem_nodes, reds, outs, guards, loads, pref) -> None:
-        """One register block: U vectors per thread, every load issued first."""
+    def _emit_block(self, w, kb: str, U: int, elem_nodes, reds, outs, guards, loads, pref, defer=False) -> None:
+        """One register block: U vectors per thread, every load issued first.
+        With `defer`, outputs are kept in registers (ho*) for stores issued by
+        the caller after the grid arrival."""
         ind = "      "
         for u in range(U):
             k = f"({kb} + {u})" if kb != "0" else f"{u}"
@@ -981,6 +1013,8 @@ class Plan:
                     w(f"{ind}if (ok{u}) gm::rload<{dt}>(P.in[{k}], e{u}, {dst});")
                 else:
                     w(f"{ind}if (ok{u}) gm::rlds<{dt}>(sres{k} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), r{k}_{u});")
+        for line in self._late:
+            w(ind + line)
         if pref is None:
             pref = {n.uid: "F" for n in elem_nodes}
         needs: dict[int, set] = {n.uid: {pref[n.uid]} for n in elem_nodes}
@@ -1004,6 +1038,13 @@ class Plan:
         for _, o in outs:
             if pref[o.uid] == "F":
                 self._f_consumers[o.uid] = True
+        if defer:
+            for u in range(U):
+                for j, o in outs:
+                    if pref.get(o.uid) == "P":
+                        w(f"{ind}u32 ho{j}_{u}[4];")
+                    else:
+                        w(f"{ind}float ho{j}_{u}[GM_VEC];")
         for u in range(U):
             w(f"{ind}if (ok{u}) {{")
             for n in elem_nodes:
@@ -1027,7 +1068,7 @@ class Plan:
                     w(ind + "    " + line.replace("\n", "\n" + ind + "    "))
             if open_block:
                 w(f"{ind}  }}")
-            self._emit_reds_outs(w, ind + "  ", reds, outs, u, pref)
+            self._emit_reds_outs(w, ind + "  ", reds, outs, u, pref, hold=defer)
             for ip, act in loads:
                 if act == "ldst":
                     w(f"{ind}  gm::rstash<{DT_CODE[ip.dtype]}>(sres{ip.slot} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), "
@@ -1164,7 +1205,18 @@ class Plan:
             return f"0x{(b << 16) | b:08x}u"
         return f"spk{s.uid}"
 
-    def _emit_reds_outs(self, w, ind, reds, outs, u, pref=None):
+    def _emit_deferred_stores(self, w, ind, outs, U, pref) -> None:
+        for u in range(U):
+            w(f"{ind}if (ok{u}) {{")
+            for j, o in outs:
+                k = self._out_slot(j)
+                if pref is not None and pref.get(o.uid) == "P":
+                    w(f"{ind}  gm::stg_raw(P.out[{k}], e{u}, ho{j}_{u});")
+                else:
+                    w(f"{ind}  gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, ho{j}_{u});")
+            w(f"{ind}}}")
+
+    def _emit_reds_outs(self, w, ind, reds, outs, u, pref=None, hold=False):
         for k, r in enumerate(reds):
             x = r.args[0]
             src = f"n{x.uid}_{u}"
@@ -1182,6 +1234,12 @@ class Plan:
                 w(f"{ind}acc{k} = gm::acc8({RED_OP[r.op]}, acc{k}, {src}, nv{u});")
         for j, o in outs:
             k = self._out_slot(j)
+            if hold:
+                if pref is not None and pref.get(o.uid) == "P":
+                    w(f"{ind}#pragma unroll\n{ind}for (int j_ = 0; j_ < 4; ++j_) ho{j}_{u}[j_] = p{o.uid}_{u}[j_];")
+                else:
+                    w(f"{ind}#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) ho{j}_{u}[l] = n{o.uid}_{u}[l];")
+                continue
             if pref is not None and pref.get(o.uid) == "P":
                 w(f"{ind}gm::stg_raw(P.out[{k}], e{u}, p{o.uid}_{u});")
             else:

@@ -785,24 +785,17 @@ __device__ __forceinline__ u64 ld_relaxed64(const u64* p) {
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// Reduce `nr` per-thread values across the grid; the results land in s_out[r]
-// in every CTA.
-//   1. CTA partial: warp butterfly, then warp 0 over the warps (fixed tree);
-//      thread 0 stores the partials and arrives on the arrival counter
-//      (atom.acq_rel: the partial stores are released with the arrival).
-//   2. Thread 0 polls the counter (relaxed loads, one acquire fence after)
-//      until it reaches the next multiple of gridDim.x — the counter is
-//      monotonic across passes and launches, so it never needs a reset.
-//   3. Every CTA combines all partials itself: warp r handles reduction r,
-//      16 independent loads per lane per round, then a fixed butterfly.
-// Same inputs, same tree in every CTA: bit-identical results everywhere and
-// in every run, with no second round trip to publish them (measured on
-// B200 by tools/barrier_bench.py: ~2.5 us per reduce at 296 CTAs, against
-// ~3.5 us for a last-arriver combine + broadcast).  The grid is sized to be
-// co-resident (<= SMs x occupancy); a 2 s %globaltimer bound turns a
-// residency violation into status=1, not a hang.
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
-                                            double* vals, double* s_warp, double* s_out, u64* prof = nullptr) {
+                                            double* vals, double* s_warp, double* s_out, u64* prof = nullptr);
+
+// First half of grid_reduce: the CTA partials are published and the CTA
+// arrives.  Returns the arrival target (thread 0; 0 elsewhere, and for a
+// one-CTA grid, whose results are already in s_out).  Stores a thread issues
+// between grid_arrive and grid_wait are not ordered before the arrival's
+// release, so the generated passes issue their output stores there: the
+// release does not wait for them to drain and they overlap the barrier.
+__device__ __forceinline__ u64 grid_arrive(const Params& P, int nr, const int* ops, const int* slots,
+                                           double* vals, double* s_warp, double* s_out, u64* prof = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r = 0; r < nr; ++r) {
     const double v = warp_combine(ops[r], vals[r]);
@@ -823,16 +816,32 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
       }
     }
   }
-  if (!multi) {
+  if (!multi) return 0;
+  GM_STAMP(0);
+  u64 target = 0;
+  if (threadIdx.x == 0) {
+    const u64 g = gridDim.x;
+    const u64 old = atom_add_acq_rel64((u64*)P.barrier, 1ull);
+    target = (old / g + 1) * g;
+#ifdef GM_PROF
+    if (prof) atomicMax(&prof[3], globaltimer());  // arrival completed (after the release)
+#endif
+  }
+  return target;
+}
+
+// Second half: thread 0 waits for the epoch (relaxed polls, one acquire
+// fence), then every CTA combines all partials itself in the same fixed
+// order (bit-identical results in every CTA, no second round trip).
+__device__ __forceinline__ void grid_wait(const Params& P, int nr, const int* ops, const int* slots, u64 target,
+                                          double* s_out, u64* prof = nullptr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (gridDim.x == 1) {
     __syncthreads();
     return;
   }
-  GM_STAMP(0);
   if (threadIdx.x == 0) {
     u64* cnt = (u64*)P.barrier;
-    const u64 g = gridDim.x;
-    const u64 old = atom_add_acq_rel64(cnt, 1ull);
-    const u64 target = (old / g + 1) * g;
     const u64 t0 = globaltimer();
     int spins = 0;
     while (ld_relaxed64(cnt) < target) {
@@ -845,6 +854,7 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
   }
   __syncthreads();
   GM_STAMP(1);
+  const double* partials = (const double*)P.partials;
   for (int r = warp; r < nr; r += GM_WARPS) {
     const double* base = partials + (i64)slots[r] * gridDim.x;
     double acc = red_identity(ops[r]);
@@ -863,6 +873,28 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
   }
   __syncthreads();
   GM_STAMP(2);
+}
+
+// Reduce `nr` per-thread values across the grid; the results land in s_out[r]
+// in every CTA.
+//   1. CTA partial: warp butterfly, then warp 0 over the warps (fixed tree);
+//      thread 0 stores the partials and arrives on the arrival counter
+//      (atom.acq_rel: the partial stores are released with the arrival).
+//   2. Thread 0 polls the counter (relaxed loads, one acquire fence after)
+//      until it reaches the next multiple of gridDim.x — the counter is
+//      monotonic across passes and launches, so it never needs a reset.
+//   3. Every CTA combines all partials itself: warp r handles reduction r,
+//      16 independent loads per lane per round, then a fixed butterfly.
+// Same inputs, same tree in every CTA: bit-identical results everywhere and
+// in every run, with no second round trip to publish them (measured on
+// B200 by tools/barrier_bench.py: ~2.5 us per reduce at 296 CTAs, against
+// ~3.5 us for a last-arriver combine + broadcast).  The grid is sized to be
+// co-resident (<= SMs x occupancy); a 2 s %globaltimer bound turns a
+// residency violation into status=1, not a hang.
+__device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
+                                            double* vals, double* s_warp, double* s_out, u64* prof) {
+  const u64 target = grid_arrive(P, nr, ops, slots, vals, s_warp, s_out, prof);
+  grid_wait(P, nr, ops, slots, target, s_out, prof);
 }
 
 // Per-thread float accumulation of one 8-lane vector (masked to nv lanes).

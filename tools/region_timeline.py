@@ -43,7 +43,7 @@ def main():
             torch.cuda.synchronize()
             tl = spec.timeline()
             rows.append({"event_us": 1e3 * s.elapsed_time(e), "timeline_ns": [v for v in tl[:32] if v], "first_cta_done_ns": [v for v in tl[32:40] if v],
-                         "barrier_ns": [v for v in tl[40:63] if v]})
+                         "barrier_ns (per reduce: last CTA before arrival, arrival done, poll done, combine done)": [v for v in tl[40:63] if v]})
         print(json.dumps({"region": r.name, "grid": spec.grid, "smem": spec.smem, "passes": spec.plan.npass,
                           "runs": rows[-2:]}))
 
