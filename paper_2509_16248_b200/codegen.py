@@ -641,8 +641,8 @@ class Plan:
         nothing: their exact fallback re-reads (from L2 in practice)."""
         sms, smem_optin = self.device_info
         self.vfull = self.n // nat.VEC
-        self.minb = 2
-        self.grid = max(1, min(2 * sms, -(-max(self.vfull, 1) // nat.THREADS)))
+        self.minb = int(os.environ.get("GM_CTAS_PER_SM", "2"))
+        self.grid = max(1, min(self.minb * sms, -(-max(self.vfull, 1) // nat.THREADS)))
         self.T = self.grid * nat.THREADS
         self.K = -(-self.vfull // self.T) if self.vfull else 0
         self.stage = {ip.slot: "none" for ip in self.inputs}
@@ -923,9 +923,10 @@ class Plan:
                 if any(v == "P" for v in pp.values()):
                     pref = pp
             if kb >= self.K:
-                # one block: with reductions, the block's output stores are
-                # issued after the grid arrival (held in registers until then)
-                deferred = bool(reds) and bool(outs) and os.environ.get("GM_DEFER_STORES", "1") != "0"
+                # one block: optionally (GM_DEFER_STORES=1) the block's output
+                # stores are held in registers and issued after the grid
+                # arrival; measured neutral on B200 (tools/ab_regions.py)
+                deferred = bool(reds) and bool(outs) and os.environ.get("GM_DEFER_STORES", "0") == "1"
                 w("    {")
                 self._emit_block(w, "0", self.K, elem_nodes, reds, outs, guards, loads, pref, defer=deferred)
                 if deferred:

@@ -6,20 +6,25 @@
 // the arm expressions (transform.py:395-423) and the `torch.where` selects
 // (transform.py:374-376), plus the elementwise statements around them.
 //
-// Execution model (one launch, persistent CTAs, at most one per SM):
+// Execution model (one launch, 2 co-resident CTAs x 512 threads per SM):
 //   * the iteration space (n elements, row-major) is cut into 8-element
-//     vectors; CTA b owns the contiguous vectors [b*vpc, (b+1)*vpc);
+//     vectors; vector v belongs to thread v % T (T = grid x 512) as its
+//     k = v / T-th vector, so at any moment the grid sweeps one contiguous
+//     stretch of HBM.  A thread issues the loads of all its vectors of a
+//     register block (K x 16-32 B per input) before any arithmetic;
 //   * pass p evaluates the elementwise code that only needs scalars known
 //     before p, accumulates the reductions of pass p and stores the outputs
 //     of pass p; after a pass with reductions every CTA publishes one partial
-//     per reduction, a self-resetting grid barrier runs, and every CTA
-//     combines the partials in the same fixed order (bit-identical scalars in
-//     all CTAs, run-to-run deterministic) — no host readback, no .item();
-//   * inputs read by more than one pass are staged once into shared memory
-//     with cp.async.bulk (bulk-copy engine, mbarrier complete_tx) and stay
-//     resident: 148 SMs x ~200 KB hold a 25 MB activation, so a predicate
-//     input is read from HBM exactly once;
-//   * everything else streams with 128-bit ld.global.nc / st.global.
+//     per reduction, arrives on a monotonic counter, and every CTA combines
+//     the partials in the same fixed order (bit-identical scalars in all
+//     CTAs, run-to-run deterministic) — no host readback, no .item();
+//   * a speculative region (codegen.Plan.spec) runs ONE pass under the
+//     decisions of its previous launch, verifies them after one grid
+//     reduction and, on a misprediction, runs the exact passes in the same
+//     launch;
+//   * inputs an exact later pass re-reads stay in registers across the grid
+//     barrier, or in their thread-private shared-memory slots;
+//   * loads are 128-bit ld.global.nc, stores 128-bit st.global.
 // Scalar predicates are CTA-uniform, so untaken arms are skipped by a
 // uniform branch and their inputs are never loaded.
 //

@@ -231,6 +231,73 @@ __global__ void gm_logring_commit_kernel(unsigned long long* dstep, unsigned lon
   *(volatile unsigned long long*)dcommit = s;
 }
 
+// ---------------------------------------------------------------------------
+// distinct-value sum of a 16-bit float tensor — `x.unique().sum()` after the
+// lowering's rank-1 rewrite (corpus/moe_minicpm_like: unique consumed only by
+// .sum()).  A 16-bit type has 65536 bit patterns, so the distinct set is a
+// 8 KB presence bitmap: each CTA marks its elements in a shared bitmap
+// (test-then-atomicOr, so repeated values cost a shared load), ORs the
+// non-empty words into the global bitmap, and one CTA sums the values of
+// the set bits in bit order (fp64, fixed tree: deterministic).  -0 is
+// folded onto +0 (torch.unique treats them as equal).  One pass over x,
+// no sort, no data-dependent shapes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void u16_mark(unsigned* bits, unsigned h) {
+  if (h == 0x8000u) h = 0;
+  const unsigned m = 1u << (h & 31);
+  unsigned* p = bits + (h >> 5);
+  if (!(*(volatile unsigned*)p & m)) atomicOr(p, m);
+}
+
+__global__ void __launch_bounds__(512) gm_unique16_mark_kernel(const uint4* __restrict__ x, long long nvec,
+                                                               const unsigned short* __restrict__ tail, int ntail,
+                                                               unsigned* __restrict__ gbits) {
+  __shared__ unsigned bits[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = 0;
+  __syncthreads();
+  const long long T = (long long)gridDim.x * blockDim.x;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += T) {
+    unsigned a, b, c, d;
+    gm::ldg16(x + v, a, b, c, d);
+    const unsigned w[4] = {a, b, c, d};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u16_mark(bits, w[j] & 0xffffu);
+      u16_mark(bits, w[j] >> 16);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) u16_mark(bits, tail[threadIdx.x]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (bits[i]) atomicOr(gbits + i, bits[i]);
+}
+
+__global__ void __launch_bounds__(1024) gm_unique16_sum_kernel(const unsigned* __restrict__ gbits, int dtype,
+                                                               void* out) {
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (int wi = threadIdx.x; wi < 2048; wi += blockDim.x) {
+    unsigned b = gbits[wi];
+    while (b) {
+      const int k = __ffs(b) - 1;
+      b &= b - 1;
+      const unsigned short h = (unsigned short)(wi * 32 + k);
+      acc += (double)(dtype == GM_BF16 ? gm::bf2f(h) : gm::h2f(h));
+    }
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      const float f = (float)t;
+      *(unsigned short*)out = dtype == GM_BF16 ? gm::f2bf(f) : gm::f2h(f);
+    }
+  }
+}
+
 int esize_of(int dtype) {
   switch (dtype) {
     case GM_F32: case GM_I32: return 4;
@@ -561,6 +628,28 @@ int gm_logring_gather(gm_logring r, const void* src, int dtype, int ndim, const 
   if ((unsigned long long)(total * A.esize) + offset > step_bytes || step_bytes * n_slots > r->bytes)
     return fail(GM_E_RING_FULL, "gm_logring_gather: record does not fit the ring slot");
   gm_logring_gather_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(A);
+  GM_CUDA(cudaGetLastError());
+  return GM_OK;
+}
+
+size_t gm_unique_sum16_scratch_bytes(void) { return 2048 * sizeof(unsigned); }
+
+int gm_unique_sum16(const void* x, int64_t n, int dtype, void* out, void* scratch, void* stream) {
+  if (g_device < 0) return fail(GM_E_INVALID, "gm_unique_sum16: gm_init not called");
+  if (!x || !out || !scratch || n < 0) return fail(GM_E_INVALID, "gm_unique_sum16: bad argument");
+  if (dtype != GM_BF16 && dtype != GM_F16) return fail(GM_E_INVALID, "gm_unique_sum16: dtype must be bf16 or f16");
+  if ((uintptr_t)x & 15) return fail(GM_E_INVALID, "gm_unique_sum16: x must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  GM_CUDA(cudaMemsetAsync(scratch, 0, gm_unique_sum16_scratch_bytes(), s));
+  const long long nvec = n / 8;
+  const int ntail = (int)(n % 8);
+  long long want = (nvec + 511) / 512;
+  int grid = (int)(want < 2LL * g_num_sms ? want : 2LL * g_num_sms);
+  if (grid < 1) grid = 1;
+  gm_unique16_mark_kernel<<<grid, 512, 0, s>>>((const uint4*)x, nvec, (const unsigned short*)x + nvec * 8, ntail,
+                                               (unsigned*)scratch);
+  GM_CUDA(cudaGetLastError());
+  gm_unique16_sum_kernel<<<1, 1024, 0, s>>>((const unsigned*)scratch, dtype, out);
   GM_CUDA(cudaGetLastError());
   return GM_OK;
 }

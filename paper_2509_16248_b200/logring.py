@@ -338,6 +338,20 @@ class step:
         return False
 
 
+_unique_scratch_by_dev: dict = {}
+
+
+def _unique_scratch(device) -> torch.Tensor:
+    """Per-device bitmap scratch of gm_unique_sum16 (calls on one stream are
+    ordered, so one buffer serves them all)."""
+    key = (device.type, device.index)
+    t = _unique_scratch_by_dev.get(key)
+    if t is None:
+        t = torch.empty(nat.lib().gm_unique_sum16_scratch_bytes(), dtype=torch.uint8, device=device)
+        _unique_scratch_by_dev[key] = t
+    return t
+
+
 class ModuleRuntime:
     """`__gm_rt` of a lowered module: its fused regions and replay sites."""
 
@@ -365,8 +379,19 @@ class ModuleRuntime:
 
     @staticmethod
     def unique_sum(x):
-        """== x.unique().sum(): sort, keep the first of each run of equal
-        values, sum — fixed shapes throughout, so no host sync."""
+        """== x.unique().sum() with fixed shapes (no host sync).  bf16/f16 on
+        the GPU: one pass into a 65536-bit presence bitmap and a sum of the
+        set bits (gm_unique_sum16).  Otherwise: sort, keep the first of each
+        run of equal values, sum."""
+        if x.is_cuda and x.dtype in (torch.bfloat16, torch.float16) and x.is_contiguous() \
+                and x.data_ptr() % 16 == 0:
+            out = torch.empty((), dtype=x.dtype, device=x.device)
+            scratch = _unique_scratch(x.device)
+            nat.check(nat.lib().gm_unique_sum16(
+                ctypes.c_void_p(x.data_ptr()), x.numel(), nat.GM_BF16 if x.dtype == torch.bfloat16 else nat.GM_F16, ctypes.c_void_p(out.data_ptr()),
+                ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
+                "gm_unique_sum16")
+            return out
         s = x.reshape(-1).sort().values
         keep = torch.ones_like(s, dtype=torch.bool)
         if s.numel() > 1:

@@ -52,3 +52,25 @@ def test_branch_select_f32(n, red):
         assert bool(s[1] != 0) == pred_ref
         ref = torch.where(torch.tensor(pred_ref), x * 2.0 + 1.0, x * 0.5 + -1.0)
         assert torch.equal(out.cpu(), ref), "affine arm must be bit-exact"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16], ids=["bf16", "f16"])
+@pytest.mark.parametrize("n", [1, 7, 8, 4099, 8 * 1024 * 768])
+def test_unique_sum16_matches_torch(n, dtype):
+    """gm_unique_sum16 (presence bitmap, one pass) == torch's
+    x.unique().sum() on CPU — the moe_minicpm_like rewrite of
+    `unique(x).sum()`; ragged sizes hit the tail path,
+    and -0.0 / +0.0 count once as in torch.unique."""
+    from paper_2509_16248_b200.logring import ModuleRuntime
+
+    torch.manual_seed(n)
+    x = (torch.softmax(torch.randn(n), 0) * 3 - 1e-3).to(dtype)
+    if n > 2:
+        x[0], x[1] = 0.0, -0.0
+    ref = x.unique().sum()
+    xd = x.cuda()
+    out = ModuleRuntime.unique_sum(xd)
+    assert out.dtype == dtype and out.shape == ()
+    r, o = float(ref), float(out.cpu())
+    assert abs(o - r) <= 1e-2 * abs(r) + 1e-6, (o, r)
