@@ -31,6 +31,7 @@ from __future__ import annotations
 import hashlib
 import math
 import os
+import re
 from dataclasses import dataclass, field
 
 import torch
@@ -47,7 +48,7 @@ RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "nzsum": 0, "amax"
 MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strided", "scalar"
 
 STATIC_SMEM_RESERVE = 8 * 1024
-DATA_REGS = 40          # raw-vector registers per thread: register stage + one block's loads
+DATA_REGS = int(os.environ.get("GM_DATA_REGS", "40"))  # raw-vector registers per thread: register stage + one block's loads
 VEC_REGS = {torch.float32: 8, torch.bfloat16: 4, torch.float16: 4, torch.bool: 2}
 MAX_DECISIONS = 24      # predicted decisions per speculative region (scratch ints at barrier + 288)
 
@@ -387,6 +388,9 @@ class Plan:
                 rec = f"gm::recip({self._ev(a[1], L, u)})"
                 rec = f"{rr}({rec})" if rr else rec
                 body = wrap(f"gm::mul({rec}, {self._sf(a[0])})")
+            elif a[1].op == "const" and self._pow2_recip(a[1].value) is not None:
+                # x / 2^k == x * 2^-k exactly (both are the correctly rounded x*2^-k)
+                body = wrap(f"gm::mul({ev(a[0], 0)}, {_fl(self._pow2_recip(a[1].value))}f)")
             else:
                 body = wrap(f"gm::div({ev(a[0], 0)}, {ev(a[1], 1)})")
         elif op == "pow":
@@ -641,7 +645,13 @@ class Plan:
         nothing: their exact fallback re-reads (from L2 in practice)."""
         sms, smem_optin = self.device_info
         self.vfull = self.n // nat.VEC
-        self.minb = int(os.environ.get("GM_CTAS_PER_SM", "2"))
+        # 2 CTAs x 512 threads per SM (64 registers a thread).  A region with
+        # 8-register (fp32) vectors and >= 3 reductions keeps more live
+        # values than that allows (phi4's chain spilled and ran 1.5x slower,
+        # tools/ab_regions.py): one CTA per SM, 128 registers a thread.
+        wide = any(VEC_REGS.get(ip.dtype, 4) == 8 for ip in self.inputs if ip.mode == MODE_FULL) \
+            and len(self.reductions) >= 3
+        self.minb = int(os.environ.get("GM_CTAS_PER_SM", "1" if wide else "2"))
         self.grid = max(1, min(self.minb * sms, -(-max(self.vfull, 1) // nat.THREADS)))
         self.T = self.grid * nat.THREADS
         self.K = -(-self.vfull // self.T) if self.vfull else 0
@@ -1046,9 +1056,23 @@ class Plan:
                         w(f"{ind}u32 ho{j}_{u}[4];")
                     else:
                         w(f"{ind}float ho{j}_{u}[GM_VEC];")
+        alias = self._arm_aliases(elem_nodes, reds, outs, pref, needs)
+        root_reds: dict[int, list] = {}
+        root_red_k: dict[int, int] = {}
+        for k, r in enumerate(reds):
+            root_reds.setdefault(r.args[0].uid, []).append(r)
+            root_red_k[r.uid] = k
+        root_outs: dict[int, list] = {}
+        for j, o in outs:
+            root_outs.setdefault(o.uid, []).append((j, o))
+        w_outer = w
         for u in range(U):
+            body: list[str] = []
+            w = body.append
             w(f"{ind}if (ok{u}) {{")
             for n in elem_nodes:
+                if n.uid in alias:
+                    continue
                 if "F" in needs[n.uid]:
                     w(f"{ind}  float n{n.uid}_{u}[GM_VEC];")
                 if "P" in needs[n.uid]:
@@ -1067,15 +1091,63 @@ class Plan:
                     cur_guard = g
                 for line in self._node_code(n, u, pref, needs):
                     w(ind + "    " + line.replace("\n", "\n" + ind + "    "))
+                # reductions and stores of a root right after it is computed
+                # (roots are unguarded), so its registers die early
+                if n.uid in root_reds or n.uid in root_outs:
+                    if open_block:
+                        w(f"{ind}  }}")
+                        open_block = False
+                        cur_guard = None
+                    self._emit_reds_outs(w, ind + "  ", root_reds.get(n.uid, []), root_outs.get(n.uid, []), u,
+                                         pref, hold=defer, red_index=root_red_k)
             if open_block:
                 w(f"{ind}  }}")
-            self._emit_reds_outs(w, ind + "  ", reds, outs, u, pref, hold=defer)
             for ip, act in loads:
                 if act == "ldst":
                     w(f"{ind}  gm::rstash<{DT_CODE[ip.dtype]}>(sres{ip.slot} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), "
                       f"r{ip.slot}_{u});")
             w(f"{ind}}}")
+            text = "\n".join(body)
+            for a_uid, w_uid in alias.items():
+                text = re.sub(rf"\b([np]){a_uid}_{u}\b", rf"\g<1>{w_uid}_{u}", text)
+            w_outer(text)
         self._preloaded = {}
+
+    def _arm_aliases(self, elem_nodes, reds, outs, pref, needs) -> dict[int, int]:
+        """Arms of a uniform select computed only for it write straight into
+        the select's registers (`where(p, A, B)`: A under `if (p)`, B under
+        `else`), so the select is a no-op and the two arms never hold
+        registers at the same time — the phi4 chain keeps ~3 live vectors
+        instead of ~10.  Returns {arm uid: select uid} (resolved through
+        chains of selects)."""
+        cons: dict[int, list] = {n.uid: [] for n in elem_nodes}
+        for n in elem_nodes:
+            for a in n.args:
+                if a.kind == "elem" and a.uid in cons:
+                    cons[a.uid].append(n)
+        for r in reds:
+            cons.setdefault(r.args[0].uid, []).append(r)
+        for _, o in outs:
+            cons.setdefault(o.uid, []).append(None)
+        alias: dict[int, int] = {}
+        for n in elem_nodes:
+            if n.op != "where" or n.args[0].kind == "elem":
+                continue
+            for arm in n.args[1:]:
+                if arm.kind != "elem" or arm.op == "free" or arm.uid in alias or arm is n.args[0]:
+                    continue
+                if any(c is not n for c in cons.get(arm.uid, [])):
+                    continue
+                if arm.dtype != n.dtype or pref[arm.uid] != pref[n.uid] or not needs[arm.uid] <= needs[n.uid]:
+                    continue
+                alias[arm.uid] = n.uid
+        # resolve chains (an arm aliased to a select that is itself an arm)
+        for a in list(alias):
+            t = alias[a]
+            while t in alias:
+                t = alias[t]
+            alias[a] = t
+        return alias
 
     def _emit_tail(self, w, elem_nodes, reds, outs, guards) -> None:
         """The partial last vector (n % 8 lanes), owned by thread VF_ % T_;
@@ -1154,6 +1226,21 @@ class Plan:
 
     # -- packed bf16x2 path ------------------------------------------------------
     @staticmethod
+    def _pow2_recip(v):
+        """1/v when v is a power of two whose reciprocal is a normal float32
+        (then x / v == x * (1/v) bit for bit), else None."""
+        try:
+            f = float(v)
+        except (TypeError, ValueError):
+            return None
+        if f == 0.0 or f != f or abs(f) == float("inf"):
+            return None
+        m, e = math.frexp(abs(f))
+        if m != 0.5 or not (-125 <= e - 1 <= 125):
+            return None
+        return 1.0 / f
+
+    @staticmethod
     def _bf16_exact(v) -> bool:
         f = torch.tensor(float(v), dtype=torch.float32)
         return bool(f.to(torch.bfloat16).to(torch.float32) == f)
@@ -1217,8 +1304,9 @@ class Plan:
                     w(f"{ind}  gm::store8<{DT_CODE[o.dtype]}>(P.out[{k}], e{u}, nv{u}, ho{j}_{u});")
             w(f"{ind}}}")
 
-    def _emit_reds_outs(self, w, ind, reds, outs, u, pref=None, hold=False):
-        for k, r in enumerate(reds):
+    def _emit_reds_outs(self, w, ind, reds, outs, u, pref=None, hold=False, red_index=None):
+        for k0, r in enumerate(reds):
+            k = red_index[r.uid] if red_index is not None else k0
             x = r.args[0]
             src = f"n{x.uid}_{u}"
             if r.op == NZSUM:

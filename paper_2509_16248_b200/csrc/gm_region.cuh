@@ -104,7 +104,19 @@ __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b);
 __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
-__device__ __forceinline__ float relu(float a) { return (a != a) ? a : (a > 0.f ? a : 0.f); }
+// NaN-propagating max/min (torch.maximum / Tensor.max semantics): one
+// FMNMX.NAN each (max.NaN / min.NaN, sm_80+)
+__device__ __forceinline__ float nmax(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ float nmin(float a, float b) {
+  float d;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ float relu(float a) { return nmax(a, 0.f); }
 __device__ __forceinline__ float recip(float a) { return __frcp_rn(a); }
 // exp via the SFU: ex2.approx(x*log2 e).  Relative error ~2 ulp + |x|*2^-24,
 // i.e. <= 1e-6 for |x| < 16 — an order below the 1e-5 parity bound (torch's
@@ -129,9 +141,6 @@ __device__ __forceinline__ float sigmoid(float a) {
 }
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
 __device__ __forceinline__ float neg(float a) { return -a; }
-// NaN-propagating max/min (torch.maximum / Tensor.max semantics)
-__device__ __forceinline__ float nmax(float a, float b) { return (a != a) ? a : ((b != b) ? b : (a > b ? a : b)); }
-__device__ __forceinline__ float nmin(float a, float b) { return (a != a) ? a : ((b != b) ? b : (a < b ? a : b)); }
 __device__ __forceinline__ double dmax(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a > b ? a : b)); }
 __device__ __forceinline__ double dmin(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a < b ? a : b)); }
 
@@ -802,6 +811,7 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
 __device__ __forceinline__ u64 grid_arrive(const Params& P, int nr, const int* ops, const int* slots,
                                            double* vals, double* s_warp, double* s_out, u64* prof = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
   for (int r = 0; r < nr; ++r) {
     const double v = warp_combine(ops[r], vals[r]);
     if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
@@ -810,6 +820,7 @@ __device__ __forceinline__ u64 grid_arrive(const Params& P, int nr, const int* o
   double* partials = (double*)P.partials;
   const bool multi = gridDim.x > 1;
   if (warp == 0) {
+#pragma unroll
     for (int r = 0; r < nr; ++r) {
       double v = lane < GM_WARPS ? s_warp[lane * GM_MAX_RED + r] : red_identity(ops[r]);
       v = warp_combine(ops[r], v);
@@ -860,7 +871,11 @@ __device__ __forceinline__ void grid_wait(const Params& P, int nr, const int* op
   __syncthreads();
   GM_STAMP(1);
   const double* partials = (const double*)P.partials;
-  for (int r = warp; r < nr; r += GM_WARPS) {
+  // reduction r is combined by warp r % GM_WARPS; the loop over r is
+  // unrolled at the (constant) call sites, so ops[]/slots[] stay registers
+#pragma unroll
+  for (int r = 0; r < nr; ++r) {
+    if (r % GM_WARPS != warp) continue;
     const double* base = partials + (i64)slots[r] * gridDim.x;
     double acc = red_identity(ops[r]);
     for (u32 b0 = 0; b0 < gridDim.x; b0 += 32 * 16) {
