@@ -767,6 +767,8 @@ class Plan:
         self.profiled = prof
         if prof:
             w("#define GM_PROF 1")
+        if os.environ.get("GM_ARRIVE_SPLIT"):
+            w(f"#define GM_ARRIVE_SPLIT {int(os.environ['GM_ARRIVE_SPLIT'])}")
         w('#include "gm_region.cuh"')
         w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
         w("#define gm_trunc(x) ((double)(long long)(x))")

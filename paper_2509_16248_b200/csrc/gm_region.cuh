@@ -777,7 +777,15 @@ __device__ __forceinline__ void st_release64(u64* p, u64 v) {
 #define GM_SCRATCH_FLAG 128     // (free: tools/barrier_bench.py protocol variants)
 #define GM_SCRATCH_RESULTS 136
 #define GM_SCRATCH_PRED 288     // int[24] predicted decisions (speculative regions)
-#define GM_SCRATCH_PARTIALS 384
+#define GM_SCRATCH_SUBCNT 384   // u64 arrival sub-counters, one per 128-byte line
+#define GM_SCRATCH_PARTIALS 2432
+// Arrival split: CTA b arrives on sub-counter b % GM_ARRIVE_SPLIT (separate
+// L2 lines), so no single address takes all 296 atomics; warp 0 polls the
+// sub-counters lane-parallel.  1 = one counter at +0.
+#ifndef GM_ARRIVE_SPLIT
+#define GM_ARRIVE_SPLIT 1
+#endif
+static_assert(GM_ARRIVE_SPLIT >= 1 && GM_ARRIVE_SPLIT <= 16, "16 sub-counter lines between +384 and the partials");
 
 // GM_PROF: optional timeline stamps (atomicMax over CTAs) for diagnostics
 #ifdef GM_PROF
@@ -836,9 +844,16 @@ __device__ __forceinline__ u64 grid_arrive(const Params& P, int nr, const int* o
   GM_STAMP(0);
   u64 target = 0;
   if (threadIdx.x == 0) {
+#if GM_ARRIVE_SPLIT > 1
+    const u32 S = GM_ARRIVE_SPLIT, i = blockIdx.x % S;
+    const u64 gi = (gridDim.x - i + S - 1) / S;  // CTAs arriving on sub-counter i
+    const u64 old = atom_add_acq_rel64((u64*)(P.barrier + GM_SCRATCH_SUBCNT + 128 * i), 1ull);
+    target = old / gi + 1;  // the epoch this arrival completes
+#else
     const u64 g = gridDim.x;
     const u64 old = atom_add_acq_rel64((u64*)P.barrier, 1ull);
     target = (old / g + 1) * g;
+#endif
 #ifdef GM_PROF
     if (prof) atomicMax(&prof[3], globaltimer());  // arrival completed (after the release)
 #endif
@@ -856,6 +871,26 @@ __device__ __forceinline__ void grid_wait(const Params& P, int nr, const int* op
     __syncthreads();
     return;
   }
+#if GM_ARRIVE_SPLIT > 1
+  if (warp == 0) {
+    const u32 S = GM_ARRIVE_SPLIT;
+    const u64 epoch = __shfl_sync(0xffffffffu, target, 0);
+    const u64 gi = lane < (int)S ? (gridDim.x - lane + S - 1) / S : 0;
+    const u64 want = epoch * gi;
+    const u64* cnt = (const u64*)(P.barrier + GM_SCRATCH_SUBCNT + 128 * (lane < (int)S ? lane : 0));
+    const u64 t0 = globaltimer();
+    int spins = 0;
+    while (true) {
+      const bool ok = lane >= (int)S || ld_relaxed64(cnt) >= want;
+      if (__all_sync(0xffffffffu, ok)) break;
+      if ((++spins & 1023) == 0 && globaltimer() - t0 > 2000000000ull) {
+        if (lane == 0) *(volatile int*)P.status = 1;
+        break;
+      }
+    }
+    fence_acq_rel_gpu();
+  }
+#else
   if (threadIdx.x == 0) {
     u64* cnt = (u64*)P.barrier;
     const u64 t0 = globaltimer();
@@ -868,6 +903,7 @@ __device__ __forceinline__ void grid_wait(const Params& P, int nr, const int* op
     }
     fence_acq_rel_gpu();
   }
+#endif
   __syncthreads();
   GM_STAMP(1);
   const double* partials = (const double*)P.partials;

@@ -29,7 +29,7 @@ from . import _native as nat
 from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
 from .ir import Graph, Node, Unsupported
 
-SCRATCH_PARTIALS = 384  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
+SCRATCH_PARTIALS = 2432  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
 SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [speculative launches, mispredictions]
 SCRATCH_PRED = 288      # GM_SCRATCH_PRED: int predicted decisions
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
