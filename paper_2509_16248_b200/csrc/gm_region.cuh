@@ -118,19 +118,6 @@ __device__ __forceinline__ float nmin(float a, float b) {
 }
 __device__ __forceinline__ float relu(float a) { return nmax(a, 0.f); }
 __device__ __forceinline__ float recip(float a) { return __frcp_rn(a); }
-// exp via the SFU: ex2.approx(x*log2 e).  Relative error ~2 ulp + |x|*2^-24,
-// i.e. <= 1e-6 for |x| < 16 — an order below the 1e-5 parity bound (torch's
-// own CPU exp/sigmoid are SLEEF approximations too).
-__device__ __forceinline__ float fexp(float a) {
-  float y;
-  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(a * 1.4426950408889634f));
-  return y;
-}
-__device__ __forceinline__ float frcp(float a) {
-  float y;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(a));
-  return y;
-}
 // sigmoid: ex2 / rcp on the SFU with flush-to-zero (1 + 2^y reads a denormal
 // 2^y as 1 anyway; only results below 1.2e-38 flush) — 2 MUFU, no fix-ups
 __device__ __forceinline__ float sigmoid(float a) {
@@ -199,19 +186,6 @@ __device__ __forceinline__ void stg16(void* p, u32 a, u32 b, u32 c, u32 d) {
 }
 __device__ __forceinline__ void stg8b(void* p, u32 a, u32 b) {
   asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
-}
-__device__ __forceinline__ u32 ld_acquire(const u32* p) {
-  u32 v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(u32* p, u32 v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ u32 atom_add_acq_rel(u32* p, u32 v) {
-  u32 old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
 }
 __device__ __forceinline__ double ld_relaxed_f64(const double* p) {
   double v;
@@ -377,19 +351,8 @@ __device__ __forceinline__ void load8(const InDesc& d, u32 sres, i64 e, i64 le, 
   }
 }
 
-// Staged (shared-memory resident) input: `sres` + local element `le`.
-template <int DT>
-__device__ __forceinline__ void load8_smem(u32 sres, i64 le, int nv, float (&x)[8]) {
-  typedef Elem<DT> E;
-  if (nv == GM_VEC) {
-    E::lds8(sres + (u32)(le * E::ES), x);
-  } else {
-#pragma unroll
-    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::lds1(sres + (u32)((le + k) * E::ES)) : 0.f;
-  }
-}
-
-// Streamed input from global memory (128-bit ld.global.nc).
+// Streamed input from global memory (128-bit ld.global.nc); per-lane loads
+// for the partial tail vector.
 template <int DT>
 __device__ __forceinline__ void load8_gmem(const InDesc& d, i64 e, int nv, float (&x)[8]) {
   typedef Elem<DT> E;
@@ -436,25 +399,18 @@ __device__ __forceinline__ void pack8(const float (&x)[8], u32 (&p)[4]) {
   for (int j = 0; j < 4; ++j) p[j] = f2bf2(x[2 * j], x[2 * j + 1]);
 }
 // raw 16-byte (8 x bf16) vector access for the packed path
-__device__ __forceinline__ void ldg_raw(const InDesc& d, i64 e, u32 (&p)[4]) {
-  ldg16((const char*)d.ptr + e * 2, p[0], p[1], p[2], p[3]);
-}
-__device__ __forceinline__ void lds_raw(u32 sres, i64 le, u32 (&p)[4]) {
-  lds16(sres + (u32)(le * 2), p[0], p[1], p[2], p[3]);
-}
-__device__ __forceinline__ void stash_raw(const InDesc& d, u32 sres, i64 e, i64 le, u32 (&p)[4]);
 __device__ __forceinline__ void stg_raw(const OutDesc& o, i64 e, const u32 (&p)[4]) {
   stg16((char*)o.ptr + e * 2, p[0], p[1], p[2], p[3]);
 }
 
 // ---------------------------------------------------------------------------
-// thread-private staging.  Every pass maps local vector lv to thread
-// lv % GM_THREADS, so a thread only ever re-reads the stash slots it wrote:
-// no mbarrier, no __syncthreads.  Pass 0 streams an input it re-reads later
-// with 128-bit loads and stores the raw vector to shared memory on the way
-// (load8_stash); an input first read by a later pass is prefetched at kernel
-// start with cp.async (LDGSTS) and waited per thread (cp_async_wait_all).
-// The one partial tail vector of a tensor always reads global memory.
+// thread-private staging.  Every pass maps vector v to the same thread, so a
+// thread only ever re-reads the stash slots it wrote: no mbarrier, no
+// __syncthreads.  The first pass that reads an input a later pass re-reads
+// stores its raw vectors to shared memory after use (rstash); an input first
+// read by a later pass is prefetched at kernel start with cp.async (LDGSTS)
+// and waited per thread (cp_async_wait_all).  The one partial tail vector of
+// a tensor always reads global memory.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void sts16(u32 s, u32 a, u32 b, u32 c, u32 d) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(s), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
@@ -464,60 +420,6 @@ __device__ __forceinline__ void cp_async16(u32 s, const void* g) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-template <int DT>
-__device__ __forceinline__ void load8_stash(const InDesc& d, u32 sres, i64 e, i64 le, int nv, float (&x)[8]) {
-  typedef Elem<DT> E;
-  if (nv != GM_VEC) {
-#pragma unroll
-    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, e + k) : 0.f;
-    return;
-  }
-  const char* g = (const char*)d.ptr + e * E::ES;
-  const u32 s = sres + (u32)(le * E::ES);
-  u32 a, b, c, w;
-  ldg16(g, a, b, c, w);
-  sts16(s, a, b, c, w);
-  if (E::ES == 4) {
-    u32 a2, b2, c2, w2;
-    ldg16(g + 16, a2, b2, c2, w2);
-    sts16(s + 16, a2, b2, c2, w2);
-    x[0] = __uint_as_float(a); x[1] = __uint_as_float(b); x[2] = __uint_as_float(c); x[3] = __uint_as_float(w);
-    x[4] = __uint_as_float(a2); x[5] = __uint_as_float(b2); x[6] = __uint_as_float(c2); x[7] = __uint_as_float(w2);
-  } else {
-    E::lds8(s, x);  // (re-read the stored vector: same thread, cheap; keeps one code path)
-  }
-}
-
-__device__ __forceinline__ void stash_raw(const InDesc& d, u32 sres, i64 e, i64 le, u32 (&p)[4]) {
-  ldg16((const char*)d.ptr + e * 2, p[0], p[1], p[2], p[3]);
-  sts16(sres + (u32)(le * 2), p[0], p[1], p[2], p[3]);
-}
-
-template <int DT>
-__device__ __forceinline__ void load8_res(const InDesc& d, u32 sres, i64 e, i64 le, int nv, float (&x)[8]) {
-  typedef Elem<DT> E;
-  if (nv == GM_VEC) {
-    E::lds8(sres + (u32)(le * E::ES), x);
-  } else {
-#pragma unroll
-    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, e + k) : 0.f;
-  }
-}
-
-// Prefetch this thread's full vectors of one input into its stash slots.
-template <int DT>
-__device__ __forceinline__ void prefetch_thread(const Params& P, const InDesc& d, u32 sres, i64 v0, i64 v1) {
-  typedef Elem<DT> E;
-  const i64 vfull = (P.n / GM_VEC < v1) ? P.n / GM_VEC : v1;
-  for (i64 v = v0 + threadIdx.x; v < vfull; v += GM_THREADS) {
-    const i64 e = v * GM_VEC, le = e - v0 * GM_VEC;
-    const char* g = (const char*)d.ptr + e * E::ES;
-    const u32 s = sres + (u32)(le * E::ES);
-#pragma unroll
-    for (int b = 0; b < GM_VEC * E::ES; b += 16) cp_async16(s + b, g + b);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // raw vectors.  The generated loops issue every load of a register block
