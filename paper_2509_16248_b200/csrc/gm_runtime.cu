@@ -11,6 +11,7 @@
 //  * the log ring: pinned, device-mapped host memory, a gather kernel for the
 //    elements torch's repr reads, and a stream-ordered step commit.
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
@@ -295,6 +296,44 @@ __global__ void __launch_bounds__(1024) gm_unique16_sum_kernel(const unsigned* _
       const float f = (float)t;
       *(unsigned short*)out = dtype == GM_BF16 ? gm::f2bf(f) : gm::f2h(f);
     }
+  }
+}
+
+// fp32: sort (CUB radix sort, by value bits) then one pass that sums the
+// first element of every run of equal values — fixed shapes, no host sync.
+// Per-thread fp64 partials over a fixed grid-stride assignment, per-CTA
+// partials in a fixed tree, then one CTA over the CTA partials: deterministic.
+__global__ void __launch_bounds__(512) gm_distinct_sum32_kernel(const float* __restrict__ s, long long n,
+                                                               double* __restrict__ partials) {
+  __shared__ double part[16];
+  double acc = 0.0;
+  const long long T = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) {
+    const float v = s[i];
+    if (i == 0 || v != s[i - 1]) acc += (double)v;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) partials[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) gm_sum_partials_kernel(const double* __restrict__ partials, int np,
+                                                               float* __restrict__ out) {
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partials[i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) *out = (float)t;
   }
 }
 
@@ -650,6 +689,35 @@ int gm_unique_sum16(const void* x, int64_t n, int dtype, void* out, void* scratc
                                                (unsigned*)scratch);
   GM_CUDA(cudaGetLastError());
   gm_unique16_sum_kernel<<<1, 1024, 0, s>>>((const unsigned*)scratch, dtype, out);
+  GM_CUDA(cudaGetLastError());
+  return GM_OK;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+size_t gm_unique_sum32_scratch_bytes(int64_t n) {
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, temp, (const float*)nullptr, (float*)nullptr, (int)n);
+  return align256(temp) + align256((size_t)n * sizeof(float)) + align256(8 * 4096);
+}
+
+int gm_unique_sum32(const float* x, int64_t n, float* out, void* scratch, size_t scratch_bytes, void* stream) {
+  if (g_device < 0) return fail(GM_E_INVALID, "gm_unique_sum32: gm_init not called");
+  if (!x || !out || !scratch || n <= 0 || n > 0x7fffffffLL) return fail(GM_E_INVALID, "gm_unique_sum32: bad argument");
+  if (scratch_bytes < gm_unique_sum32_scratch_bytes(n)) return fail(GM_E_INVALID, "gm_unique_sum32: scratch too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t temp = 0;
+  GM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, x, (float*)nullptr, (int)n));
+  char* base = (char*)scratch;
+  float* keys = (float*)(base + align256(temp));
+  double* partials = (double*)(base + align256(temp) + align256((size_t)n * sizeof(float)));
+  GM_CUDA(cub::DeviceRadixSort::SortKeys(base, temp, x, keys, (int)n, 0, 32, s));
+  long long want = (n + 511) / 512;
+  int grid = (int)(want < 2LL * g_num_sms ? want : 2LL * g_num_sms);
+  if (grid < 1) grid = 1;
+  gm_distinct_sum32_kernel<<<grid, 512, 0, s>>>(keys, n, partials);
+  GM_CUDA(cudaGetLastError());
+  gm_sum_partials_kernel<<<1, 1024, 0, s>>>(partials, grid, out);
   GM_CUDA(cudaGetLastError());
   return GM_OK;
 }

@@ -381,8 +381,9 @@ class ModuleRuntime:
     def unique_sum(x):
         """== x.unique().sum() with fixed shapes (no host sync).  bf16/f16 on
         the GPU: one pass into a 65536-bit presence bitmap and a sum of the
-        set bits (gm_unique_sum16).  Otherwise: sort, keep the first of each
-        run of equal values, sum."""
+        set bits (gm_unique_sum16); fp32 on the GPU: radix sort + one pass
+        over the runs (gm_unique_sum32).  Otherwise (CPU tensors): sort, keep
+        the first of each run of equal values, sum."""
         if x.is_cuda and x.dtype in (torch.bfloat16, torch.float16) and x.is_contiguous() \
                 and x.data_ptr() % 16 == 0:
             out = torch.empty((), dtype=x.dtype, device=x.device)
@@ -391,6 +392,15 @@ class ModuleRuntime:
                 ctypes.c_void_p(x.data_ptr()), x.numel(), nat.GM_BF16 if x.dtype == torch.bfloat16 else nat.GM_F16, ctypes.c_void_p(out.data_ptr()),
                 ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
                 "gm_unique_sum16")
+            return out
+        if x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and 0 < x.numel() < 2 ** 31:
+            out = torch.empty((), dtype=x.dtype, device=x.device)
+            nb = nat.lib().gm_unique_sum32_scratch_bytes(x.numel())
+            scratch = torch.empty(nb, dtype=torch.uint8, device=x.device)
+            nat.check(nat.lib().gm_unique_sum32(
+                ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
+                ctypes.c_void_p(scratch.data_ptr()), nb, ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
+                "gm_unique_sum32")
             return out
         s = x.reshape(-1).sort().values
         keep = torch.ones_like(s, dtype=torch.bool)
