@@ -767,6 +767,8 @@ class Plan:
         self.profiled = prof
         if prof:
             w("#define GM_PROF 1")
+        if os.environ.get("GM_ARRIVE_RED"):
+            w(f"#define GM_ARRIVE_RED {int(os.environ['GM_ARRIVE_RED'])}")
         if os.environ.get("GM_ARRIVE_SPLIT"):
             w(f"#define GM_ARRIVE_SPLIT {int(os.environ['GM_ARRIVE_SPLIT'])}")
         w('#include "gm_region.cuh"')
@@ -793,6 +795,7 @@ class Plan:
         # programmatic dependent launch: wait for the previous kernel's
         # results before the first global read (a no-op without PDL)
         w('  asm volatile("griddepcontrol.wait;" ::: "memory");')
+        w("  u64 ep_ = gm::grid_epoch_begin(P); (void)ep_;  // arrival epoch (thread 0)")
         for ip in self.inputs:
             if ip.mode == MODE_FULL and self.stage[ip.slot] == "smem":
                 w(f"  const u32 sres{ip.slot} = smem_u32(smem + {self.smem_off[ip.slot]});")
@@ -918,7 +921,7 @@ class Plan:
 
         def arrive():
             w(f"    {{ double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
-            w(f"      tgt_ = grid_arrive(P, {nr}, ops_, slots_, vals_, s_warp, s_red{pargs}); }}")
+            w(f"      tgt_ = grid_arrive(P, {nr}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs}); }}")
 
         deferred = False
         if self.K:

@@ -688,6 +688,14 @@ __device__ __forceinline__ void st_release64(u64* p, u64 v) {
 #define GM_ARRIVE_SPLIT 1
 #endif
 static_assert(GM_ARRIVE_SPLIT >= 1 && GM_ARRIVE_SPLIT <= 16, "16 sub-counter lines between +384 and the partials");
+// Arrival as a fire-and-forget `red.release` (1) or a returning
+// `atom.acq_rel` (0).  With `red`, thread 0 knows its epoch from the counter
+// value read at kernel start (grid_epoch_begin): before a CTA's own first
+// arrival at most gridDim.x - 1 arrivals of this launch can have landed, so
+// count / gridDim.x is the epoch every CTA of the launch agrees on.
+#ifndef GM_ARRIVE_RED
+#define GM_ARRIVE_RED 0
+#endif
 
 // GM_PROF: optional timeline stamps (atomicMax over CTAs) for diagnostics
 #ifdef GM_PROF
@@ -710,7 +718,14 @@ __device__ __forceinline__ u64 ld_relaxed64(const u64* p) {
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
-                                            double* vals, double* s_warp, double* s_out, u64* prof = nullptr);
+                                            double* vals, double* s_warp, double* s_out, u64& ep,
+                                            u64* prof = nullptr);
+
+// Thread 0's view of the arrival counter at kernel start (see GM_ARRIVE_RED);
+// the load is consumed only at the first arrival, so it overlaps the pass.
+__device__ __forceinline__ u64 grid_epoch_begin(const Params& P) {
+  return (threadIdx.x == 0 && gridDim.x > 1) ? ld_relaxed64((const u64*)P.barrier) : 0ull;
+}
 
 // First half of grid_reduce: the CTA partials are published and the CTA
 // arrives.  Returns the arrival target (thread 0; 0 elsewhere, and for a
@@ -719,7 +734,8 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
 // release, so the generated passes issue their output stores there: the
 // release does not wait for them to drain and they overlap the barrier.
 __device__ __forceinline__ u64 grid_arrive(const Params& P, int nr, const int* ops, const int* slots,
-                                           double* vals, double* s_warp, double* s_out, u64* prof = nullptr) {
+                                           double* vals, double* s_warp, double* s_out, u64& ep,
+                                           u64* prof = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int r = 0; r < nr; ++r) {
@@ -751,10 +767,16 @@ __device__ __forceinline__ u64 grid_arrive(const Params& P, int nr, const int* o
     const u64 gi = (gridDim.x - i + S - 1) / S;  // CTAs arriving on sub-counter i
     const u64 old = atom_add_acq_rel64((u64*)(P.barrier + GM_SCRATCH_SUBCNT + 128 * i), 1ull);
     target = old / gi + 1;  // the epoch this arrival completes
+#elif GM_ARRIVE_RED
+    const u64 g = gridDim.x;
+    target = (ep / g + 1) * g;
+    ep = target;
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"((u64*)P.barrier) : "memory");
 #else
     const u64 g = gridDim.x;
     const u64 old = atom_add_acq_rel64((u64*)P.barrier, 1ull);
     target = (old / g + 1) * g;
+    (void)ep;
 #endif
 #ifdef GM_PROF
     if (prof) atomicMax(&prof[3], globaltimer());  // arrival completed (after the release)
@@ -850,8 +872,8 @@ __device__ __forceinline__ void grid_wait(const Params& P, int nr, const int* op
 // co-resident (<= SMs x occupancy); a 2 s %globaltimer bound turns a
 // residency violation into status=1, not a hang.
 __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* ops, const int* slots,
-                                            double* vals, double* s_warp, double* s_out, u64* prof) {
-  const u64 target = grid_arrive(P, nr, ops, slots, vals, s_warp, s_out, prof);
+                                            double* vals, double* s_warp, double* s_out, u64& ep, u64* prof) {
+  const u64 target = grid_arrive(P, nr, ops, slots, vals, s_warp, s_out, ep, prof);
   grid_wait(P, nr, ops, slots, target, s_out, prof);
 }
 

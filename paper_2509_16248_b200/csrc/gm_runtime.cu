@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;
   const bool resident = P.in[0].smem_off >= 0;
   const u32 sres = resident ? smem_u32(smem + P.in[0].smem_off) : 0u;
+  u64 ep_ = grid_epoch_begin(P);
   Stage st, st_unused;
   st.wend = st_unused.wend = 0;
   st.bars = s_bars;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   double vals[1] = {(double)acc};
   const int ops[1] = {op};
   const int slots[1] = {0};
-  grid_reduce(P, 1, ops, slots, vals, s_warp, s_red);
+  grid_reduce(P, 1, ops, slots, vals, s_warp, s_red, ep_);
   // statistic in T's dtype (fp32), compared with the threshold cast to fp32
   const double r = s_red[0];
   float stat;

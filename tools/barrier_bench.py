@@ -103,10 +103,11 @@ __device__ void body(const Params& P) {
   double acc = (double)(threadIdx.x + blockIdx.x);
   const int ops[1] = {GM_R_SUM};
   const int slots[1] = {0};
+  u64 ep_ = grid_epoch_begin(P);
   for (int k = 0; k < (int)P.n; ++k) {
     if (V == 0) {
       double vals[1] = {acc};
-      grid_reduce(P, 1, ops, slots, vals, s_warp, s_red);
+      grid_reduce(P, 1, ops, slots, vals, s_warp, s_red, ep_);
     } else {
       grid_reduce_v<V>(P, acc, s_warp, s_red);
     }
