@@ -45,3 +45,14 @@ def test_nvrtc_compiles_skeleton_for_sm100a():
            '{ float x[8]; gm::load8<GM_DT_BF16>(P.in[0], 0u, 0, 0, 8, x); gm::store8<GM_DT_F32>(P.out[0], 0, 8, x); }\n')
     cubin = nat.compile_cubin(src, (10, 0))
     assert cubin[:4] == b"\x7fELF"
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: without libgm_b200.so the native entry points raise
+    NativeError instead of routing the path anywhere else."""
+    import pytest
+
+    monkeypatch.setattr(nat, "_lib", None)
+    monkeypatch.setattr(nat, "LIB_PATH", str(tmp_path / "libgm_b200.so"))
+    with pytest.raises(nat.NativeError, match="no fallback"):
+        nat.lib()
