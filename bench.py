@@ -333,7 +333,7 @@ def main():
     # ---- end to end through the public API, host buffers in and out:
     # (a) single call latency: executor(*pinned host inputs) -> D2H into a
     #     pinned host tensor, synchronised; (b) throughput: the executor's
-    #     double-buffered host pipeline (H2D / forward / D2H overlapped).
+    #     pipelined host path (H2D / forward / D2H overlapped, 3 graph slots).
     h2d = sum(t.numel() * t.element_size() for t in x_host)
     out0 = ex(*x_host)
     out_pinned = torch.empty(out0.shape, dtype=out0.dtype, pin_memory=True)
@@ -355,6 +355,9 @@ def main():
     ex.run_host_pipelined(host_batches, out=outs)
     barrier()
     e2e_total = max_over_ranks(time.perf_counter() - t_e2e, pg, dev)
+    # the same pipelined H2D / D2H traffic with no forward: the PCIe
+    # bound the end-to-end number sits against
+    pcie_s = _copy_only_pipeline(x_host, outs, dev, args.steps)
     ex.flush()
     d2h = out_pinned.numel() * out_pinned.element_size()
 
@@ -385,9 +388,11 @@ def main():
                    "l2": "flushed between timed steps: 256 MB write, then 256 MB read (cold, clean L2)"},
         "e2e": {"value": replica_value(batch, args.steps, ws, e2e_total), "unit": "samples/s",
                 "how": "B200Executor.run_host_pipelined: pinned host inputs -> H2D -> graph replay -> D2H into "
-                       "pinned host outputs, double-buffered; wall clock, max over ranks",
+                       "pinned host outputs, 3 rotating graph slots; wall clock, max over ranks",
                 "p50_ms_single_call": statistics.median(e2e_ms),
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "copy_only_samples_per_s": replica_value(batch, args.steps, ws, pcie_s),
+                "copy_only_how": "same pipeline (two copy streams, pinned buffers) with the forward removed"},
         "gpu_launches": gpu_launches,
         "roofline": roofline,
         "kernels": kernels,
@@ -399,6 +404,37 @@ def main():
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.destroy_process_group()
+
+
+def _copy_only_pipeline(x_host, outs, dev, steps: int) -> float:
+    """Wall time of `steps` H2D input copies + D2H output copies over 3
+    rotating buffers (no forward), the same streams/events pattern as
+    B200Executor.run_host_pipelined."""
+    import torch
+
+    S = 3
+    dst = [[torch.empty_like(t, device=dev) for t in x_host] for _ in range(S)]
+    src = [torch.empty(o.shape, dtype=o.dtype, device=dev) for o in outs[:S]]
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    loaded = [torch.cuda.Event() for _ in range(S)]
+    free = [torch.cuda.Event() for _ in range(S)]
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        s = k % S
+        with torch.cuda.stream(h2d):
+            if k >= S:
+                h2d.wait_event(free[s])
+            for d, h in zip(dst[s], x_host):
+                d.copy_(h, non_blocking=True)
+            loaded[s].record(h2d)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(loaded[s])
+            outs[k].copy_(src[s], non_blocking=True)
+            free[s].record(d2h)
+    d2h.synchronize()
+    h2d.synchronize()
+    return time.perf_counter() - t0
 
 
 def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5, mispredict: bool = False) -> float:

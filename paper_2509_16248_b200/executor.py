@@ -200,37 +200,39 @@ class B200Executor:
         e.load(args)
         return e.run()
 
-    def run_host_pipelined(self, batches, out=None):
+    def run_host_pipelined(self, batches, out=None, slots: int = 3):
         """Throughput path for host-resident inputs: each batch (a tuple of
         pinned CPU tensors) is copied H2D on a copy stream, replayed on the
         compute stream and its output copied D2H into pinned host memory on a
-        second copy stream, double-buffered across two captured graphs so
-        the copies of batch k+1 / k-1 overlap the forward of batch k.
-        Returns the list of host outputs (pinned tensors), in order."""
+        second copy stream, rotating over `slots` captured graphs (each with
+        its own static buffers) so the copies of batches k+1.. / k-1.. overlap
+        the forward of batch k.  Returns the list of host outputs (pinned
+        tensors), in order."""
         batches = list(batches)
         if not batches:
             return []
         dev = self.device
-        entries = [self.prepare(*[b.to(dev) for b in batches[0]], slot=s) for s in (0, 1)]
+        S = max(2, int(slots))
+        entries = [self.prepare(*[b.to(dev) for b in batches[0]], slot=s) for s in range(S)]
         comp = torch.cuda.current_stream(dev)
         h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        free = [torch.cuda.Event() for _ in range(2)]      # slot's buffers reusable
-        loaded = [torch.cuda.Event() for _ in range(2)]
-        done = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(S)]      # slot's buffers reusable
+        loaded = [torch.cuda.Event() for _ in range(S)]
+        done = [torch.cuda.Event() for _ in range(S)]
         results = []
         outs_host = out or [None] * len(batches)
         for k, batch in enumerate(batches):
-            s = k % 2
+            s = k % S
             e = entries[s]
             with torch.cuda.stream(h2d):
-                if k >= 2:
+                if k >= S:
                     h2d.wait_event(free[s])
                 for st, a in zip(e.static, batch):
                     if torch.is_tensor(st):
                         st.copy_(a, non_blocking=True)
                 loaded[s].record(h2d)
             comp.wait_event(loaded[s])
-            if k >= 2:
+            if k >= S:
                 comp.wait_event(free[s])
             o = e.run()
             done[s].record(comp)

@@ -80,7 +80,7 @@ def test_workloads(programs, name, dtype):
 
 @pytest.mark.gpu
 def test_host_pipeline_matches_single_calls(programs):
-    """B200Executor.run_host_pipelined (double-buffered H2D / replay / D2H)
+    """B200Executor.run_host_pipelined (pipelined H2D / replay / D2H over rotating graph slots)
     returns, batch by batch, exactly what single calls return."""
     prog = programs["bigbird_like"]
     ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
