@@ -43,6 +43,7 @@ from .ir import (BOOL_AND, BOOL_NOT, BOOL_OR, COMPARE, INT_REDUCE, ITEM, NZSUM, 
 DT_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2, torch.bool: 4}
 DT_SIZE = {torch.float32: 4, torch.bfloat16: 2, torch.float16: 2, torch.bool: 1}
 RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "nzsum": 0, "amax": 1, "amin": 2, "prod": 3,
+          "argmax": 6, "argmin": 6,
           "any": 4, "all": 5}
 
 MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strided", "scalar"
@@ -579,6 +580,9 @@ class Plan:
             return f"{dst} = ({x} != 0.0) ? 1.0 : 0.0;"
         if r.op == "count_nonzero":
             return f"{dst} = {x};"
+        if r.op in ("argmax", "argmin"):
+            # index = ~(low word of the winning key)
+            return (f"{dst} = (double)(0xffffffffu - (u32)((u64)__double_as_longlong({x}) & 0xffffffffull));")
         return f"{dst} = {R}({x});" if R else f"{dst} = {x};"
 
     # -- contexts ----------------------------------------------------------------
@@ -896,7 +900,9 @@ class Plan:
                 late.append(f"sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
         self._late = late
         for k, r in enumerate(reds):
-            if self._exact_acc(r):
+            if r.op in ("argmax", "argmin"):
+                w(f"    u64 acc{k} = 0ull;")
+            elif self._exact_acc(r):
                 w(f"    double acc{k} = 0.0;")
             else:
                 w(f"    float acc{k} = gm::acc_identity({RED_OP[r.op]});")
@@ -920,7 +926,9 @@ class Plan:
                   f"atomicMin(&prof_[{32 + idx}], t_); }}")
 
         def arrive():
-            w(f"    {{ double vals_[{nr}] = {{{', '.join(f'(double)acc{k}' for k in range(nr))}}};")
+            vals = ", ".join(f"__longlong_as_double((long long)acc{k})" if r.op in ("argmax", "argmin")
+                             else f"(double)acc{k}" for k, r in enumerate(reds))
+            w(f"    {{ double vals_[{nr}] = {{{vals}}};")
             w(f"      tgt_ = grid_arrive(P, {nr}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs}); }}")
 
         deferred = False
@@ -1314,7 +1322,9 @@ class Plan:
             k = red_index[r.uid] if red_index is not None else k0
             x = r.args[0]
             src = f"n{x.uid}_{u}"
-            if r.op == NZSUM:
+            if r.op in ("argmax", "argmin"):
+                w(f"{ind}acc{k} = gm::argkey8(acc{k}, {src}, e{u}, nv{u}, {'true' if r.op == 'argmin' else 'false'});")
+            elif r.op == NZSUM:
                 w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "
                   f"if (l < nv{u} && {src}[l] != 0.f) t_ += (double)({self._coordsum(f'(e{u} + l)')});\n"
                   f"{ind}acc{k} += t_; }}")

@@ -66,6 +66,7 @@ typedef unsigned char u8;
 #define GM_R_PROD 3
 #define GM_R_OR 4
 #define GM_R_AND 5
+#define GM_R_KEYMAX 6  // max of u64 keys carried in the fp64 slots (argmax / argmin)
 
 // Every field is 8 bytes wide so the ctypes mirror (_native.py) has the same
 // layout with no padding rules involved.
@@ -644,6 +645,8 @@ __device__ __forceinline__ double red_identity(int op) {
 }
 __device__ __forceinline__ double red_combine(int op, double a, double b) {
   switch (op) {
+    case GM_R_KEYMAX:
+      return ((u64)__double_as_longlong(a) >= (u64)__double_as_longlong(b)) ? a : b;
     case GM_R_MAX: return dmax(a, b);
     case GM_R_MIN: return dmin(a, b);
     case GM_R_PROD: return a * b;
@@ -875,6 +878,28 @@ __device__ __forceinline__ void grid_reduce(const Params& P, int nr, const int* 
                                             double* vals, double* s_warp, double* s_out, u64& ep, u64* prof) {
   const u64 target = grid_arrive(P, nr, ops, slots, vals, s_warp, s_out, ep, prof);
   grid_wait(P, nr, ops, slots, target, s_out, prof);
+}
+
+// argmax / argmin as a max over ordered 64-bit keys: the high word orders
+// the values (NaN above everything, as torch's argmax/argmin return the
+// first NaN; -0.0 folded onto +0.0), the low word is ~index so the first
+// occurrence wins a tie.  Identity 0; combined by GM_R_KEYMAX.
+__device__ __forceinline__ u32 order_key(float x, bool for_min) {
+  if (x != x) return 0xffffffffu;
+  if (x == 0.f) x = 0.f;
+  u32 b = __float_as_uint(x);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // monotone in x
+  return for_min ? ~b - 1u : b;                       // below the NaN key
+}
+__device__ __forceinline__ u64 argkey8(u64 acc, const float (&x)[8], i64 e, int nv, bool for_min) {
+#pragma unroll
+  for (int l = 0; l < GM_VEC; ++l) {
+    if (l < nv) {
+      const u64 key = ((u64)order_key(x[l], for_min) << 32) | (u64)(0xffffffffu - (u32)(e + l));
+      acc = key > acc ? key : acc;
+    }
+  }
+  return acc;
 }
 
 // Per-thread float accumulation of one 8-lane vector (masked to nv lanes).

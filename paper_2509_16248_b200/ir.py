@@ -41,7 +41,7 @@ UNARY = {
 BINARY = {"add", "sub", "mul", "div", "pow", "maximum", "minimum", "gt", "ge", "lt", "le", "eq", "ne",
           "logical_and", "logical_or"}
 COMPARE = {"gt", "ge", "lt", "le", "eq", "ne"}
-REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_nonzero", "nzsum"}
+REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_nonzero", "nzsum", "argmax", "argmin"}
 # reductions whose result is an integer count/sum: accumulated exactly in fp64
 INT_REDUCE = {"count_nonzero", "nzsum"}
 # `torch.nonzero(m).sum()` lowered to a reduction: the sum over the positions
@@ -62,7 +62,7 @@ _TORCH_FUNCS = {
     "logical_and": "logical_and", "logical_or": "logical_or", "where": "where", "clamp": "clamp",
     "clip": "clamp", "sum": "sum", "mean": "mean", "amax": "amax", "amin": "amin", "prod": "prod",
     "any": "any", "all": "all", "count_nonzero": "count_nonzero", "norm": "norm",
-    "max": "max", "min": "min",
+    "argmax": "argmax", "argmin": "argmin", "max": "max", "min": "min",
 }
 # Tensor.<name>(...) spellings (pure_ops.cfg plus the attr_table reductions)
 _METHODS = dict(_TORCH_FUNCS)
@@ -336,6 +336,8 @@ META_FNS = {
     "any": lambda a: a.any(),
     "all": lambda a: a.all(),
     "count_nonzero": lambda a: torch.count_nonzero(a),
+    "argmax": lambda a: a.argmax(),
+    "argmin": lambda a: a.argmin(),
     "nzsum": lambda a: torch.zeros((), dtype=torch.int64, device=a.device),
 }
 

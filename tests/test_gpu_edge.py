@@ -116,3 +116,47 @@ def test_region_decisions_are_deterministic():
         torch.cuda.synchronize()
         stats.add(tuple(low.regions[0].last_spec.scalars()))
     assert len(stats) == 1
+
+
+ARG = '''import torch
+
+def f(x, y):
+    h = x * 2
+    __gm_pred_0 = h.argmax() > PIVOT
+    __gm_then_a_0 = h + y
+    __gm_else_a_0 = h - y
+    a = torch.where(__gm_pred_0, __gm_then_a_0, __gm_else_a_0)
+    __gm_pred_1 = a.argmin() < PIVOT
+    z = torch.where(__gm_pred_1, a * 3, a)
+    return z
+'''
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("n", [13, 10007, 8 * 1024 * 768])
+def test_argmax_argmin_predicates(n, dtype):
+    """argmax / argmin predicates (data/attr_table.cfg) as fused reductions:
+    ordered 64-bit keys (value order, first index on ties, NaN above all),
+    branch decisions equal to torch's on CPU — including ties, -0.0/+0.0 and
+    a NaN, and the maximum placed either side of the pivot."""
+    pivot = n // 2
+    text = ARG.replace("PIVOT", str(pivot))
+    torch.manual_seed(n)
+    cases = []
+    for where in (pivot // 2, pivot + (n - pivot) // 2):
+        x = torch.randn(n)
+        x[where] = 50.0                       # unique maximum on one side
+        y = torch.randn(n)
+        cases.append((x, y))
+    x = torch.round(torch.randn(n) * 2)       # many ties: the first index wins
+    cases.append((x, torch.randn(n)))
+    x = torch.zeros(n)
+    x[: n // 3] = -0.0                        # -0.0 == +0.0: first occurrence
+    cases.append((x, torch.ones(n)))
+    x = torch.randn(n)
+    x[n - 2] = float("nan")                   # NaN is the argmax and the argmin
+    cases.append((x, torch.randn(n)))
+    for x, y in cases:
+        out, ref, ex, low = _run(text, "f", [x.to(dtype), y.to(dtype)], dtype)
+        assert_parity(out, ref, dtype, what=f"argmax/argmin n={n}")
