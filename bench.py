@@ -134,6 +134,28 @@ def _ncu_traffic(kernel: str):
     return best
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _transform_ms(workload: str):
+    """The reference fix_file's one-time cost for this program (measured in
+    the build container by oracle/time_transform.py; the reference is not on
+    the GPU box)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "transform_times.json")) as fh:
+            return json.load(fh)["ms"].get(workload)
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -185,7 +207,7 @@ def run_reference(args, ws, rank):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (manifest seed/dist), random-init weights",
         "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
                    "shape": list(x[0].shape)},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port", "cpu_model": _cpu_model(),
                          "sample": f"{len(times)} full forwards of the reference-transformed program, eager "
                                    f"torch CPU, {threads} threads"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -212,6 +234,7 @@ def cpu_baseline(prog, shapes, dtype, budget_s=15.0):
         times.append(time.perf_counter() - t0)
     batch = int(x[0].shape[0])
     return {"value": batch * len(times) / sum(times), "unit": "samples/s", "cores": threads, "kind": "port",
+            "cpu_model": _cpu_model(),
             "sample": f"{len(times)} forwards of the reference-transformed program (same inputs), eager torch "
                       f"CPU, {threads} threads; p50 {1e3 * statistics.median(times):.2f} ms"}
 
@@ -376,6 +399,7 @@ def main():
         "ms_per_step": total_ms / args.steps,
         "p50_ms": statistics.median(step_ms),
         "cold_ms": cold_ms,
+        "transform_ms_one_time": _transform_ms(args.workload),
         "host_syncs_per_forward": info.host_syncs,
         "mode": info.mode,
         "higher_is_better": True,
