@@ -117,6 +117,7 @@ class Plan:
         self._classify(args)
         self._passes()
         self._inputs(args)
+        self._hoist()
         self.source = self._emit()
         digest = hashlib.sha1(self.source.encode()).hexdigest()[:16]
         self.kernel = f"gm_region_{digest}"
@@ -190,6 +191,112 @@ class Plan:
         self.scalars = [n for n in self.order if n.kind in ("host", "dscalar") and n.op != "const"]
         self.slot = {n.uid: i for i, n in enumerate(self.scalars)}
         self.max_level = max([avail[n.uid] for n in self.scalars] or [0])
+
+    # -- monotone reduction hoisting -----------------------------------------------
+    def _hoist(self) -> None:
+        """A max/min in pass p >= 1 of `E = Y ⋈ s` (⋈ in *, +, -; Y an
+        elementwise value of an earlier pass q; s a scalar first known at
+        level p) equals E's own elementwise code applied to max(Y) or min(Y):
+        each such E is monotone in Y (direction from the sign of s for *),
+        and rounding to the storage type is monotone too.  So pass q also
+        reduces max(Y) and min(Y), and at level p — when s is known — the
+        statistic is computed from them.  The exact sweep of pass p runs only
+        when the guard fails: s, max(Y) or min(Y) not finite (NaN or inf
+        would break the identity), checked on the device, uniform across
+        CTAs.  Applied to a pass only when every reduction in it qualifies
+        and it stores no output (longformer_like: 3 sweeps -> 2)."""
+        self.hoisted: dict[int, list] = {}
+        if os.environ.get("GM_HOIST", "1") == "0" or self.npass < 2:
+            return
+        aux = self.graph.__dict__.setdefault("_gm_aux", {})
+        plans = {}
+        for p in range(1, self.npass):
+            reds = self.pass_reds[p]
+            if not reds or self.pass_outputs[p]:
+                continue
+            items = []
+            for r in reds:
+                e = r.args[0]
+                if r.op not in ("amax", "amin") or e.op not in ("mul", "add", "sub") or not e.dtype.is_floating_point:
+                    break
+                elem = [a for a in e.args if a.kind == "elem"]
+                scal = [a for a in e.args if a.kind != "elem"]
+                if len(elem) != 1 or len(scal) != 1 or elem[0].dtype != e.dtype:
+                    break
+                y, s = elem[0], scal[0]
+                if self.need[y.uid] >= p or s.op == "const":
+                    break
+                if self._guard_expr(self._guards(p).get(e.uid, frozenset({frozenset()}))):
+                    break
+                # monotone direction: +1 increasing in Y, -1 decreasing, 0 = sign of s
+                if e.op == "mul":
+                    direction = 0
+                elif e.op == "add":
+                    direction = 1
+                else:
+                    direction = 1 if e.args[0] is y else -1
+                items.append((r, e, y, s, direction))
+            else:
+                plans[p] = items
+        if not plans:
+            return
+        for p, items in plans.items():
+            for r, e, y, s, direction in items:
+                ext = []
+                for op in ("amax", "amin"):
+                    key = (y.uid, op)
+                    n = aux.get(key)
+                    if n is None:
+                        n = self.graph.add(Node(op, (y,)))
+                        aux[key] = n
+                    if n not in self.reductions:
+                        v = y.meta.max() if op == "amax" else y.meta.min()
+                        n.meta, n.kind, n.dtype, n.shape = v, "dscalar", v.dtype, ()
+                        self.reductions.append(n)
+                        q = self.need[y.uid]
+                        self.pass_reds[q].append(n)
+                        self.avail[n.uid] = q + 1
+                        self.slot[n.uid] = len(self.scalars)
+                        self.scalars.append(n)
+                    ext.append(n)
+                self.hoisted.setdefault(p, []).append((r, e, y, s, direction, ext[0], ext[1]))
+        if len(self.reductions) > nat.MAX_RED:
+            raise Unsupported("too many reductions in one region")
+
+    def _emit_hoist_guard(self, w, p: int) -> None:
+        """Thread 0, at scalar level p: decide whether pass p can be skipped
+        and, if so, fill its statistics from the hoisted max/min."""
+        items = self.hoisted[p]
+        w(f"  __shared__ int s_hoist{p};")
+        w("  if (threadIdx.x == 0) {")
+        conds = []
+        for r, e, y, s, d, hmax, hmin in items:
+            for n in (s, hmax, hmin):
+                v = self._sv(n)
+                conds.append(f"(({v}) - ({v}) == 0.0)")  # finite
+        w(f"    const int ok_ = ({' && '.join(conds)}) ? 1 : 0;")
+        w(f"    s_hoist{p} = ok_;")
+        w("    if (ok_) {")
+        for r, e, y, s, d, hmax, hmin in items:
+            want_max = r.op == "amax"
+            if d == 0:
+                inc = f"({self._sv(s)} >= 0.0)"
+            else:
+                inc = "true" if d > 0 else "false"
+            pick_max = f"({inc} ? {'1' if want_max else '0'} : {'0' if want_max else '1'})"
+            w("      {")
+            w(f"        const double yx_ = {pick_max} ? {self._sv(hmax)} : {self._sv(hmin)};")
+            w(f"        float n{y.uid}_h[GM_VEC];")
+            w(f"        for (int l = 0; l < GM_VEC; ++l) n{y.uid}_h[l] = (float)yx_;")
+            w(f"        const float sf{s.uid} = (float){self._sv(s)}; (void)sf{s.uid};")
+            w(f"        float n{e.uid}_h[GM_VEC];")
+            for line in self._elem_code(e, "h"):
+                w("        " + line.replace("\n", "\n        "))
+            w(f"        s_scal[{self.slot[r.uid]}] = (double)n{e.uid}_h[0];")
+            w("      }")
+        w("    }")
+        w("  }")
+        w("  __syncthreads();")
 
     # -- inputs ---------------------------------------------------------------
     def _inputs(self, args) -> None:
@@ -832,7 +939,14 @@ class Plan:
             w("  }")
             w("  // misprediction: the exact multi-pass path (inputs re-read)")
         for p in range(self.npass):
-            self._emit_ctx(w, p)
+            if p in self.hoisted and not self.spec:
+                self._emit_hoist_guard(w, p)
+                w(f"  if (!s_hoist{p}) {{  // hoisting guard failed: the exact sweep")
+                self._emit_ctx(w, p, scalar_level=False)
+                w("  }")
+                self._emit_scalar_level(w, p + 1)
+            else:
+                self._emit_ctx(w, p)
         if prof:
             w("  __syncthreads();")
             w("  if (threadIdx.x == 0) atomicMax(&prof_[63], gm::globaltimer());")
@@ -866,7 +980,7 @@ class Plan:
                     w(f"{ind}  pred_[{j}] = (s_scal[{self.slot[d.uid]}] != 0.0) ? 1 : 0;")
         w(f"{ind}}}")
 
-    def _emit_ctx(self, w, ctx) -> None:
+    def _emit_ctx(self, w, ctx, scalar_level: bool = True) -> None:
         spec = ctx == "spec"
         roots = self._ctx_roots(ctx)
         elem_nodes = self._nodes(roots)
@@ -1000,7 +1114,8 @@ class Plan:
                     w("      " + self._finish_reduction(r, k))
                 w("    }")
                 w("    __syncthreads();")
-                self._emit_scalar_level(w, ctx + 1)
+                if scalar_level:
+                    self._emit_scalar_level(w, ctx + 1)
         w("  }")
 
     def _emit_block(self, w, kb: str, U: int, elem_nodes, reds, outs, guards, loads, pref, defer=False) -> None:

@@ -160,3 +160,34 @@ def test_argmax_argmin_predicates(n, dtype):
     for x, y in cases:
         out, ref, ex, low = _run(text, "f", [x.to(dtype), y.to(dtype)], dtype)
         assert_parity(out, ref, dtype, what=f"argmax/argmin n={n}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+def test_hoisted_max_guard(programs, dtype):
+    """longformer_like: `scaled.max()` with `scaled = win * w0` is computed
+    from max/min(win) at the first grid reduce (codegen.Plan._hoist); the
+    guard sends non-finite cases (NaN, inf, overflow) through the exact
+    sweep.  Every case equals torch eager on CPU."""
+    from paper_2509_16248_b200 import codegen
+
+    prog = programs["longformer_like"]
+    text, fn = prog["transformed"], prog["callable"]
+    torch.manual_seed(7)
+    base = torch.randn(4, 512, 768)
+    cases = {"normal": base.clone(), "all_negative": -base.abs() - 1.0}
+    c = base.clone()
+    c[1, 2, 3] = float("nan")
+    cases["nan"] = c
+    c = base.clone()
+    c[0, 0, 5] = float("inf")
+    cases["inf"] = c
+    c = base.clone()
+    c[2, 7, 9] = 3.0e38 if dtype == torch.float32 else 3.0e38
+    cases["overflow"] = c
+    for name, x in cases.items():
+        x = x.to(dtype)
+        out, ref, ex, low = _run(text, fn, [x], dtype)
+        assert_parity(out, ref, dtype, what=f"longformer {name}")
+    r = low.regions[0]
+    assert r.last_spec.plan.hoisted, "the max was not hoisted"
