@@ -1163,7 +1163,9 @@ class Plan:
                     needs[a.uid].add(pref[n.uid] if (pref[n.uid] == "P" and not (n.op == "where" and a is n.args[0]))
                                      else "F")
         for r in reds:
-            needs[r.args[0].uid].add("F")
+            x = r.args[0]
+            packed_red = r.op in ("amax", "amin") and pref.get(x.uid) == "P"
+            needs[x.uid].add("P" if packed_red else "F")
         for _, o in outs:
             needs[o.uid].add(pref[o.uid])
         # nodes some consumer reads unpacked (float lanes)
@@ -1173,7 +1175,8 @@ class Plan:
                 if a.kind == "elem" and (pref[n.uid] == "F" or (n.op == "where" and a is n.args[0])):
                     self._f_consumers[a.uid] = True
         for r in reds:
-            self._f_consumers[r.args[0].uid] = True
+            if not (r.op in ("amax", "amin") and pref.get(r.args[0].uid) == "P"):
+                self._f_consumers[r.args[0].uid] = True
         for _, o in outs:
             if pref[o.uid] == "F":
                 self._f_consumers[o.uid] = True
@@ -1337,6 +1340,11 @@ class Plan:
         if n.op in ("add", "sub", "mul"):
             fn = {"add": "gm::hadd2", "sub": "gm::hsub2", "mul": "gm::hmul2"}[n.op]
             body = f"{fn}({pv(a[0])}, {pv(a[1])})"
+        elif n.op == "div":
+            rb = self._bf16_bits(self._pow2_recip(a[1].value))
+            body = f"gm::hmul2({pv(a[0])}, 0x{(rb << 16) | rb:08x}u)"
+        elif n.op == "relu":
+            body = f"gm::hmax2({pv(a[0])}, 0u)"
         elif n.op == "neg":
             body = f"({pv(a[0])} ^ 0x80008000u)"
         elif n.op == "abs":
@@ -1406,7 +1414,10 @@ class Plan:
                             ok &= self._scalar_packable(a, n.op)
                     if ok and any(a.kind == "elem" for a in n.args):
                         r = "P"
-                elif n.op in ("neg", "pos", "abs"):
+                elif n.op == "div" and n.args[0].kind == "elem" and n.args[0].dtype == bf \
+                        and n.args[1].op == "const" and self._pow2_recip(n.args[1].value) is not None:
+                    r = "P"   # x / 2^k == x * 2^-k (bf16-exact), one rounding either way
+                elif n.op in ("neg", "pos", "abs", "relu"):
                     if n.args[0].kind == "elem" and n.args[0].dtype == bf:
                         r = "P"
                 elif n.op == "where" and n.args[0].kind != "elem":
@@ -1437,7 +1448,10 @@ class Plan:
             k = red_index[r.uid] if red_index is not None else k0
             x = r.args[0]
             src = f"n{x.uid}_{u}"
-            if r.op in ("argmax", "argmin"):
+            if r.op in ("amax", "amin") and pref is not None and pref.get(x.uid) == "P":
+                # bf16 max/min on the packed words: 3 max.NaN.bf16x2, then 2 lanes
+                w(f"{ind}acc{k} = gm::acc_minmax_p<{1 if r.op == 'amax' else 0}>(acc{k}, p{x.uid}_{u});")
+            elif r.op in ("argmax", "argmin"):
                 w(f"{ind}acc{k} = gm::argkey8(acc{k}, {src}, e{u}, nv{u}, {'true' if r.op == 'argmin' else 'false'});")
             elif r.op == NZSUM:
                 w(f"{ind}{{ double t_ = 0.0;\n#pragma unroll\n{ind}for (int l = 0; l < GM_VEC; ++l) "

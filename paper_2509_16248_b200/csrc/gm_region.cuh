@@ -387,6 +387,18 @@ __device__ __forceinline__ u32 hmul2(u32 a, u32 b) {
   asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
+// NaN-propagating packed max/min (max.NaN.bf16x2, sm_90+): relu and the
+// bf16 max/min reductions stay packed
+__device__ __forceinline__ u32 hmax2(u32 a, u32 b) {
+  u32 d;
+  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ u32 hmin2(u32 a, u32 b) {
+  u32 d;
+  asm("min.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 __device__ __forceinline__ void unpack_bf2(u32 p, float& lo, float& hi) {
   lo = __uint_as_float(p << 16);
   hi = __uint_as_float(p & 0xffff0000u);
@@ -394,6 +406,13 @@ __device__ __forceinline__ void unpack_bf2(u32 p, float& lo, float& hi) {
 __device__ __forceinline__ void unpack8(const u32 (&p)[4], float (&x)[8]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) unpack_bf2(p[j], x[2 * j], x[2 * j + 1]);
+}
+template <int MAX>
+__device__ __forceinline__ float acc_minmax_p(float acc, const u32 (&p)[4]) {
+  const u32 m = MAX ? hmax2(hmax2(p[0], p[1]), hmax2(p[2], p[3])) : hmin2(hmin2(p[0], p[1]), hmin2(p[2], p[3]));
+  float lo, hi;
+  unpack_bf2(m, lo, hi);
+  return MAX ? nmax(acc, nmax(lo, hi)) : nmin(acc, nmin(lo, hi));
 }
 __device__ __forceinline__ void pack8(const float (&x)[8], u32 (&p)[4]) {
 #pragma unroll
