@@ -1006,8 +1006,8 @@ class Plan:
             else:
                 w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
                 w(f"    const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
-            if s.op == "free" and s.kind == "host":
-                w(f"    const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
+            if (s.op == "free" and s.kind == "host") or (s.kind == "dscalar" and s.dtype == torch.bfloat16):
+                w(f"    u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
         for ip in self.inputs:
             if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in elem_nodes:
                 w(f"    float sin{ip.slot} = 0.f;")
@@ -1393,6 +1393,9 @@ class Plan:
             return op in ("add", "sub") or self._bf16_exact(s.value)
         if s.op == "free" and s.kind == "host":
             return op in ("add", "sub") or self.host_exact.get(s.uid, False)
+        if s.kind == "dscalar" and s.dtype == torch.bfloat16:
+            # a 0-d bf16 tensor holds a bf16 value: the packed op is exact
+            return op in ("add", "sub", "mul")
         return False
 
     def _packed_plan(self, elem_nodes: list[Node]) -> dict[int, str]:
