@@ -9,14 +9,22 @@ Given a region DAG (ir.py) and the runtime arguments, `Plan` decides
     pass p runs in pass p; an elementwise output is stored in the first pass
     where all its scalars are known.  A predicated block is one reduction
     pass plus one select pass (transform.py:386-388 then :374-376);
+  * speculation (`spec`): when every reduction-derived scalar the later
+    passes read is a boolean branch decision, the kernel runs one pass under
+    the previous launch's decisions, verifies them after one grid reduce and
+    falls back to the exact passes in the same launch;
+  * monotone hoisting (`_hoist`): a max/min of `Y * s`, `Y + s`, `Y - s` is
+    taken from max/min(Y) at an earlier grid reduce, guarded on the device;
   * guards: an elementwise node that feeds only one side of a `where` with a
     uniform (scalar) predicate is evaluated under that predicate, so the
     untaken arm costs nothing — the reference evaluates both arms eagerly
     (transform.py:404-412), which is equivalent because arms are pure;
-  * residency: inputs read by more than one pass are staged once in shared
-    memory (bulk copy) and re-read from there.
+  * the launch layout (`_plan_layout`): 2 CTAs x 512 threads per SM over a
+    grid-stride vector map, every load of a register block issued first, and
+    register or thread-private shared-memory staging of inputs that exact
+    later passes re-read;
 
-and `emit()` writes the kernel on top of csrc/gm_region.cuh.
+and `_emit()` writes the kernel on top of csrc/gm_region.cuh.
 
 Numerics follow torch's CPU eager kernels (the reference executes the
 transformed program eagerly on CPU, runner.py:154-157), measured in this
@@ -95,7 +103,6 @@ class InputPlan:
     mode: str
     dtype: torch.dtype
     slot: int              # index into P.in
-    resident: bool = False
     passes: set = field(default_factory=set)
 
 
@@ -190,7 +197,6 @@ class Plan:
         # scalar slots
         self.scalars = [n for n in self.order if n.kind in ("host", "dscalar") and n.op != "const"]
         self.slot = {n.uid: i for i, n in enumerate(self.scalars)}
-        self.max_level = max([avail[n.uid] for n in self.scalars] or [0])
 
     # -- monotone reduction hoisting -----------------------------------------------
     def _hoist(self) -> None:
@@ -302,7 +308,6 @@ class Plan:
     def _inputs(self, args) -> None:
         self.inputs: list[InputPlan] = []
         self.host_frees: list[Node] = []
-        self.dscalar_frees: list[Node] = []
         used_passes: dict[int, set] = {}
         for p in range(self.npass):
             for node in self._pass_nodes(p):
@@ -313,8 +318,6 @@ class Plan:
                 continue
             if node.kind == "host":
                 self.host_frees.append(node)
-            elif node.kind == "dscalar":
-                self.dscalar_frees.append(node)
         if len(self.host_frees) > nat.MAX_HS:
             raise Unsupported("too many host scalars")
         for node in self.order:

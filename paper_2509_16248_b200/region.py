@@ -137,7 +137,7 @@ class _Spec:
         P.n = n
         P.nvec = nvec
         P.vpc = vpc
-        P.piece_vecs = max(64, -(-vpc // nat.MAX_PIECES)) if vpc else 1
+        P.piece_vecs = 1  # (bulk-copy staging: gm_branch_select_f32 only)
         P.barrier = base
         P.status = base + 16
         P.partials = base + SCRATCH_PARTIALS
