@@ -224,11 +224,58 @@ class _FunctionLowerer:
             ast.fix_missing_locations(self.fn)
         return out
 
+    def _fusable(self, e: ast.expr) -> bool:
+        try:
+            Builder(Graph(), self.owner.torch_names, self.owner.functional_names).expr(e)
+        except Unsupported:
+            return False
+        return True
+
+    def _split_calls(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
+        """`x = f(g(y)) + z` with g non-fusable (a module or library call,
+        e.g. a Linear on cuBLAS) and the rest elementwise becomes
+        `__gm_t_k = g(y); x = f(__gm_t_k) + z`, so the elementwise remainder
+        joins a fused region instead of running as separate PyTorch ops.
+        Hoisted calls keep their left-to-right order; what is left around
+        them is pure (fusable), so evaluation order is unchanged."""
+        out: list[ast.stmt] = []
+        for s in stmts:
+            if not self._eligible(s) or self._fusable(s.value):
+                out.append(s)
+                continue
+            temps: list[ast.stmt] = []
+
+            def split(e: ast.expr) -> ast.expr:
+                if self._fusable(e):
+                    return e
+                if isinstance(e, ast.BinOp):
+                    return ast.BinOp(split(e.left), e.op, split(e.right))
+                if isinstance(e, ast.UnaryOp):
+                    return ast.UnaryOp(e.op, split(e.operand))
+                if isinstance(e, ast.Call) and not e.keywords and not any(isinstance(a, ast.Starred) for a in e.args):
+                    cand = ast.Call(e.func, [split(a) for a in e.args], [])
+                    if self._fusable(cand):
+                        return cand
+                name = f"__gm_t_{self.owner.next_tmp()}"
+                temps.append(ast.copy_location(ast.Assign(targets=[ast.Name(name, ast.Store())], value=e), s))
+                self.loads.append(((s.lineno, s.col_offset + 1), name))
+                return ast.Name(name, ast.Load())
+
+            new_value = split(s.value)
+            if not temps or isinstance(new_value, ast.Name) or not self._fusable(new_value):
+                out.append(s)
+                continue
+            res = ast.copy_location(ast.Assign(targets=s.targets, value=new_value), s)
+            res.end_lineno, res.end_col_offset = s.end_lineno, s.end_col_offset
+            ast.fix_missing_locations(res)
+            out.extend(temps + [res])
+        return out
+
     def lower_block(self, stmts: list[ast.stmt], in_loop: bool) -> list[ast.stmt]:
         out: list[ast.stmt] = []
         run: list[ast.stmt] = []
         hoist: list[ast.stmt] = []
-        stmts = self._lower_dynamic_shape(stmts)
+        stmts = self._split_calls(self._lower_dynamic_shape(stmts))
         for stmt in self._split_returns(stmts):
             cap = _is_capture(stmt)
             if cap is not None and run:
@@ -340,6 +387,10 @@ class _Lowerer:
         self.sites: list[ReplaySite] = []
         self.fallback_defs: list[ast.FunctionDef] = []
         self.dyn_lowered: list[tuple[str, str]] = []
+
+    def next_tmp(self) -> int:
+        self._tmp = getattr(self, "_tmp", 0) + 1
+        return self._tmp - 1
 
     def next_ret(self) -> int:
         self._ret = getattr(self, "_ret", -1) + 1
