@@ -364,6 +364,18 @@ class ModuleRuntime:
     # -- fixed-shape replacements of dynamic-shape ops whose
     #    only consumer is a full sum (see lowering._lower_dynamic_shape)
     @staticmethod
+    def linear_relu(mod, x):
+        """relu(mod(x)).  For an nn.Linear with bias on a CUDA tensor: one
+        cuBLASLt GEMM with the RELU_BIAS epilogue (torch._addmm_activation)
+        instead of a GEMM and a separate relu launch — relu commutes with
+        the rounding of the output, so the value is relu(Linear(x))."""
+        if (isinstance(mod, torch.nn.Linear) and mod.bias is not None and torch.is_tensor(x) and x.is_cuda
+                and x.dim() >= 2 and x.dtype == mod.weight.dtype and x.shape[-1] == mod.in_features):
+            y = torch._addmm_activation(mod.bias, x.reshape(-1, mod.in_features), mod.weight.t())
+            return y.view(*x.shape[:-1], mod.out_features)
+        return torch.relu(mod(x))
+
+    @staticmethod
     def nonzero_sum(mask):
         """== torch.nonzero(mask).sum() (int64).  Inside a fused region this
         is a coordinate-sum reduction; here (unfused) it is computed without

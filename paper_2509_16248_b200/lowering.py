@@ -248,6 +248,9 @@ class _FunctionLowerer:
             def split(e: ast.expr) -> ast.expr:
                 if self._fusable(e):
                     return e
+                lr = self._linear_relu(e)
+                if lr is not None:
+                    e = lr
                 if isinstance(e, ast.BinOp):
                     return ast.BinOp(split(e.left), e.op, split(e.right))
                 if isinstance(e, ast.UnaryOp):
@@ -262,6 +265,13 @@ class _FunctionLowerer:
                 return ast.Name(name, ast.Load())
 
             new_value = split(s.value)
+            if len(temps) == 1 and isinstance(new_value, ast.Name) and isinstance(temps[0].value, ast.Call) \
+                    and ast.unparse(temps[0].value.func) == f"{GM_RT}.linear_relu":
+                # the whole statement was relu(Linear(x))
+                res = ast.copy_location(ast.Assign(targets=s.targets, value=temps[0].value), s)
+                res.end_lineno, res.end_col_offset = s.end_lineno, s.end_col_offset
+                out.append(res)
+                continue
             if not temps or isinstance(new_value, ast.Name) or not self._fusable(new_value):
                 out.append(s)
                 continue
@@ -270,6 +280,24 @@ class _FunctionLowerer:
             ast.fix_missing_locations(res)
             out.extend(temps + [res])
         return out
+
+    def _linear_relu(self, e: ast.expr) -> ast.expr | None:
+        """`relu(m(x))` with m a module call -> `__gm_rt__.linear_relu(m, x)`:
+        for an nn.Linear on CUDA one cuBLASLt GEMM with the RELU_BIAS
+        epilogue (relu commutes with the output rounding, so the value is
+        relu(Linear(x))); otherwise the runtime falls back to relu(m(x))."""
+        mods = self.owner.torch_names | self.owner.functional_names
+        if not (isinstance(e, ast.Call) and isinstance(e.func, ast.Attribute) and e.func.attr == "relu"
+                and isinstance(e.func.value, ast.Name) and e.func.value.id in mods
+                and len(e.args) == 1 and not e.keywords):
+            return None
+        inner = e.args[0]
+        if not (isinstance(inner, ast.Call) and len(inner.args) == 1 and not inner.keywords
+                and not isinstance(inner.args[0], ast.Starred) and attr_chain(inner.func) is not None
+                and attr_chain(inner.func)[0] not in mods and not self._fusable(inner)):
+            return None
+        return ast.Call(ast.Attribute(ast.Name(GM_RT, ast.Load()), "linear_relu", ast.Load()),
+                        [inner.func, inner.args[0]], [])
 
     def lower_block(self, stmts: list[ast.stmt], in_loop: bool) -> list[ast.stmt]:
         out: list[ast.stmt] = []
