@@ -154,3 +154,23 @@ def test_boolean_predicates_lowered():
     plan = codegen.Plan(low.regions[0].graph, low.regions[0].out_nodes, [torch.randn(4096)], "f", allow_cpu=True)
     assert plan.npass == 3
     nat.compile_cubin(plan.source, (10, 0))
+
+
+def test_calls_hoisted_out_of_elementwise_expressions(programs):
+    """bart_step: `out = self.fc2(f) + h` becomes `t = self.fc2(f); out = t + h`
+    so the add fuses with the epilogue `out * 0.5`; `relu(self.fc1(h))`
+    becomes one cuBLASLt GEMM with a RELU_BIAS epilogue (linear_relu)."""
+    low, _ = lowering.lower(programs["bart_step"]["transformed"])
+    assert [r.out_names for r in low.regions] == [["h"], ["__gm_ret_0"]]
+    body = low.source.split("def forward")[1]
+    assert "__gm_rt__.linear_relu(self.fc1, h)" in body
+    assert "= self.fc2(f)" in body and "torch.relu" not in body
+
+
+def test_linear_relu_cpu_fallback_is_exact():
+    from paper_2509_16248_b200.logring import ModuleRuntime
+
+    torch.manual_seed(0)
+    lin = torch.nn.Linear(16, 8)
+    x = torch.randn(3, 5, 16)
+    assert torch.equal(ModuleRuntime.linear_relu(lin, x), torch.relu(lin(x)))
