@@ -910,6 +910,8 @@ class Plan:
         # results before the first global read (a no-op without PDL)
         w('  asm volatile("griddepcontrol.wait;" ::: "memory");')
         w("  u64 ep_ = gm::grid_epoch_begin(P); (void)ep_;  // arrival epoch (thread 0)")
+        w("  __shared__ int s_epi_;  // does this CTA write the scalar outputs / mirror")
+        w("  if (threadIdx.x == 0) s_epi_ = blockIdx.x == 0;")
         for ip in self.inputs:
             if ip.mode == MODE_FULL and self.stage[ip.slot] == "smem":
                 w(f"  const u32 sres{ip.slot} = smem_u32(smem + {self.smem_off[ip.slot]});")
@@ -960,7 +962,7 @@ class Plan:
     def _emit_epilogue(self, w, ind: str, miss: bool) -> None:
         """Scalar outputs, the debug mirror and (speculative kernels) the
         prediction update + hit/miss counters, by CTA 0 thread 0."""
-        w(f"{ind}if (blockIdx.x == 0 && threadIdx.x == 0) {{")
+        w(f"{ind}if (s_epi_ && threadIdx.x == 0) {{")
         for j, o in enumerate(self.outputs):
             if o.kind == "dscalar":
                 k = self._out_slot(j)
@@ -1082,16 +1084,27 @@ class Plan:
                 w(f"    for (int kb = 0; kb < {self.K}; kb += {kb}) {{")
                 self._emit_block(w, "kb", kb, elem_nodes, reds, outs, guards, loads, pref)
                 w("    }")
+        # the launch's last reduction (exact path, results feed only scalar
+        # outputs): the completing CTA combines alone, the others exit
+        last_arriver = (bool(reds) and not spec and ctx == self.npass - 1 and not deferred
+                        and os.environ.get("GM_LAST_ARRIVER", "1") != "0")
         if not deferred:
             if self.n % nat.VEC:
                 for line in self._late:
                     w("    " + line)
                 self._emit_tail(w, elem_nodes, reds, outs, guards)
             stamp_loop_end()
-            if reds:
+            if reds and not last_arriver:
                 arrive()
-        if reds:
+        if last_arriver:
+            vals = ", ".join(f"__longlong_as_double((long long)acc{k})" if r.op in ("argmax", "argmin")
+                             else f"(double)acc{k}" for k, r in enumerate(reds))
+            w(f"    {{ double vals_[{nr}] = {{{vals}}};")
+            w(f"      if (!gm::grid_reduce_last(P, {nr}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs})) return; }}")
+            w("    if (threadIdx.x == 0) s_epi_ = 1;  // this CTA writes the scalar outputs")
+        elif reds:
             w(f"    grid_wait(P, {nr}, ops_, slots_, tgt_, s_red{pargs});")
+        if reds:
             if prof:
                 idx = 2 + 2 * pidx
                 w(f"    if (threadIdx.x == 0) atomicMax(&prof_[{idx}], gm::globaltimer());")

@@ -877,6 +877,70 @@ __device__ __forceinline__ void grid_wait(const Params& P, int nr, const int* op
   GM_STAMP(2);
 }
 
+// Final reduction of a launch (its results feed only scalar outputs): the
+// CTA whose arrival completes the epoch combines the partials alone; the
+// others return false and may exit — nobody polls.  Same fixed combine
+// order as grid_wait, so the statistics are bit-identical to it.
+__device__ __forceinline__ bool grid_reduce_last(const Params& P, int nr, const int* ops, const int* slots,
+                                                 double* vals, double* s_warp, double* s_out, u64& ep,
+                                                 u64* prof = nullptr) {
+  __shared__ int s_last_;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < nr; ++r) {
+    const double v = warp_combine(ops[r], vals[r]);
+    if (lane == 0) s_warp[warp * GM_MAX_RED + r] = v;
+  }
+  __syncthreads();
+  const bool multi = gridDim.x > 1;
+  double* partials = (double*)P.partials;
+  if (warp == 0) {
+#pragma unroll
+    for (int r = 0; r < nr; ++r) {
+      double v = lane < GM_WARPS ? s_warp[lane * GM_MAX_RED + r] : red_identity(ops[r]);
+      v = warp_combine(ops[r], v);
+      if (lane == 0) {
+        if (multi)
+          partials[(i64)slots[r] * gridDim.x + blockIdx.x] = v;
+        else
+          s_out[r] = v;
+      }
+    }
+  }
+  if (!multi) {
+    __syncthreads();
+    return true;
+  }
+  if (threadIdx.x == 0) {
+    const u64 old = atom_add_acq_rel64((u64*)P.barrier, 1ull);
+    s_last_ = (old % gridDim.x) == gridDim.x - 1;
+    (void)ep;
+  }
+  __syncthreads();
+  if (!s_last_) return false;
+#pragma unroll
+  for (int r = 0; r < nr; ++r) {
+    if (r % GM_WARPS != warp) continue;
+    const double* base = partials + (i64)slots[r] * gridDim.x;
+    double acc = red_identity(ops[r]);
+    for (u32 b0 = 0; b0 < gridDim.x; b0 += 32 * 16) {
+      double t[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const u32 b = b0 + i * 32 + lane;
+        t[i] = b < gridDim.x ? ld_relaxed_f64(base + b) : red_identity(ops[r]);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc = red_combine(ops[r], acc, t[i]);
+    }
+    acc = warp_combine(ops[r], acc);
+    if (lane == 0) s_out[r] = acc;
+  }
+  __syncthreads();
+  GM_STAMP(2);
+  return true;
+}
+
 // Reduce `nr` per-thread values across the grid; the results land in s_out[r]
 // in every CTA.
 //   1. CTA partial: warp butterfly, then warp 0 over the warps (fixed tree);
