@@ -15,13 +15,13 @@ import concurrent.futures as cf
 
 import torch
 
-from .codegen import Plan
+from .codegen import B200_DEVICE, Plan
 from .harness import make_args, programs
 from .ir import Unsupported
 from .lowering import load
 from .region import aot_compile
 
-B200 = (148, 232448)   # SMs, max opt-in dynamic shared memory per block
+B200 = B200_DEVICE   # SMs, max opt-in dynamic shared memory per block
 
 # (program, dtype, shapes) — BASELINE configs 2-5 plus the corpus at its own shapes
 SPECS = [("bigbird_like", d, None) for d in (torch.bfloat16, torch.float32)] + \

@@ -57,6 +57,8 @@ RED_OP = {"sum": 0, "mean": 0, "norm": 0, "count_nonzero": 0, "nzsum": 0, "amax"
 MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strided", "scalar"
 
 STATIC_SMEM_RESERVE = 8 * 1024
+SMEM_PER_SM = 233472    # B200: 228 KB of shared memory per SM (shared by its resident CTAs)
+B200_DEVICE = (148, 232448)  # SMs, opt-in dynamic shared memory per block
 DATA_REGS = int(os.environ.get("GM_DATA_REGS", "40"))  # raw-vector registers per thread: register stage + one block's loads
 VEC_REGS = {torch.float32: 8, torch.bfloat16: 4, torch.float16: 4, torch.bool: 2}
 MAX_DECISIONS = 24      # predicted decisions per speculative region (scratch ints at barrier + 288)
@@ -110,7 +112,7 @@ class Plan:
     """One specialisation of a region for concrete argument types/shapes."""
 
     def __init__(self, graph: Graph, outputs: list[Node], args: list, name: str = "region",
-                 device_info: tuple[int, int] = (148, 232448), allow_cpu: bool = False):
+                 device_info: tuple[int, int] = B200_DEVICE, allow_cpu: bool = False):
         self.device_info = device_info
         self.allow_cpu = allow_cpu
         self.graph = graph
@@ -142,6 +144,8 @@ class Plan:
             raise Unsupported(f"outputs/reductions disagree on shape: {shapes}")
         self.shape = next(iter(shapes)) if shapes else ()
         self.n = math.prod(self.shape) if shapes else 0
+        if self.n >= 2 ** 32 and any(n.op in ("argmax", "argmin") for n in red_nodes):
+            raise Unsupported("argmax/argmin keys carry a 32-bit index")
         for node in self.order:
             if node.kind == "elem":
                 if not is_fusable_dtype(node.dtype):
@@ -802,7 +806,7 @@ class Plan:
         for ip in staged:
             self.stage[ip.slot] = "reg"
             self.load_pass[ip.slot] = 0 if ip in later else min(ip.passes)
-        budget = 233472 // self.minb - STATIC_SMEM_RESERVE
+        budget = SMEM_PER_SM // self.minb - STATIC_SMEM_RESERVE
         used = 0
         for ip in multi + later:
             if ip in staged or DT_SIZE[ip.dtype] < 2:
