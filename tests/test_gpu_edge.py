@@ -191,3 +191,22 @@ def test_hoisted_max_guard(programs, dtype):
         assert_parity(out, ref, dtype, what=f"longformer {name}")
     r = low.regions[0]
     assert r.last_spec.plan.hoisted, "the max was not hoisted"
+
+
+@pytest.mark.gpu
+def test_beyond_int32_elements():
+    """A predicated block over 2^31 + 5 elements (beyond 32-bit indexing,
+    with a partial tail vector): vector indices, staging decisions and the
+    grid reduce are 64-bit.  Property check instead of the CPU oracle (4 GB
+    per tensor): x = 1 everywhere, so sum > 0 and every output is 2."""
+    n = 2 ** 31 + 5
+    x = torch.ones(n, dtype=torch.bfloat16, device="cuda")
+    ex, mod, low = compile_program(BLOCK, "f")
+    out = ex(x, torch.ones((), dtype=torch.bfloat16, device="cuda"))
+    torch.cuda.synchronize()
+    assert any(r.stats.launches for r in low.regions)
+    assert out.shape == (n,) and out.dtype == torch.bfloat16
+    assert float(out.min()) == 2.0 and float(out.max()) == 2.0
+    assert float(out[-1]) == 2.0 and float(out[2 ** 31]) == 2.0
+    spec = low.regions[0].last_spec
+    assert spec.status() == 0 and spec.plan.n == n
