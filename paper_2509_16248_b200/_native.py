@@ -28,6 +28,15 @@ THREADS = 512
 VEC = 8
 LAUNCH_PDL = 1   # GM_LAUNCH_PDL
 
+# kernels this library launched (incremented per launching call; a CUDA graph
+# replays what was counted while it was captured) — bench.py's gpu_launches
+launch_count = 0
+
+
+def count_launches(k: int = 1) -> None:
+    global launch_count
+    launch_count += k
+
 
 class NativeError(RuntimeError):
     """A libgm_b200 call returned a non-zero status."""
@@ -212,6 +221,7 @@ class CompiledRegion:
         return n.value
 
     def launch(self, params: Params, grid: int, threads: int, smem: int, stream: int, pdl: bool = False) -> None:
+        count_launches()
         check(
             lib().gm_region_launch_ex(self.handle, ctypes.byref(params), ctypes.sizeof(params), grid, threads, smem,
                                       ctypes.c_void_p(stream), LAUNCH_PDL if pdl else 0),

@@ -177,6 +177,7 @@ class LogRing:
                                                 self.slot_bytes, self.n_slots, off, ctypes.c_void_p(stream)),
                     "gm_logring_gather",
                 )
+                nat.count_launches()
                 self.gathers += 1
                 tmpl.gathers += 1
                 gf = a.grad_fn
@@ -197,6 +198,7 @@ class LogRing:
         if tmpl.gathers:
             stream = torch.cuda.current_stream(self.device).cuda_stream
             nat.check(nat.lib().gm_logring_commit(self.handle, ctypes.c_void_p(stream)), "gm_logring_commit")
+            nat.count_launches()
         return tmpl
 
     @property
@@ -400,6 +402,7 @@ class ModuleRuntime:
                 and x.data_ptr() % 16 == 0:
             out = torch.empty((), dtype=x.dtype, device=x.device)
             scratch = _unique_scratch(x.device)
+            nat.count_launches(2)
             nat.check(nat.lib().gm_unique_sum16(
                 ctypes.c_void_p(x.data_ptr()), x.numel(), nat.GM_BF16 if x.dtype == torch.bfloat16 else nat.GM_F16, ctypes.c_void_p(out.data_ptr()),
                 ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
@@ -409,6 +412,7 @@ class ModuleRuntime:
             out = torch.empty((), dtype=x.dtype, device=x.device)
             nb = nat.lib().gm_unique_sum32_scratch_bytes(x.numel())
             scratch = torch.empty(nb, dtype=torch.uint8, device=x.device)
+            nat.count_launches(2)  # the two distinct-sum kernels (the CUB radix-sort passes are not counted)
             nat.check(nat.lib().gm_unique_sum32(
                 ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
                 ctypes.c_void_p(scratch.data_ptr()), nb, ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
