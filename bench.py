@@ -215,7 +215,7 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(prog, shapes, dtype, budget_s=15.0):
+def cpu_baseline(prog, shapes, dtype, budget_s=10.0):
     """Bounded CPU-oracle sample on the box's host cores (rank 0, N=1)."""
     import torch
 
@@ -228,7 +228,7 @@ def cpu_baseline(prog, shapes, dtype, budget_s=15.0):
     orc.call_captured(fn, x)
     times = []
     t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end and len(times) < 50:
+    while time.perf_counter() < t_end and len(times) < 2000:
         t0 = time.perf_counter()
         orc.call_captured(fn, x)
         times.append(time.perf_counter() - t0)
