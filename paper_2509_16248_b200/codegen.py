@@ -769,9 +769,11 @@ class Plan:
         # tools/ab_regions.py): one CTA per SM, 128 registers a thread.
         wide = any(VEC_REGS.get(ip.dtype, 4) == 8 for ip in self.inputs if ip.mode == MODE_FULL) \
             and len(self.reductions) >= 3
-        self.minb = int(os.environ.get("GM_CTAS_PER_SM", "1" if wide else "2"))
-        self.grid = max(1, min(self.minb * sms, -(-max(self.vfull, 1) // nat.THREADS)))
-        self.T = self.grid * nat.THREADS
+        self.threads = int(os.environ.get("GM_CTA_THREADS", str(nat.THREADS)))
+        per_sm = 1024 // self.threads     # 2 x 512 or 1 x 1024 threads per SM
+        self.minb = int(os.environ.get("GM_CTAS_PER_SM", str(max(1, per_sm // 2) if wide else per_sm)))
+        self.grid = max(1, min(self.minb * sms, -(-max(self.vfull, 1) // self.threads)))
+        self.T = self.grid * self.threads
         self.K = -(-self.vfull // self.T) if self.vfull else 0
         self.stage = {ip.slot: "none" for ip in self.inputs}
         self.load_pass: dict[int, int] = {}
@@ -811,7 +813,7 @@ class Plan:
         for ip in multi + later:
             if ip in staged or DT_SIZE[ip.dtype] < 2:
                 continue
-            b = (self.K * nat.THREADS * nat.VEC * DT_SIZE[ip.dtype] + 127) // 128 * 128
+            b = (self.K * self.threads * nat.VEC * DT_SIZE[ip.dtype] + 127) // 128 * 128
             if used + b <= min(budget, smem_optin - STATIC_SMEM_RESERVE):
                 self.stage[ip.slot] = "smem"
                 self.smem_off[ip.slot] = used
@@ -885,6 +887,8 @@ class Plan:
         self.profiled = prof
         if prof:
             w("#define GM_PROF 1")
+        if self.threads != nat.THREADS:
+            w(f"#define GM_THREADS {self.threads}")
         if os.environ.get("GM_ARRIVE_RED"):
             w(f"#define GM_ARRIVE_RED {int(os.environ['GM_ARRIVE_RED'])}")
         if os.environ.get("GM_ARRIVE_SPLIT"):
@@ -893,7 +897,7 @@ class Plan:
         w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
         w("#define gm_trunc(x) ((double)(long long)(x))")
         w(f"// region {self.name}: shape {list(self.shape)}, {self.npass} pass(es), "
-          f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s); grid {self.grid} x {nat.THREADS}, "
+          f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s); grid {self.grid} x {self.threads}, "
           f"{self.K} vector(s)/thread{', speculative' if self.spec else ''}")
         w(f'extern "C" __global__ void __launch_bounds__(GM_THREADS, {self.minb})')
         w("GM_KERNEL_NAME(const __grid_constant__ gm::Params P) {")

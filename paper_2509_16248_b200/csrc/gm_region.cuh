@@ -48,7 +48,9 @@ typedef unsigned char u8;
 #define GM_MAX_HS 32
 #define GM_MAX_DIMS 6
 #define GM_MAX_PIECES 16
-#define GM_THREADS 512
+#ifndef GM_THREADS
+#define GM_THREADS 512  // threads per CTA (a generated region may define 1024)
+#endif
 #define GM_WARPS (GM_THREADS / 32)
 #define GM_VEC 8
 

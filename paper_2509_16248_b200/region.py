@@ -115,7 +115,7 @@ class _Spec:
         self.kernel = compiled_kernel(plan.source, plan.kernel)
         n = plan.n
         nvec = -(-n // nat.VEC) if n else 0
-        threads = nat.THREADS
+        threads = plan.threads
         grid, smem = plan.grid, plan.smem_bytes
         vpc = plan.K
         if plan.reductions and grid > 1:
