@@ -53,6 +53,22 @@ def test_float_item_scalars_are_not_speculated(programs):
     assert "speculative pass" not in plan.source
 
 
+def test_monotone_max_is_hoisted(programs, monkeypatch):
+    """longformer_like: `peak = (win * w0).max()` is taken from max/min(win)
+    at pass 0's grid reduce; pass 1's sweep runs only if the device-side
+    finiteness guard fails.  GM_HOIST=0 keeps the 3-sweep kernel."""
+    plan = _plan(programs, "longformer_like", torch.bfloat16, (4, 4096, 768))
+    assert list(plan.hoisted) == [1]
+    (r, e, y, s, direction, hmax, hmin), = plan.hoisted[1]
+    assert r.op == "amax" and e.op == "mul" and direction == 0
+    assert hmax in plan.pass_reds[0] and hmin in plan.pass_reds[0]
+    assert "if (!s_hoist1)" in plan.source
+    monkeypatch.setenv("GM_HOIST", "0")
+    plan = _plan(programs, "longformer_like", torch.bfloat16, (4, 4096, 768))
+    assert not plan.hoisted and "s_hoist" not in plan.source
+    assert [len(plan.pass_reds[p]) for p in range(3)] == [1, 1, 0]
+
+
 @pytest.mark.parametrize("v,expect", [(2.0, 0.5), (0.5, 2.0), (-4.0, -0.25), (3.0, None), (0.0, None),
                                       (float("inf"), None), (2.0 ** 127, None), (1.0, 1.0)])
 def test_pow2_reciprocal(v, expect):
