@@ -85,7 +85,9 @@ def _watch_side_effects():
 def _key(args) -> tuple:
     k = []
     for a in args:
-        if torch.is_tensor(a):
+        if isinstance(a, torch.nn.Parameter):
+            k.append(("p", id(a)))          # read in place (see _Entry)
+        elif torch.is_tensor(a):
             k.append(("t", a.dtype, tuple(a.shape)))
         else:
             k.append(("v", type(a), a if isinstance(a, (int, float, bool, str, type(None))) else id(a)))
@@ -105,8 +107,12 @@ class _Entry:
         self.ex = ex
         dev = ex.device
         t0 = time.perf_counter()
+        # parameters (e.g. lifted into a Dynamo graph's inputs) are read in
+        # place: the entry is keyed by their identity, so no per-call copy
         self.static = [
-            torch.empty_like(a, device=dev).copy_(a) if torch.is_tensor(a) else a for a in args
+            a if isinstance(a, torch.nn.Parameter) and a.device == dev
+            else (torch.empty_like(a, device=dev).copy_(a) if torch.is_tensor(a) else a)
+            for a in args
         ]
         ring = logring.ring_for(dev)
         self.ring = ring
