@@ -7,7 +7,6 @@ only (see oracle/__init__.py).
 from __future__ import annotations
 
 import contextlib
-import importlib.util
 import io
 import itertools
 import linecache

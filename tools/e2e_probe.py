@@ -1,6 +1,6 @@
 import sys, time, torch
 sys.path.insert(0, '/root/repo')
-from bench import WORKLOADS, _inputs
+from bench import _inputs
 from paper_2509_16248_b200 import compile_program
 from paper_2509_16248_b200.harness import programs
 prog = programs()['bigbird_like']
@@ -12,8 +12,6 @@ outs = [torch.empty(out0.shape, dtype=out0.dtype, pin_memory=True) for _ in rang
 batches = [tuple(x_host)] * steps
 ex.run_host_pipelined(batches[:4], out=outs[:4]); ex.flush()
 torch.cuda.synchronize()
-import paper_2509_16248_b200.executor as E
-# instrument: time the issue loop by monkeypatching d2h.synchronize
 t0 = time.perf_counter()
 orig = torch.cuda.Stream.synchronize
 issue_end = []
