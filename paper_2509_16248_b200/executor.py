@@ -103,14 +103,15 @@ class EntryInfo:
 
 
 class _Entry:
-    def __init__(self, ex: "B200Executor", args: list):
+    def __init__(self, ex: "B200Executor", args: list, bound: bool = False):
         self.ex = ex
         dev = ex.device
         t0 = time.perf_counter()
         # parameters (e.g. lifted into a Dynamo graph's inputs) are read in
-        # place: the entry is keyed by their identity, so no per-call copy
+        # place: the entry is keyed by their identity, so no per-call copy.
+        # A bound entry (B200Executor.bind) reads the caller's tensors in place.
         self.static = [
-            a if isinstance(a, torch.nn.Parameter) and a.device == dev
+            a if ((bound and torch.is_tensor(a)) or isinstance(a, torch.nn.Parameter)) and a.device == dev
             else (torch.empty_like(a, device=dev).copy_(a) if torch.is_tensor(a) else a)
             for a in args
         ]
@@ -198,6 +199,22 @@ class B200Executor:
         if e is None:
             with torch.cuda.device(self.device):
                 e = _Entry(self, list(args))
+            self.entries[key] = e
+        return e
+
+    def bind(self, *args) -> _Entry:
+        """An entry captured on the caller's own CUDA tensors: `entry.run()`
+        replays the graph reading them in place (no input copy), so a serving
+        loop refills those tensors and calls `run()`.  The tensors must stay
+        alive and keep their storage; `entry.outputs` are the graph's static
+        outputs (valid until the next run)."""
+        if not all(a.device == self.device for a in args if torch.is_tensor(a)):
+            raise ValueError("bind() takes tensors on the executor's device")
+        key = ("bound",) + tuple(("t", id(a)) if torch.is_tensor(a) else ("v", type(a), a) for a in args)
+        e = self.entries.get(key)
+        if e is None:
+            with torch.cuda.device(self.device):
+                e = _Entry(self, list(args), bound=True)
             self.entries[key] = e
         return e
 

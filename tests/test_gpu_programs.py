@@ -114,3 +114,24 @@ def test_aot_cubins_are_used(programs):
     ex.flush()
     for r in low.regions:
         assert r.last_spec is not None and r.last_spec.kernel.from_cache, r.name
+
+
+@pytest.mark.gpu
+def test_bound_entry_reads_inputs_in_place(programs):
+    """B200Executor.bind: the graph is captured on the caller's tensors; a
+    serving loop refills them in place and replays with no input copy —
+    each replay equals a fresh call on the same values."""
+    prog = programs["bigbird_like"]
+    ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
+    specs = prog["inputs"]
+    first = orc.make_args(specs[0]["args"], specs[0]["seed"], torch.bfloat16)[0].cuda()
+    entry = ex.bind(first)
+    assert entry.info.mode == "graph"
+    for spec in specs:
+        x = orc.make_args(spec["args"], spec["seed"], torch.bfloat16)[0].cuda()
+        first.copy_(x)
+        out = entry.run().clone()
+        ex.flush()
+        ref = ex(x).clone()
+        ex.flush()
+        assert torch.equal(out, ref)
