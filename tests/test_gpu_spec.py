@@ -71,3 +71,40 @@ def test_forced_mispredictions_match_hits(programs):
     after = [r.last_spec.spec_stats()[1] for r in low.regions]
     assert all(a == b + 1 for a, b in zip(after, before)), (before, after)
     assert torch.equal(hit, miss)
+
+
+@pytest.mark.gpu
+def test_many_replays_stay_exact():
+    """2000 graph replays alternating three inputs whose decisions differ:
+    every output equals the first output for that input bit for bit, no
+    grid barrier ever timed out, and the misprediction count equals the
+    number of decision changes (monotonic arrival counter, prediction
+    update after every miss)."""
+    import json
+    import os
+
+    progs = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "programs.json")))
+    prog = progs["bigbird_like"]
+    ex, mod, low, _ = harness.b200_program("bigbird_like", dtype=torch.bfloat16)
+    xs = [orc.make_args(s["args"], s["seed"], torch.bfloat16)[0].cuda() for s in prog["inputs"]]
+    buf = xs[0].clone()
+    entry = ex.bind(buf)
+    firsts = []
+    for x in xs:
+        buf.copy_(x)
+        firsts.append(entry.run().clone())
+    base = [r.last_spec.spec_stats() for r in low.regions]
+    order = [(i // 7) % 3 for i in range(2000)]
+    mismatch = 0
+    for i in order:
+        buf.copy_(xs[i])
+        out = entry.run()
+        mismatch += int(not torch.equal(out, firsts[i]))
+    torch.cuda.synchronize()
+    ex.flush()
+    assert mismatch == 0
+    for r, (l0, m0) in zip(low.regions, base):
+        assert r.last_spec.status() == 0
+        launches, misses = r.last_spec.spec_stats()
+        assert launches - l0 == len(order)
+        assert misses - m0 <= sum(1 for a, b in zip(order, order[1:]) if a != b) + 1
