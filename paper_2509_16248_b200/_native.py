@@ -102,6 +102,9 @@ _SIGNATURES = [
     ("gm_region_release", ctypes.c_int, [ctypes.c_void_p]),
     ("gm_unique_sum16_scratch_bytes", ctypes.c_size_t, []),
     ("gm_unique_sum32_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
+    ("gm_unique_sum32_hash_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
+    ("gm_unique_sum32_hash", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     ("gm_unique_sum32", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     ("gm_unique_sum16", ctypes.c_int,

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1)
   const i64 v0 = (i64)blockIdx.x * P.vpc;
   const i64 v1 = (v0 + P.vpc < P.nvec) ? v0 + P.vpc : P.nvec;
   const bool resident = P.in[0].smem_off >= 0;
-  const u32 sres = resident ? smem_u32(smem + P.in[0].smem_off) : 0u;
+  const unsigned sres = resident ? smem_u32(smem + P.in[0].smem_off) : 0u;
   u64 ep_ = grid_epoch_begin(P);
   Stage st, st_unused;
   st.wend = st_unused.wend = 0;
@@ -336,6 +336,299 @@ __global__ void __launch_bounds__(1024) gm_sum_partials_kernel(const double* __r
     for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     if (threadIdx.x == 0) *out = (float)t;
   }
+}
+
+// fp32, sort-free distinct sum.  Deduplication: values whose binade lies in
+// a window of GM_U32_WIN binades below the largest finite exponent set one
+// bit of a presence bitmap (sign x binade x 2^23 mantissas; red.or, so a
+// duplicate is free); the rest go to a hash set of the value bits (open
+// addressing, 64-bit slots = call tag << 32 | bits, so a slot written by an
+// earlier call reads as empty and the table is never cleared).  Summation is
+// EXACT: v = M * 2^shift * 2^-149 with M < 2^24 is added into a fixed-point
+// super-accumulator of 32-bit digits held in int64 (per thread in local
+// memory, per CTA in shared memory, per call in global memory) — integer
+// sums, so the result does not depend on which thread saw a value first.
+// The bitmap pass sums the mantissas of the set bits per binade (an exact
+// int64) and clears the words it read, ready for the next call.  The finish
+// rounds the exact sum once to fp32 (nearest-even).  NaN anywhere -> NaN;
+// +inf and -inf -> NaN; one infinity -> it.
+#define GM_U32_DIGITS 11
+#define GM_U32_WIN 16
+#define GM_U32_BITMAP_WORDS (2ull * GM_U32_WIN << 18)   // 2 signs x WIN binades x 2^23 bits
+__device__ __forceinline__ unsigned gm_hash32(unsigned x) {
+  x ^= x >> 16; x *= 0x85ebca6bu; x ^= x >> 13; x *= 0xc2b2ae35u; x ^= x >> 16;
+  return x;
+}
+
+// acc += (neg ? -1 : 1) * S * 2^shift (S < 2^48), digits of 32 bits
+__device__ __forceinline__ void gm_u32_acc_add(long long* acc, unsigned long long S, int shift, bool neg) {
+  const int d = shift >> 5, off = shift & 31;
+  const unsigned long long lo = (S & 0xffffffffull) << off, hi = (S >> 32) << off;
+  long long a0 = (long long)(lo & 0xffffffffull), a1 = (long long)(lo >> 32) + (long long)(hi & 0xffffffffull),
+            a2 = (long long)(hi >> 32);
+  if (neg) { a0 = -a0; a1 = -a1; a2 = -a2; }
+  acc[d] += a0; acc[d + 1] += a1;
+  if (d + 2 < GM_U32_DIGITS) acc[d + 2] += a2;
+}
+
+// CTA total of the per-thread digit arrays -> global atomics.  Warp sums by
+// shuffle, then one thread per digit adds the warps' sums (64-bit shared
+// atomics are CAS loops on this GPU — 512-way contention on them is slow).
+__device__ __forceinline__ void gm_u32_flush(long long* acc, long long (*swarp)[GM_U32_DIGITS],
+                                             long long* digits) {
+#pragma unroll
+  for (int d = 0; d < GM_U32_DIGITS; ++d) {
+    long long v = acc[d];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) swarp[threadIdx.x >> 5][d] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < GM_U32_DIGITS) {
+    long long v = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += swarp[w][threadIdx.x];
+    if (v) atomicAdd((unsigned long long*)&digits[threadIdx.x], (unsigned long long)v);
+  }
+}
+
+// largest biased exponent among finite values -> *emax (atomicMax; memset 0)
+__global__ void __launch_bounds__(512) gm_unique32_window_kernel(const float* __restrict__ x, long long n,
+                                                                 int* __restrict__ emax) {
+  unsigned m = 0;
+  const long long T = (long long)gridDim.x * blockDim.x, t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n4 = ((uintptr_t)x & 15) ? 0 : n >> 2;
+  auto fin = [](unsigned b) { const unsigned e = (b >> 23) & 0xff; return e == 255 ? 0u : e; };
+#pragma unroll 4
+  for (long long i = t0; i < n4; i += T) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(x) + i);
+    m = max(m, max(max(fin(v.x), fin(v.y)), max(fin(v.z), fin(v.w))));
+  }
+  for (long long i = n4 * 4 + t0; i < n; i += T) {
+    const unsigned e = (__float_as_uint(x[i]) >> 23) & 0xff;
+    m = max(m, e == 255 ? 0u : e);
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(emax, (int)m);
+}
+
+__global__ void __launch_bounds__(512) gm_unique32_insert_kernel(const float* __restrict__ x, long long n,
+                                                                 unsigned* __restrict__ bitmap,
+                                                                 const int* __restrict__ emax,
+                                                                 unsigned long long* __restrict__ table,
+                                                                 unsigned long long mask,
+                                                                 const unsigned long long* __restrict__ calls,
+                                                                 long long* __restrict__ digits,
+                                                                 int* __restrict__ flags,
+                                                                 unsigned* __restrict__ touched) {
+  __shared__ long long swarp[16][GM_U32_DIGITS];
+  const unsigned tag = (unsigned)(*calls % 0xffffffffull) + 1u;
+  const int lo_e = max(*emax - (GM_U32_WIN - 1), 0);
+  long long acc[GM_U32_DIGITS];
+#pragma unroll
+  for (int d = 0; d < GM_U32_DIGITS; ++d) acc[d] = 0;
+  int fl = 0;
+  unsigned tm = 0;                                       // bitmap slices (sign x binade) this thread marked
+  // bitmap values: returns the bit index (the caller marks it); otherwise
+  // handles the value (flags, hash set) and returns NONE
+  constexpr unsigned long long NONE = ~0ull;
+  auto one = [&](unsigned bits) -> unsigned long long {
+    const unsigned e = (bits >> 23) & 0xffu;
+    if (e == 255u) {                                     // inf / NaN
+      fl |= (bits & 0x007fffffu) ? 1 : ((bits >> 31) ? 4 : 2);
+      return NONE;
+    }
+    if ((bits & 0x7fffffffu) == 0) return NONE;          // +-0 adds nothing
+    if ((int)e >= lo_e) {
+      const unsigned slice = (bits >> 31) * GM_U32_WIN + (e - lo_e);
+      tm |= 1u << slice;
+      return ((unsigned long long)slice << 23) | (bits & 0x7fffffu);
+    }
+    const unsigned long long want = ((unsigned long long)tag << 32) | bits;
+    unsigned long long h = gm_hash32(bits) & mask;
+    while (true) {
+      unsigned long long cur;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(table + h) : "memory");
+      if ((unsigned)(cur >> 32) == tag) {
+        if ((unsigned)cur == bits) return NONE;          // seen
+        h = (h + 1) & mask;
+        continue;
+      }
+      if (atomicCAS(table + h, cur, want) == cur) break; // claimed: first occurrence
+      // lost a race for this slot: re-examine it (it now holds this tag)
+    }
+    const unsigned fr = bits & 0x7fffffu;
+    gm_u32_acc_add(acc, e ? (fr | 0x800000u) : fr, e ? (int)e - 1 : 0, bits >> 31);
+    return NONE;
+  };
+  // mark a batch: read the words first (L1/L2; a word read stale shows a
+  // subset of its bits, so a skipped red.or is always one already done) and
+  // issue red.or only for bits not yet set — duplicates of hot values (a
+  // narrow value range) would otherwise serialise on a few L2 lines
+  auto mark = [&](const unsigned long long (&b)[4]) {
+    unsigned w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = b[k] != NONE ? __ldca(bitmap + (b[k] >> 5)) : ~0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (b[k] != NONE && !(w[k] >> (b[k] & 31) & 1u)) atomicOr(bitmap + (b[k] >> 5), 1u << (b[k] & 31));
+  };
+  const long long T = (long long)gridDim.x * blockDim.x, t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n4 = ((uintptr_t)x & 15) ? 0 : n >> 2;
+  // four 16-byte loads in flight per thread before any atomic is issued
+  // (the hash path's relaxed loads would otherwise serialise the sweep)
+  for (long long i = t0; i < n4; i += 4 * T) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = i + u * T < n4 ? __ldcs(reinterpret_cast<const uint4*>(x) + i + u * T) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned long long b[4] = {one(v[u].x), one(v[u].y), one(v[u].z), one(v[u].w)};
+      mark(b);
+    }
+  }
+  for (long long i = n4 * 4 + t0; i < n; i += T) {
+    const unsigned long long b[4] = {one(__float_as_uint(x[i])), NONE, NONE, NONE};
+    mark(b);
+  }
+  if (fl) atomicOr(flags, fl);
+  tm = __reduce_or_sync(0xffffffffu, tm);
+  if ((threadIdx.x & 31) == 0 && tm) atomicOr(touched, tm);
+  gm_u32_flush(acc, swarp, digits);
+}
+
+__device__ void gm_u32_finish(const long long* digits, const int* flags, unsigned long long* calls, float* out);
+
+// sum the mantissas of the set bits of the presence bitmap, clearing it;
+// the last CTA to finish rounds the call's total into *out
+__global__ void __launch_bounds__(512) gm_unique32_bitmap_sum_kernel(uint4* __restrict__ bitmap,
+                                                                     const int* __restrict__ emax,
+                                                                     const unsigned* __restrict__ touched,
+                                                                     long long* __restrict__ digits,
+                                                                     unsigned* __restrict__ done,
+                                                                     const int* __restrict__ flags,
+                                                                     unsigned long long* __restrict__ calls,
+                                                                     float* __restrict__ out) {
+  __shared__ long long swarp[16][GM_U32_DIGITS];
+  const int lo_e = max(*emax - (GM_U32_WIN - 1), 0);
+  long long acc[GM_U32_DIGITS];
+#pragma unroll
+  for (int d = 0; d < GM_U32_DIGITS; ++d) acc[d] = 0;
+  // only the slices some value marked are swept (untouched ones are zero):
+  // virtual vector index v -> slice = the (v >> 16)-th set bit of `touched`
+  const unsigned tmask = *touched;
+  const long long nv = (long long)__popc(tmask) << 16, T = (long long)gridDim.x * blockDim.x;
+  // each warp walks one contiguous chunk (lanes interleaved, so loads
+  // coalesce) and so meets few binades
+  const long long warps = T >> 5, wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long per = ((nv + warps - 1) / warps + 31) & ~31ll;
+  const long long v0 = wid * per + (threadIdx.x & 31), v1 = min(nv, wid * per + per);
+  long long cur_b = -1;
+  unsigned long long S = 0;
+  auto flush_binade = [&]() {
+    if (cur_b >= 0 && S) {
+      const int e = lo_e + (int)(cur_b % GM_U32_WIN);
+      if (e < 255) gm_u32_acc_add(acc, S, e ? e - 1 : 0, cur_b >= GM_U32_WIN);
+    }
+    S = 0;
+  };
+  auto real = [&](long long vv) -> long long {
+    return ((long long)__fns(tmask, 0, (int)(vv >> 16) + 1) << 16) | (vv & 0xffff);
+  };
+  for (long long vb = v0; vb < v1; vb += 32 * 4) {
+    uint4 qs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) qs[u] = vb + 32 * u < v1 ? bitmap[real(vb + 32 * u)] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long v = real(vb + 32 * u);
+      const uint4 q = qs[u];
+      if (!(q.x | q.y | q.z | q.w)) continue;
+      bitmap[v] = make_uint4(0, 0, 0, 0);
+      const long long b = (v * 4) >> 18;                   // sign * WIN + binade
+      if (b != cur_b) { flush_binade(); cur_b = b; }
+      const int e = lo_e + (int)(b % GM_U32_WIN);
+      const unsigned base_m = e ? 0x800000u : 0u;
+      const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned x = w[k];
+        if (!x) continue;
+        const unsigned j = (unsigned)((v * 4 + k) & ((1 << 18) - 1));   // word within the binade
+        const unsigned idx_sum = __popc(x & 0xaaaaaaaau) + 2 * __popc(x & 0xccccccccu) + 4 * __popc(x & 0xf0f0f0f0u) +
+                                 8 * __popc(x & 0xff00ff00u) + 16 * __popc(x & 0xffff0000u);
+        S += (unsigned long long)__popc(x) * (base_m + j * 32u) + idx_sum;
+      }
+    }
+  }
+  flush_binade();
+  gm_u32_flush(acc, swarp, digits);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      gm_u32_finish(digits, flags, calls, out);
+    }
+  }
+}
+
+// one thread: round the exact sum to fp32 (or the NaN/inf outcome) -> *out
+__device__ void gm_u32_finish(const long long* digits, const int* flags, unsigned long long* calls, float* out) {
+  const int fl = __ldcg(flags);
+  float r;
+  if ((fl & 1) || (fl & 6) == 6) {
+    r = __int_as_float(0x7fc00000);
+  } else if (fl & 2) {
+    r = __int_as_float(0x7f800000);
+  } else if (fl & 4) {
+    r = __int_as_float(0xff800000);
+  } else {
+    // carry-normalise the signed 32-bit digits into a two's complement integer
+    unsigned mag[GM_U32_DIGITS + 1];
+    long long c = 0;
+    for (int d = 0; d < GM_U32_DIGITS; ++d) {
+      const long long t = __ldcg(digits + d) + c;
+      const long long q = t >> 32;                      // floor division by 2^32
+      mag[d] = (unsigned)(t - (q << 32));
+      c = q;
+    }
+    mag[GM_U32_DIGITS] = (unsigned)c;
+    const bool neg = c < 0;
+    if (neg) {                                          // magnitude = -value
+      unsigned long long carry = 1;
+      for (int d = 0; d <= GM_U32_DIGITS; ++d) {
+        const unsigned long long t = (unsigned long long)(~mag[d]) + carry;
+        mag[d] = (unsigned)t;
+        carry = t >> 32;
+      }
+    }
+    int top = -1;
+    for (int d = GM_U32_DIGITS; d >= 0 && top < 0; --d)
+      if (mag[d]) top = d * 32 + 31 - __clz(mag[d]);
+    unsigned fb;
+    if (top < 23) {
+      fb = mag[0];                                      // subnormal (or zero): exact
+    } else {
+      auto bit = [&](int b) -> unsigned { return b < 0 ? 0u : (mag[b >> 5] >> (b & 31)) & 1u; };
+      unsigned m = 0;
+      for (int b = top; b > top - 24; --b) m = (m << 1) | bit(b);
+      const unsigned g = bit(top - 24);
+      const int gb = top - 24;                          // guard bit; sticky = any bit below it
+      unsigned sticky = gb > 0 ? mag[gb >> 5] & ((1u << (gb & 31)) - 1u) : 0u;
+      for (int d = 0; d < (gb >> 5) && !sticky; ++d) sticky |= mag[d];
+      int B = top;
+      if (g && (sticky || (m & 1u))) {
+        ++m;
+        if (m >> 24) { m >>= 1; ++B; }
+      }
+      const int ef = B - 22;                            // biased exponent
+      fb = ef >= 255 ? 0x7f800000u : (((unsigned)ef << 23) | (m & 0x7fffffu));
+    }
+    r = __uint_as_float(fb | (neg ? 0x80000000u : 0u));
+  }
+  *out = r;
+  *calls += 1;
 }
 
 int esize_of(int dtype) {
@@ -695,6 +988,48 @@ int gm_unique_sum16(const void* x, int64_t n, int dtype, void* out, void* scratc
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// hash-set capacity: a power of two >= 2n (load <= 1/2)
+static unsigned long long u32_table_slots(int64_t n) {
+  unsigned long long s = 1ull << 16;
+  while (s < 2ull * (unsigned long long)n) s <<= 1;
+  return s;
+}
+
+size_t gm_unique_sum32_hash_scratch_bytes(int64_t n) {
+  return 4096 + 4 * GM_U32_BITMAP_WORDS + 8 * u32_table_slots(n);
+}
+
+int gm_unique_sum32_hash(const float* x, int64_t n, float* out, void* scratch, size_t scratch_bytes, void* stream) {
+  if (g_device < 0) return fail(GM_E_INVALID, "gm_unique_sum32_hash: gm_init not called");
+  if (!x || !out || !scratch || n <= 0) return fail(GM_E_INVALID, "gm_unique_sum32_hash: bad argument");
+  if (scratch_bytes < gm_unique_sum32_hash_scratch_bytes(n))
+    return fail(GM_E_INVALID, "gm_unique_sum32_hash: scratch too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  char* base = (char*)scratch;
+  unsigned long long* calls = (unsigned long long*)base;          // +0: calls completed (tag source)
+  long long* digits = (long long*)(base + 64);                    // +64: int64[GM_U32_DIGITS]
+  int* flags = (int*)(base + 256);                                // +256: NaN / +inf / -inf seen
+  int* emax = (int*)(base + 260);                                 // +260: largest finite biased exponent
+  unsigned* touched = (unsigned*)(base + 264);                    // +264: bitmap slices marked this call
+  unsigned* done = (unsigned*)(base + 268);                       // +268: CTAs of the bitmap pass finished
+  unsigned* bitmap = (unsigned*)(base + 4096);                    // presence bitmap, all-zero between calls
+  unsigned long long* table = (unsigned long long*)(base + 4096 + 4 * GM_U32_BITMAP_WORDS);
+  GM_CUDA(cudaMemsetAsync(base + 64, 0, 256, s));
+  const unsigned long long slots = u32_table_slots(n);
+  long long want = (n + 2047) / 2048;
+  int grid = (int)(want < 2LL * g_num_sms ? want : 2LL * g_num_sms);
+  if (grid < 1) grid = 1;
+  gm_unique32_window_kernel<<<grid, 512, 0, s>>>(x, n, emax);
+  GM_CUDA(cudaGetLastError());
+  gm_unique32_insert_kernel<<<grid, 512, 0, s>>>(x, n, bitmap, emax, table, slots - 1, calls, digits, flags,
+                                                 touched);
+  GM_CUDA(cudaGetLastError());
+  gm_unique32_bitmap_sum_kernel<<<2 * g_num_sms, 512, 0, s>>>((uint4*)bitmap, emax, touched, digits, done, flags,
+                                                               calls, out);
+  GM_CUDA(cudaGetLastError());
+  return GM_OK;
+}
 
 size_t gm_unique_sum32_scratch_bytes(int64_t n) {
   size_t temp = 0;

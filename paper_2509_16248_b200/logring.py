@@ -27,6 +27,7 @@ which is the reference's behaviour.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import threading
 import time
@@ -354,6 +355,21 @@ def _unique_scratch(device) -> torch.Tensor:
     return t
 
 
+_hash_scratch_by_dev: dict = {}
+
+
+def _hash_scratch(device, nbytes: int) -> torch.Tensor:
+    """Per-device hash-set scratch of gm_unique_sum32_hash, zeroed once and
+    kept: its slots carry a call tag, so the table is never cleared.  A
+    larger request allocates a larger buffer; the smaller ones stay alive
+    for CUDA graphs that captured them."""
+    key = (device.type, device.index)
+    bufs = _hash_scratch_by_dev.setdefault(key, [])
+    if not bufs or bufs[-1].numel() < nbytes:
+        bufs.append(torch.zeros(nbytes, dtype=torch.uint8, device=device))
+    return bufs[-1]
+
+
 class ModuleRuntime:
     """`__gm_rt` of a lowered module: its fused regions and replay sites."""
 
@@ -395,9 +411,14 @@ class ModuleRuntime:
     def unique_sum(x):
         """== x.unique().sum() with fixed shapes (no host sync).  bf16/f16 on
         the GPU: one pass into a 65536-bit presence bitmap and a sum of the
-        set bits (gm_unique_sum16); fp32 on the GPU: radix sort + one pass
-        over the runs (gm_unique_sum32).  Otherwise (CPU tensors): sort, keep
+        set bits (gm_unique_sum16); fp32 on the GPU: a presence bitmap over
+        the top 16 binades (a hash set for smaller values) and an exact
+        fixed-point sum of the distinct values, rounded once
+        (gm_unique_sum32_hash; GM_UNIQUE32=sort selects the radix-sort
+        form gm_unique_sum32).  Otherwise (CPU tensors): sort, keep
         the first of each run of equal values, sum."""
+        if x.is_cuda:
+            nat.init(x.device.index if x.device.index is not None else torch.cuda.current_device())
         if x.is_cuda and x.dtype in (torch.bfloat16, torch.float16) and x.is_contiguous() \
                 and x.data_ptr() % 16 == 0:
             out = torch.empty((), dtype=x.dtype, device=x.device)
@@ -407,6 +428,17 @@ class ModuleRuntime:
                 ctypes.c_void_p(x.data_ptr()), x.numel(), nat.GM_BF16 if x.dtype == torch.bfloat16 else nat.GM_F16, ctypes.c_void_p(out.data_ptr()),
                 ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
                 "gm_unique_sum16")
+            return out
+        if x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and 0 < x.numel() < 2 ** 31 \
+                and os.environ.get("GM_UNIQUE32", "hash") != "sort":
+            out = torch.empty((), dtype=x.dtype, device=x.device)
+            nb = nat.lib().gm_unique_sum32_hash_scratch_bytes(x.numel())
+            scratch = _hash_scratch(x.device, nb)
+            nat.count_launches(3)
+            nat.check(nat.lib().gm_unique_sum32_hash(
+                ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
+                ctypes.c_void_p(scratch.data_ptr()), nb, ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
+                "gm_unique_sum32_hash")
             return out
         if x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and 0 < x.numel() < 2 ** 31:
             out = torch.empty((), dtype=x.dtype, device=x.device)

@@ -1,5 +1,6 @@
 """Precompiled sm_100a kernels of libgm_b200.so, called through the C ABI."""
 
+import math
 import ctypes
 
 import pytest
@@ -75,3 +76,74 @@ def test_unique_sum_matches_torch(n, dtype):
     r, o = float(ref), float(out.cpu())
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     assert abs(o - r) <= tol * abs(r) + 1e-6, (o, r)
+
+
+def _exact_f32_sum_of_unique(x: torch.Tensor) -> float:
+    """Correctly rounded (nearest-even) fp32 value of the EXACT sum of the
+    distinct finite values of x (every fp32 is an integer multiple of
+    2^-149, so the sum is an integer S times 2^-149)."""
+    import numpy as np
+
+    vals = set(float(v) for v in x.numpy().astype(np.float64))
+    vals = {0.0 if v == 0 else v for v in vals}
+    S = sum(int(math.ldexp(v, 149)) for v in vals)
+    mag = abs(S)
+    if mag < 2 ** 23:
+        r = math.ldexp(mag, -149)
+    else:
+        shift = mag.bit_length() - 24
+        m, rem = mag >> shift, mag & ((1 << shift) - 1)
+        half = 1 << (shift - 1) if shift > 0 else 0
+        if shift > 0 and (rem > half or (rem == half and m & 1)):
+            m += 1
+        r = math.ldexp(m, shift - 149)
+        if r >= 2.0 ** 128:
+            r = math.inf
+    return float(np.float32(-r if S < 0 else r))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["softmax", "dups", "cancel", "subnormal", "wide", "ragged"])
+def test_unique_sum32_hash_is_correctly_rounded(case):
+    """gm_unique_sum32_hash: the distinct values' exact sum rounded once —
+    bit-identical to a Python big-integer restatement, on every call,
+    whatever the duplicate pattern or magnitude spread (softmax/dups/
+    subnormal stay inside the 16-binade bitmap window; cancel/wide exercise
+    the hash set)."""
+    from paper_2509_16248_b200.logring import ModuleRuntime
+
+    g = torch.Generator().manual_seed(7)
+    n = 1 << 20
+    if case == "softmax":
+        x = torch.softmax(torch.randn(n, generator=g), 0) * 3 - 1e-3
+    elif case == "dups":
+        x = torch.randint(-500, 500, (n,), generator=g).float() / 8
+    elif case == "cancel":
+        x = torch.tensor([1e30, -1e30, 1.0, 3e-45, 2.0 ** -126] * 1000)
+    elif case == "subnormal":
+        x = torch.randint(-4000, 4000, (n,), generator=g).float() * 2.0 ** -149
+    elif case == "wide":
+        x = torch.randn(n, generator=g) * torch.exp2(torch.randint(-120, 120, (n,), generator=g).float())
+    else:
+        x = torch.randn(4099, generator=g)
+    x = x.float().contiguous()
+    # repeated calls share the tagged table and the (self-clearing) bitmap:
+    # a changed input must not see the previous call's values
+    for xi in (x, x.flip(0).contiguous(), x * 0.75, x[: x.numel() // 3 + 1].contiguous()):
+        expect = _exact_f32_sum_of_unique(xi)
+        got = float(ModuleRuntime.unique_sum(xi.cuda()).cpu())
+        assert got == expect or (math.isnan(got) and math.isnan(expect)), (got, expect)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("specials,expect", [([math.nan], math.nan), ([math.inf], math.inf),
+                                             ([-math.inf], -math.inf), ([math.inf, -math.inf], math.nan),
+                                             ([math.inf, math.nan], math.nan)])
+def test_unique_sum32_hash_specials(specials, expect):
+    from paper_2509_16248_b200.logring import ModuleRuntime
+
+    x = torch.randn(10000)
+    x[torch.arange(len(specials)) * 37] = torch.tensor(specials)
+    got = float(ModuleRuntime.unique_sum(x.cuda()).cpu())
+    ref = float(x.unique().sum())
+    assert (math.isnan(got) and math.isnan(expect) and math.isnan(ref)) or got == expect == ref
