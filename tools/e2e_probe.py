@@ -95,3 +95,29 @@ t = timed(lambda: [dst[k % S][0].copy_(x_host[0], non_blocking=True) for k in ra
 print(f"H2D alone: {1e6 * t / steps:.1f} us/step ({x_host[0].numel() * 2 * steps / t / 1e9:.1f} GB/s)")
 t = timed(lambda: [outs[k].copy_(src[k % S], non_blocking=True) for k in range(steps)])
 print(f"D2H alone: {1e6 * t / steps:.1f} us/step")
+
+
+# per-slot streams: step k runs H2D -> forward -> D2H on stream k % S, so
+# stream order alone guards slot reuse (no cross-stream events)
+def per_slot(n_slots: int, forward: bool):
+    streams = [torch.cuda.Stream(dev) for _ in range(n_slots)]
+    entries = [ex.prepare(*[b.to(dev) for b in batches[0]], slot=s) for s in range(n_slots)]
+    for k in range(steps):
+        s = k % n_slots
+        e = entries[s]
+        with torch.cuda.stream(streams[s]):
+            for st, a in zip(e.static, batches[k]):
+                if torch.is_tensor(st):
+                    st.copy_(a, non_blocking=True)
+            o = e.run() if forward else e.outputs
+            outs[k].copy_(o, non_blocking=True)
+    for st in streams:
+        st.synchronize()
+
+
+for n_slots in (3, 4, 3, 4):
+    for fwd in (True, False):
+        per_slot(n_slots, fwd)
+        t = timed(lambda: per_slot(n_slots, fwd))
+        print(f"per-slot streams x{n_slots}, forward={fwd}: {1e6 * t / steps:.1f} us/step")
+        ex.flush()
