@@ -121,3 +121,67 @@ for n_slots in (3, 4, 3, 4):
         t = timed(lambda: per_slot(n_slots, fwd))
         print(f"per-slot streams x{n_slots}, forward={fwd}: {1e6 * t / steps:.1f} us/step")
         ex.flush()
+
+
+# do kernels slow the copies at all?  copy-only pipeline with an independent
+# stream kept busy by spin kernels (no memory traffic) / by the forward graph
+def copy_with_background(kind: str):
+    bg = torch.cuda.Stream(dev)
+    with torch.cuda.stream(bg):
+        for _ in range(steps // 2):
+            if kind == "spin":
+                torch.cuda._sleep(200000)
+            else:
+                ex.entries[next(iter(ex.entries))].graph.replay()
+    return _copy_only_pipeline(x_host, outs, dev, steps)
+
+
+for kind in ("spin", "forward"):
+    torch.cuda.synchronize()
+    t = copy_with_background(kind)
+    torch.cuda.synchronize()
+    print(f"copy-only with a busy background stream ({kind}): {1e6 * t / steps:.1f} us/step")
+
+
+# software-pipelined issue order: H2D of step k+L is issued before the D2H of
+# step k, so a D2H waiting on its forward never sits ahead of later H2Ds in a
+# copy queue
+def lookahead(L: int, n_slots: int = 3):
+    entries = [ex.prepare(*[b.to(dev) for b in batches[0]], slot=s) for s in range(n_slots)]
+    comp = torch.cuda.current_stream(dev)
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    free = [torch.cuda.Event() for _ in range(n_slots)]
+    loaded = [torch.cuda.Event() for _ in range(n_slots)]
+    done = [torch.cuda.Event() for _ in range(n_slots)]
+
+    def load(j):
+        s = j % n_slots
+        with torch.cuda.stream(h2d):
+            if j >= n_slots:
+                h2d.wait_event(free[s])
+            for st, a in zip(entries[s].static, batches[j]):
+                if torch.is_tensor(st):
+                    st.copy_(a, non_blocking=True)
+            loaded[s].record(h2d)
+
+    for j in range(min(L, steps)):
+        load(j)
+    for k in range(steps):
+        if k + L < steps:
+            load(k + L)
+        s = k % n_slots
+        comp.wait_event(loaded[s])
+        o = entries[s].run()
+        done[s].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done[s])
+            outs[k].copy_(o, non_blocking=True)
+            free[s].record(d2h)
+    d2h.synchronize()
+
+
+for L, S in ((1, 3), (2, 3), (1, 4), (2, 4), (3, 4), (1, 3), (2, 4)):
+    lookahead(L, S)
+    t = timed(lambda: lookahead(L, S))
+    print(f"lookahead L={L} slots={S}: {1e6 * t / steps:.1f} us/step")
+    ex.flush()
