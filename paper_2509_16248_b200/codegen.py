@@ -1478,6 +1478,9 @@ class Plan:
             if r.op in ("amax", "amin") and pref is not None and pref.get(x.uid) == "P":
                 # bf16 max/min on the packed words: 3 max.NaN.bf16x2, then 2 lanes
                 w(f"{ind}acc{k} = gm::acc_minmax_p<{1 if r.op == 'amax' else 0}>(acc{k}, p{x.uid}_{u});")
+            elif r.op in ("sum", "mean", "norm") and pref is not None and pref.get(x.uid) == "P" \
+                    and x.dtype == torch.bfloat16 and os.environ.get("GM_PACKED_SUM", "1") != "0":
+                w(f"{ind}acc{k} = gm::acc_sum_p<{'true' if r.op == 'norm' else 'false'}>(acc{k}, p{x.uid}_{u}, nv{u});")
             elif r.op in ("argmax", "argmin"):
                 w(f"{ind}acc{k} = gm::argkey8(acc{k}, {src}, e{u}, nv{u}, {'true' if r.op == 'argmin' else 'false'});")
             elif r.op == NZSUM:

@@ -409,6 +409,29 @@ __device__ __forceinline__ void unpack8(const u32 (&p)[4], float (&x)[8]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) unpack_bf2(p[j], x[2 * j], x[2 * j + 1]);
 }
+// fp32 sum / sum of squares straight from packed bf16x2 words: the sm_100
+// mixed-precision add / fma (FHADD.BF16 / FHFMA.BF16 with .H0/.H1 operand
+// selects) — one instruction per element instead of an unpack and an FADD.
+// Summed in element order (a chain; the unpacked path sums a tree of 8).
+__device__ __forceinline__ float fadd_bf(float acc, u32 w, int half) {
+  const u16 h = (u16)(half ? w >> 16 : w & 0xffffu);
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc) : "h"(h));
+  return acc;
+}
+__device__ __forceinline__ float ffma_bf(float acc, u32 w, int half) {
+  const u16 h = (u16)(half ? w >> 16 : w & 0xffffu);
+  asm("fma.rn.f32.bf16 %0, %1, %1, %0;" : "+f"(acc) : "h"(h));
+  return acc;
+}
+template <bool SQ>
+__device__ __forceinline__ float acc_sum_p(float acc, const u32 (&p)[4], int nv) {
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    if (l >= nv) break;
+    acc = SQ ? ffma_bf(acc, p[l >> 1], l & 1) : fadd_bf(acc, p[l >> 1], l & 1);
+  }
+  return acc;
+}
 template <int MAX>
 __device__ __forceinline__ float acc_minmax_p(float acc, const u32 (&p)[4]) {
   const u32 m = MAX ? hmax2(hmax2(p[0], p[1]), hmax2(p[2], p[3])) : hmin2(hmin2(p[0], p[1]), hmin2(p[2], p[3]));
