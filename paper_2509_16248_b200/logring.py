@@ -360,9 +360,12 @@ _hash_scratch_by_dev: dict = {}
 
 def _hash_scratch(device, nbytes: int) -> torch.Tensor:
     """Per-device hash-set scratch of gm_unique_sum32_hash, zeroed once and
-    kept: its slots carry a call tag, so the table is never cleared.  A
-    larger request allocates a larger buffer; the smaller ones stay alive
-    for CUDA graphs that captured them."""
+    kept: the bitmap pass clears what it read and the hash slots carry a
+    call tag, so nothing is cleared per call.  A larger request allocates a
+    larger buffer; the smaller ones stay alive for CUDA graphs that captured
+    them.  Per device, not per stream (the warm-up that allocates it and the
+    capture that reuses it run on different streams): the calls of one
+    device must be stream-ordered, as the executor's forwards are."""
     key = (device.type, device.index)
     bufs = _hash_scratch_by_dev.setdefault(key, [])
     if not bufs or bufs[-1].numel() < nbytes:
