@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -413,7 +414,8 @@ __global__ void __launch_bounds__(512) gm_unique32_window_kernel(const float* __
 
 __global__ void __launch_bounds__(512) gm_unique32_insert_kernel(const float* __restrict__ x, long long n,
                                                                  unsigned* __restrict__ bitmap,
-                                                                 const int* __restrict__ emax,
+                                                                 const int* __restrict__ window_top, int head,
+                                                                 int* __restrict__ emax_seen,
                                                                  unsigned long long* __restrict__ table,
                                                                  unsigned long long mask,
                                                                  const unsigned long long* __restrict__ calls,
@@ -422,11 +424,12 @@ __global__ void __launch_bounds__(512) gm_unique32_insert_kernel(const float* __
                                                                  unsigned* __restrict__ touched) {
   __shared__ long long swarp[16][GM_U32_DIGITS];
   const unsigned tag = (unsigned)(*calls % 0xffffffffull) + 1u;
-  const int lo_e = max(*emax - (GM_U32_WIN - 1), 0);
+  const int top_e = min(*window_top + head, 254), lo_e = max(top_e - (GM_U32_WIN - 1), 0);
   long long acc[GM_U32_DIGITS];
 #pragma unroll
   for (int d = 0; d < GM_U32_DIGITS; ++d) acc[d] = 0;
   int fl = 0;
+  unsigned seen = 0;                                     // largest finite exponent met
   unsigned tm = 0;                                       // bitmap slices (sign x binade) this thread marked
   // bitmap values: returns the bit index (the caller marks it); otherwise
   // handles the value (flags, hash set) and returns NONE
@@ -438,7 +441,8 @@ __global__ void __launch_bounds__(512) gm_unique32_insert_kernel(const float* __
       return NONE;
     }
     if ((bits & 0x7fffffffu) == 0) return NONE;          // +-0 adds nothing
-    if ((int)e >= lo_e) {
+    seen = max(seen, e);
+    if ((int)e >= lo_e && (int)e <= top_e) {
       const unsigned slice = (bits >> 31) * GM_U32_WIN + (e - lo_e);
       tm |= 1u << slice;
       return ((unsigned long long)slice << 23) | (bits & 0x7fffffu);
@@ -494,6 +498,8 @@ __global__ void __launch_bounds__(512) gm_unique32_insert_kernel(const float* __
   if (fl) atomicOr(flags, fl);
   tm = __reduce_or_sync(0xffffffffu, tm);
   if ((threadIdx.x & 31) == 0 && tm) atomicOr(touched, tm);
+  seen = __reduce_max_sync(0xffffffffu, seen);
+  if ((threadIdx.x & 31) == 0 && seen) atomicMax(emax_seen, (int)seen);
   gm_u32_flush(acc, swarp, digits);
 }
 
@@ -502,7 +508,8 @@ __device__ void gm_u32_finish(const long long* digits, const int* flags, unsigne
 // sum the mantissas of the set bits of the presence bitmap, clearing it;
 // the last CTA to finish rounds the call's total into *out
 __global__ void __launch_bounds__(512) gm_unique32_bitmap_sum_kernel(uint4* __restrict__ bitmap,
-                                                                     const int* __restrict__ emax,
+                                                                     int* __restrict__ window_top, int head,
+                                                                     const int* __restrict__ emax_seen,
                                                                      const unsigned* __restrict__ touched,
                                                                      long long* __restrict__ digits,
                                                                      unsigned* __restrict__ done,
@@ -510,7 +517,7 @@ __global__ void __launch_bounds__(512) gm_unique32_bitmap_sum_kernel(uint4* __re
                                                                      unsigned long long* __restrict__ calls,
                                                                      float* __restrict__ out) {
   __shared__ long long swarp[16][GM_U32_DIGITS];
-  const int lo_e = max(*emax - (GM_U32_WIN - 1), 0);
+  const int top_e = min(__ldcg(window_top) + head, 254), lo_e = max(top_e - (GM_U32_WIN - 1), 0);
   long long acc[GM_U32_DIGITS];
 #pragma unroll
   for (int d = 0; d < GM_U32_DIGITS; ++d) acc[d] = 0;
@@ -569,6 +576,9 @@ __global__ void __launch_bounds__(512) gm_unique32_bitmap_sum_kernel(uint4* __re
     if (atomicAdd(done, 1u) == gridDim.x - 1) {
       __threadfence();
       gm_u32_finish(digits, flags, calls, out);
+      // predicted mode: the next call's window sits under this call's
+      // largest exponent (every CTA read the old value before arriving)
+      if (head) *window_top = __ldcg(emax_seen);
     }
   }
 }
@@ -1011,6 +1021,7 @@ int gm_unique_sum32_hash(const float* x, int64_t n, float* out, void* scratch, s
   long long* digits = (long long*)(base + 64);                    // +64: int64[GM_U32_DIGITS]
   int* flags = (int*)(base + 256);                                // +256: NaN / +inf / -inf seen
   int* emax = (int*)(base + 260);                                 // +260: largest finite biased exponent
+  int* pred = (int*)(base + 48);                                  // +48: previous call's largest exponent (kept)
   unsigned* touched = (unsigned*)(base + 264);                    // +264: bitmap slices marked this call
   unsigned* done = (unsigned*)(base + 268);                       // +268: CTAs of the bitmap pass finished
   unsigned* bitmap = (unsigned*)(base + 4096);                    // presence bitmap, all-zero between calls
@@ -1020,13 +1031,24 @@ int gm_unique_sum32_hash(const float* x, int64_t n, float* out, void* scratch, s
   long long want = (n + 2047) / 2048;
   int grid = (int)(want < 2LL * g_num_sms ? want : 2LL * g_num_sms);
   if (grid < 1) grid = 1;
-  gm_unique32_window_kernel<<<grid, 512, 0, s>>>(x, n, emax);
-  GM_CUDA(cudaGetLastError());
-  gm_unique32_insert_kernel<<<grid, 512, 0, s>>>(x, n, bitmap, emax, table, slots - 1, calls, digits, flags,
+  // bitmap window: by default the 16 binades from 2 above the PREVIOUS
+  // call's largest exponent down (values outside it go to the hash set, so
+  // the window only decides speed, never the result); GM_U32_WINDOW_PASS=1
+  // measures this call's largest exponent first (one more read of x)
+  static const bool window_pass = getenv("GM_U32_WINDOW_PASS") && atoi(getenv("GM_U32_WINDOW_PASS"));
+  int* top = pred;
+  int head = 2;
+  if (window_pass) {
+    gm_unique32_window_kernel<<<grid, 512, 0, s>>>(x, n, emax);
+    GM_CUDA(cudaGetLastError());
+    top = emax;
+    head = 0;
+  }
+  gm_unique32_insert_kernel<<<grid, 512, 0, s>>>(x, n, bitmap, top, head, emax, table, slots - 1, calls, digits, flags,
                                                  touched);
   GM_CUDA(cudaGetLastError());
-  gm_unique32_bitmap_sum_kernel<<<2 * g_num_sms, 512, 0, s>>>((uint4*)bitmap, emax, touched, digits, done, flags,
-                                                               calls, out);
+  gm_unique32_bitmap_sum_kernel<<<2 * g_num_sms, 512, 0, s>>>((uint4*)bitmap, top, head, emax, touched, digits, done,
+                                                               flags, calls, out);
   GM_CUDA(cudaGetLastError());
   return GM_OK;
 }
