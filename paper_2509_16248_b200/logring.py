@@ -415,7 +415,7 @@ class ModuleRuntime:
         """== x.unique().sum() with fixed shapes (no host sync).  bf16/f16 on
         the GPU: one pass into a 65536-bit presence bitmap and a sum of the
         set bits (gm_unique_sum16); fp32 on the GPU: a presence bitmap over
-        the top 16 binades (a hash set for smaller values) and an exact
+        a 16-binade window (a hash set for the other values) and an exact
         fixed-point sum of the distinct values, rounded once
         (gm_unique_sum32_hash; GM_UNIQUE32=sort selects the radix-sort
         form gm_unique_sum32).  Otherwise (CPU tensors): sort, keep
