@@ -252,17 +252,10 @@ __device__ __forceinline__ void u16_mark(unsigned* bits, unsigned h) {
   if (!(*(volatile unsigned*)p & m)) atomicOr(p, m);
 }
 
-// One pass over x into the presence bitmap; the last CTA to finish sums the
-// values of the set bits (fp64, a fixed thread/word assignment and a fixed
-// tree: deterministic) and rounds once into *out.
 __global__ void __launch_bounds__(512) gm_unique16_mark_kernel(const uint4* __restrict__ x, long long nvec,
                                                                const unsigned short* __restrict__ tail, int ntail,
-                                                               unsigned* __restrict__ gbits,
-                                                               unsigned* __restrict__ done, int dtype,
-                                                               void* __restrict__ out) {
+                                                               unsigned* __restrict__ gbits) {
   __shared__ unsigned bits[2048];
-  __shared__ double part[16];
-  __shared__ int s_last;
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = 0;
   __syncthreads();
   const long long T = (long long)gridDim.x * blockDim.x;
@@ -280,20 +273,17 @@ __global__ void __launch_bounds__(512) gm_unique16_mark_kernel(const uint4* __re
   __syncthreads();
   for (int i = threadIdx.x; i < 2048; i += blockDim.x)
     if (bits[i]) atomicOr(gbits + i, bits[i]);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+}
+
+__global__ void __launch_bounds__(1024) gm_unique16_sum_kernel(const unsigned* __restrict__ gbits, int dtype,
+                                                               void* out) {
+  __shared__ double part[32];
   double acc = 0.0;
   for (int wi = threadIdx.x; wi < 2048; wi += blockDim.x) {
-    unsigned bm = __ldcg(gbits + wi);
-    while (bm) {
-      const int k = __ffs(bm) - 1;
-      bm &= bm - 1;
+    unsigned b = gbits[wi];
+    while (b) {
+      const int k = __ffs(b) - 1;
+      b &= b - 1;
       const unsigned short h = (unsigned short)(wi * 32 + k);
       acc += (double)(dtype == GM_BF16 ? gm::bf2f(h) : gm::h2f(h));
     }
@@ -302,7 +292,7 @@ __global__ void __launch_bounds__(512) gm_unique16_mark_kernel(const uint4* __re
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x < 32) {
-    double t = threadIdx.x < (int)(blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    double t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
     for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     if (threadIdx.x == 0) {
       const float f = (float)t;
@@ -350,8 +340,8 @@ __global__ void __launch_bounds__(1024) gm_sum_partials_kernel(const double* __r
 }
 
 // fp32, sort-free distinct sum.  Deduplication: values whose binade lies in
-// a window of GM_U32_WIN binades (placed from the previous call's largest
-// finite exponent) set one bit of a presence bitmap (sign x binade x 2^23 mantissas; red.or, so a
+// a window of GM_U32_WIN binades below the largest finite exponent set one
+// bit of a presence bitmap (sign x binade x 2^23 mantissas; red.or, so a
 // duplicate is free); the rest go to a hash set of the value bits (open
 // addressing, 64-bit slots = call tag << 32 | bits, so a slot written by an
 // earlier call reads as empty and the table is never cleared).  Summation is
@@ -985,7 +975,7 @@ int gm_logring_gather(gm_logring r, const void* src, int dtype, int ndim, const 
   return GM_OK;
 }
 
-size_t gm_unique_sum16_scratch_bytes(void) { return 2048 * sizeof(unsigned) + 64; }  // bitmap + CTA counter
+size_t gm_unique_sum16_scratch_bytes(void) { return 2048 * sizeof(unsigned); }
 
 int gm_unique_sum16(const void* x, int64_t n, int dtype, void* out, void* scratch, void* stream) {
   if (g_device < 0) return fail(GM_E_INVALID, "gm_unique_sum16: gm_init not called");
@@ -1000,7 +990,9 @@ int gm_unique_sum16(const void* x, int64_t n, int dtype, void* out, void* scratc
   int grid = (int)(want < 2LL * g_num_sms ? want : 2LL * g_num_sms);
   if (grid < 1) grid = 1;
   gm_unique16_mark_kernel<<<grid, 512, 0, s>>>((const uint4*)x, nvec, (const unsigned short*)x + nvec * 8, ntail,
-                                               (unsigned*)scratch, (unsigned*)scratch + 2048, dtype, out);
+                                               (unsigned*)scratch);
+  GM_CUDA(cudaGetLastError());
+  gm_unique16_sum_kernel<<<1, 1024, 0, s>>>((const unsigned*)scratch, dtype, out);
   GM_CUDA(cudaGetLastError());
   return GM_OK;
 }

@@ -426,7 +426,7 @@ class ModuleRuntime:
                 and x.data_ptr() % 16 == 0:
             out = torch.empty((), dtype=x.dtype, device=x.device)
             scratch = _unique_scratch(x.device)
-            nat.count_launches(1)
+            nat.count_launches(2)
             nat.check(nat.lib().gm_unique_sum16(
                 ctypes.c_void_p(x.data_ptr()), x.numel(), nat.GM_BF16 if x.dtype == torch.bfloat16 else nat.GM_F16, ctypes.c_void_p(out.data_ptr()),
                 ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
@@ -437,7 +437,7 @@ class ModuleRuntime:
             out = torch.empty((), dtype=x.dtype, device=x.device)
             nb = nat.lib().gm_unique_sum32_hash_scratch_bytes(x.numel())
             scratch = _hash_scratch(x.device, nb)
-            nat.count_launches(2)
+            nat.count_launches(3)
             nat.check(nat.lib().gm_unique_sum32_hash(
                 ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(out.data_ptr()),
                 ctypes.c_void_p(scratch.data_ptr()), nb, ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
