@@ -340,8 +340,8 @@ __global__ void __launch_bounds__(1024) gm_sum_partials_kernel(const double* __r
 }
 
 // fp32, sort-free distinct sum.  Deduplication: values whose binade lies in
-// a window of GM_U32_WIN binades below the largest finite exponent set one
-// bit of a presence bitmap (sign x binade x 2^23 mantissas; red.or, so a
+// a window of GM_U32_WIN binades (placed from the previous call's largest
+// finite exponent) set one bit of a presence bitmap (sign x binade x 2^23 mantissas; red.or, so a
 // duplicate is free); the rest go to a hash set of the value bits (open
 // addressing, 64-bit slots = call tag << 32 | bits, so a slot written by an
 // earlier call reads as empty and the table is never cleared).  Summation is
@@ -393,6 +393,7 @@ __device__ __forceinline__ void gm_u32_flush(long long* acc, long long (*swarp)[
 }
 
 // largest biased exponent among finite values -> *emax (atomicMax; memset 0)
+// — only with GM_U32_WINDOW_PASS=1 (the window of THIS call)
 __global__ void __launch_bounds__(512) gm_unique32_window_kernel(const float* __restrict__ x, long long n,
                                                                  int* __restrict__ emax) {
   unsigned m = 0;
