@@ -11,5 +11,6 @@ for w in longformer_like phi4_like qwen_audio_like biogpt_like blenderbot_like f
       python bench.py --workload $w --dtype $d --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_${w}_${d}.log 2>&1
     python tools/ncu_summary.py gpurun_out/prof_${w}_${d}.ncu-rep profiles/r01_${w}_${d}_ncu_regions.json \
       > /dev/null 2>&1 && cp profiles/r01_${w}_${d}_ncu_regions.json gpurun_out/
+    rm -f gpurun_out/prof_${w}_${d}.ncu-rep  # gpurun copies back <= 64 MiB
   done
 done
