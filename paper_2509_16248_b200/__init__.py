@@ -24,12 +24,15 @@ from .lowering import Lowered, load, lower
 __all__ = ["B200Executor", "Lowered", "count_syncs", "load", "lower", "compile_program"]
 
 
-def compile_program(text: str, callable_name: str, device=None, dtype=None, use_graphs: bool = True):
+def compile_program(text: str, callable_name: str, device=None, dtype=None, use_graphs: bool = True,
+                    allow_eager: bool = False):
     """Lower `text` (a GraphMend-transformed program), move its callable to
-    the GPU and wrap it in a B200Executor.  Returns (executor, module, lowered)."""
+    the GPU and wrap it in a B200Executor.  Returns (executor, module, lowered).
+    A region the fused kernels cannot run raises region.RegionUnsupported
+    unless `allow_eager` (then it runs its statements with PyTorch)."""
     import torch
 
-    module, lowered = load(text)
+    module, lowered = load(text, allow_eager=allow_eager)
     fn = getattr(module, callable_name)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if isinstance(fn, torch.nn.Module):

@@ -100,6 +100,9 @@ _SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int,
       ctypes.c_void_p, ctypes.c_int]),
     ("gm_region_release", ctypes.c_int, [ctypes.c_void_p]),
+    ("gm_stream_capture_id", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]),
+    ("gm_status_page", ctypes.c_int,
+     [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
     ("gm_unique_sum16_scratch_bytes", ctypes.c_size_t, []),
     ("gm_unique_sum32_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
     ("gm_unique_sum32_hash_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
@@ -193,6 +196,28 @@ def compile_cubin(src: str, cc: tuple[int, int] = (10, 0)) -> bytes:
         return ctypes.string_at(out, n.value)
     finally:
         lib().gm_free(out)
+
+
+def capture_id(stream: int) -> int:
+    """CUDA-graph capture id of `stream` (0 when not capturing)."""
+    v = ctypes.c_uint64(0)
+    check(lib().gm_stream_capture_id(ctypes.c_void_p(stream), ctypes.byref(v)), "gm_stream_capture_id")
+    return int(v.value)
+
+
+STATUS_WORDS = 1 << 16
+_status = None
+
+
+def status_page():
+    """(host int array, device base address) of the process-wide mapped
+    status page (gm_status_page)."""
+    global _status
+    if _status is None:
+        h, d = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib().gm_status_page(STATUS_WORDS, ctypes.byref(h), ctypes.byref(d)), "gm_status_page")
+        _status = ((ctypes.c_int * STATUS_WORDS).from_address(h.value), d.value)
+    return _status
 
 
 class CompiledRegion:

@@ -848,6 +848,40 @@ int gm_region_release(gm_region r) {
 
 size_t gm_region_params_bytes(void) { return sizeof(gm::Params); }
 
+int gm_stream_capture_id(void* stream, uint64_t* id) {
+  if (!id) return fail(GM_E_INVALID, "gm_stream_capture_id: null id");
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long cid = 0;
+  GM_CUDA(cudaStreamGetCaptureInfo((cudaStream_t)stream, &st, &cid));
+  *id = st == cudaStreamCaptureStatusActive ? (uint64_t)cid : 0ull;
+  return GM_OK;
+}
+
+namespace {
+int* g_status_host = nullptr;
+int* g_status_dev = nullptr;
+int g_status_n = 0;
+}  // namespace
+
+int gm_status_page(int n, int** host, int** dev) {
+  if (n <= 0 || !host || !dev) return fail(GM_E_INVALID, "gm_status_page: bad argument");
+  if (!g_status_host) {
+    void* h = nullptr;
+    GM_CUDA(cudaHostAlloc(&h, (size_t)n * sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(h, 0, (size_t)n * sizeof(int));
+    void* d = nullptr;
+    GM_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    g_status_host = (int*)h;
+    g_status_dev = (int*)d;
+    g_status_n = n;
+  } else if (n > g_status_n) {
+    return fail(GM_E_INVALID, "gm_status_page: already open with %d words (< %d)", g_status_n, n);
+  }
+  *host = g_status_host;
+  *dev = g_status_dev;
+  return GM_OK;
+}
+
 // barrier scratch (counter, epoch, status, results) | partials @ GM_SCRATCH_PARTIALS
 size_t gm_branch_select_scratch_bytes(void) { return GM_SCRATCH_PARTIALS + 8 * 4096; }
 

@@ -28,30 +28,52 @@ import torch
 from . import _native as nat
 from .executor import B200Executor
 from .lowering import load
+from .region import RegionUnsupported
 
 _PRELUDE = "import math\nimport operator\nimport torch\n\n"
 
 
-def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs):
+def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool = False,
+                    static_outputs: bool = False):
     """Dynamo backend: lower the FX graph's source into fused regions and run
-    it as one CUDA graph per input signature (CPU inputs run the lowered
-    statements eagerly, bit-identical to the graph)."""
-    module, lowered = load(_PRELUDE + textwrap.dedent(gm.code))
+    it as one CUDA graph per input signature.
+
+    torch.compile semantics are kept: every call returns fresh tensors (the
+    graph's static outputs are cloned unless `static_outputs=True`, the
+    make_graphed_callables contract), and a call that needs autograd (grad
+    mode on and an input requiring grad) runs the FX graph itself, so
+    gradients flow — the fused kernels are inference-only.  CPU inputs raise
+    unless `allow_eager` (then the lowered statements run eagerly with
+    PyTorch, bit-identical to the graph): there is no silent CPU path.
+    `functools.partial(gm_b200_backend, allow_eager=True)` opts in."""
+    module, lowered = load(_PRELUDE + textwrap.dedent(gm.code), allow_eager=allow_eager)
     forward = functools.partial(module.forward, gm)
     on_cuda = any(torch.is_tensor(a) and a.is_cuda for a in example_inputs)
     if not on_cuda:
+        if not allow_eager:
+            raise RegionUnsupported("gm_b200 backend: no CUDA input (the B200 path has no CPU fallback; "
+                                    "use functools.partial(gm_b200_backend, allow_eager=True) to run the lowered "
+                                    "statements eagerly)")
         return forward
     dev = next(a.device for a in example_inputs if torch.is_tensor(a) and a.is_cuda)
     executor = B200Executor(forward, dev)
+    stats = {"graph_calls": 0, "autograd_calls": 0}
 
     def run(*args):
+        if torch.is_grad_enabled() and any(torch.is_tensor(a) and a.requires_grad for a in args):
+            stats["autograd_calls"] += 1
+            return gm(*args)
+        stats["graph_calls"] += 1
         with torch.no_grad():
             out = executor(*args)
+        if not static_outputs:
+            out = torch.utils._pytree.tree_map(lambda t: t.clone() if torch.is_tensor(t) else t, out)
         executor.flush()
         return out
 
     run.executor = executor
     run.lowered = lowered
+    run.stats = stats
     return run
 
 

@@ -33,8 +33,10 @@ import warnings
 from dataclasses import dataclass
 
 import torch
+from torch.utils._pytree import tree_flatten, tree_unflatten
 
 from . import logring
+from .region import check_status
 
 _SYNC_MSG = "synchroniz"
 
@@ -219,6 +221,7 @@ class B200Executor:
         return e
 
     def __call__(self, *args):
+        check_status()  # a grid-barrier timeout of an earlier launch raises here (no sync)
         e = self.prepare(*args)
         e.load(args)
         return e.run()
@@ -229,8 +232,9 @@ class B200Executor:
         compute stream and its output copied D2H into pinned host memory on a
         second copy stream, rotating over `slots` captured graphs (each with
         its own static buffers) so the copies of batches k+1.. / k-1.. overlap
-        the forward of batch k.  Returns the list of host outputs (pinned
-        tensors), in order."""
+        the forward of batch k.  Returns the list of host outputs in order,
+        each with the forward's output structure (tensor, tuple, list or
+        dict) and pinned tensors at its leaves; `out` may supply them."""
         batches = list(batches)
         if not batches:
             return []
@@ -261,17 +265,24 @@ class B200Executor:
             done[s].record(comp)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(done[s])
+                leaves, spec = tree_flatten(o)
                 if outs_host[k] is None:
-                    outs_host[k] = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
-                outs_host[k].copy_(o, non_blocking=True)
+                    outs_host[k] = tree_unflatten(
+                        [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) if torch.is_tensor(t) else t
+                         for t in leaves], spec)
+                for h, t in zip(tree_flatten(outs_host[k])[0], leaves):
+                    if torch.is_tensor(t):
+                        h.copy_(t, non_blocking=True)
                 free[s].record(d2h)
             results.append(outs_host[k])
         d2h.synchronize()
         return results
 
     def flush(self) -> None:
-        """Deliver every deferred print/log of the calls made so far."""
+        """Deliver every deferred print/log of the calls made so far, then
+        raise if any region launch so far hit the grid-barrier timeout."""
         logring.ring_for(self.device).flush()
+        check_status()
 
     def info(self) -> list[EntryInfo]:
         return [e.info for e in self.entries.values()]

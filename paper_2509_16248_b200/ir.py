@@ -50,6 +50,11 @@ INT_REDUCE = {"count_nonzero", "nzsum"}
 NZSUM = "nzsum"
 GM_RT_NAME = "__gm_rt__"
 BOOL_AND, BOOL_OR, BOOL_NOT = "bool_and", "bool_or", "bool_not"
+# `v is None` / `v is not None`: the reference copies such predicates verbatim
+# (transform.py:386-388; parameters are taint seeds, analysis.py:340-344), so
+# the rewrite hands torch.where a Python bool.  They are resolved on the host
+# when a region is specialised (fold_host_predicates): the original `if`.
+IS_NONE, IS_NOT_NONE = "is_none", "is_not_none"
 
 # torch.<name>(...) / torch.nn.functional.<name>(...) spellings
 _TORCH_FUNCS = {
@@ -191,6 +196,15 @@ class Builder:
         if isinstance(e, ast.Compare):
             if len(e.ops) != 1:
                 raise Unsupported("chained comparison")
+            if isinstance(e.ops[0], (ast.Is, ast.IsNot)):
+                left, right = e.left, e.comparators[0]
+                if isinstance(right, ast.Constant) and right.value is None:
+                    operand = left
+                elif isinstance(left, ast.Constant) and left.value is None:
+                    operand = right
+                else:
+                    raise Unsupported("identity comparison with a value other than None")
+                return self.op(IS_NONE if isinstance(e.ops[0], ast.Is) else IS_NOT_NONE, self.expr(operand))
             name = _CMPOP.get(type(e.ops[0]))
             if name is None:
                 raise Unsupported(f"comparison {type(e.ops[0]).__name__}")
@@ -427,6 +441,61 @@ def infer(graph: Graph, args: list, needed: list[Node]) -> None:
             node.shape = ()
         else:
             raise Unsupported(f"value of type {type(v).__name__}")
+
+
+def fold_host_predicates(graph: Graph, outputs: list[Node], args: list) -> tuple[Graph, list[Node]]:
+    """Resolve `is None` / `is not None` of the region's free values for these
+    arguments (the specialisation key includes each argument's type) and
+    keep only the selected arm of a `where` whose condition becomes a host
+    bool — the original `if` semantics (the reference's rewrite would hand
+    torch.where a Python bool and evaluate an arm on None).  and/or/not with
+    a resolved operand fold as Python does.  Graphs without identity tests
+    are returned unchanged."""
+    if not any(n.op in (IS_NONE, IS_NOT_NONE) for n in graph.nodes):
+        return graph, outputs
+    g = Graph()
+    consts: dict = {}
+    memo: dict[int, Node] = {}
+    for fv in graph.frees:
+        nn = g.add(Node("free", value=fv.node.value))
+        g.frees.append(FreeVar(fv.text, nn))
+        memo[id(fv.node)] = nn
+
+    def const(v) -> Node:
+        key = (type(v), v)
+        if key not in consts:
+            consts[key] = g.add(Node("const", value=v))
+        return consts[key]
+
+    def is_const_bool(n: Node) -> bool:
+        return n.op == "const" and isinstance(n.value, bool)
+
+    def fold(n: Node) -> Node:
+        if id(n) in memo:
+            return memo[id(n)]
+        if n.op == "const":
+            r = const(n.value)
+        elif n.op in (IS_NONE, IS_NOT_NONE):
+            a = n.args[0]
+            if a.op != "free":
+                raise Unsupported("identity test of a computed value")
+            none = args[a.value] is None
+            r = const(none if n.op == IS_NONE else not none)
+        elif n.op == "where" and is_const_bool(fold(n.args[0])):
+            r = fold(n.args[1] if fold(n.args[0]).value else n.args[2])
+        elif n.op == BOOL_NOT and is_const_bool(fold(n.args[0])):
+            r = const(not fold(n.args[0]).value)
+        elif n.op in (BOOL_AND, BOOL_OR) and is_const_bool(fold(n.args[0])):
+            v = fold(n.args[0]).value
+            short = (not v) if n.op == BOOL_AND else v
+            r = const(v) if short else fold(n.args[1])
+        else:
+            r = g.add(Node(n.op, tuple(fold(a) for a in n.args), value=n.value))
+        memo[id(n)] = r
+        return r
+
+    outs = [fold(o) for o in outputs]
+    return g, outs
 
 
 def topo(roots: list[Node]) -> list[Node]:

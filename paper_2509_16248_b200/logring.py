@@ -37,6 +37,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _native as nat
+from .region import stream_key, zeroed
 
 EDGEITEMS = 3      # torch._tensor_str.PRINT_OPTS defaults
 THRESHOLD = 1000
@@ -345,12 +346,13 @@ _unique_scratch_by_dev: dict = {}
 
 
 def _unique_scratch(device) -> torch.Tensor:
-    """Per-device bitmap scratch of gm_unique_sum16 (calls on one stream are
-    ordered, so one buffer serves them all)."""
-    key = (device.type, device.index)
+    """Bitmap scratch of gm_unique_sum16, one per (stream, graph capture)
+    (region.stream_key): calls on one stream are ordered, so one buffer
+    serves them all, and concurrent streams or graphs never share one."""
+    key = (device.index,) + stream_key(device)
     t = _unique_scratch_by_dev.get(key)
     if t is None:
-        t = torch.empty(nat.lib().gm_unique_sum16_scratch_bytes(), dtype=torch.uint8, device=device)
+        t = zeroed(nat.lib().gm_unique_sum16_scratch_bytes(), device)
         _unique_scratch_by_dev[key] = t
     return t
 
@@ -363,13 +365,12 @@ def _hash_scratch(device, nbytes: int) -> torch.Tensor:
     kept: the bitmap pass clears what it read and the hash slots carry a
     call tag, so nothing is cleared per call.  A larger request allocates a
     larger buffer; the smaller ones stay alive for CUDA graphs that captured
-    them.  Per device, not per stream (the warm-up that allocates it and the
-    capture that reuses it run on different streams): the calls of one
-    device must be stream-ordered, as the executor's forwards are."""
-    key = (device.type, device.index)
+    them.  One set per (stream, graph capture) (region.stream_key), so
+    concurrent streams or graphs never share a table."""
+    key = (device.index,) + stream_key(device)
     bufs = _hash_scratch_by_dev.setdefault(key, [])
     if not bufs or bufs[-1].numel() < nbytes:
-        bufs.append(torch.zeros(nbytes, dtype=torch.uint8, device=device))
+        bufs.append(zeroed(nbytes, device))
     return bufs[-1]
 
 

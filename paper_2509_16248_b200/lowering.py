@@ -138,9 +138,20 @@ class _FunctionLowerer:
             for n in ast.walk(fn)
             if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Load)
         ]
+        # names a deferred scope may read whenever it runs (a lambda / nested
+        # def / class body defined anywhere in the function, or a name
+        # declared global / nonlocal): never dead, whatever their position
+        self.always_live: set[str] = set()
+        for n in ast.walk(fn):
+            if n is fn:
+                continue
+            if isinstance(n, (ast.Lambda, ast.FunctionDef, ast.AsyncFunctionDef, ast.ClassDef)):
+                self.always_live |= {m.id for m in ast.walk(n) if isinstance(m, ast.Name)}
+            elif isinstance(n, (ast.Global, ast.Nonlocal)):
+                self.always_live |= set(n.names)
 
     def read_after(self, name: str, pos: tuple[int, int]) -> bool:
-        return any(p > pos and n == name for p, n in self.loads)
+        return name in self.always_live or any(p > pos and n == name for p, n in self.loads)
 
     # -- region formation -------------------------------------------------------
     def _build(self, stmts: list[ast.stmt]) -> tuple[Graph, Builder]:
@@ -175,8 +186,11 @@ class _FunctionLowerer:
         unfixable, data/dynamic_shape_ops.cfg; the counts stay the reference's):
           nonzero(M).sum()          -> __gm_rt__.nonzero_sum(M)   (fused coordinate sum)
           masked_select(X, M).sum() -> torch.where(M, X, 0).sum() (fused)
-          X.unique().sum()          -> __gm_rt__.unique_sum(X)    (sort + adjacent-distinct mask)
-        """
+          X.unique().sum()          -> __gm_rt__.unique_sum(X)    (distinct-value sum kernels)
+        The replacement is evaluated AT THE DEFINITION SITE (`V = op(X)` becomes
+        `__gm_s_k = <fixed-shape sum>`) and the use `V.sum()` reads
+        `__gm_s_k`, so names of X rebound or mutated between the definition
+        and the use cannot change the result."""
         torch_name = sorted(self.owner.torch_names)[0]
         out = list(stmts)
         i = 0
@@ -203,6 +217,7 @@ class _FunctionLowerer:
                                  [operands[1], operands[0], ast.Constant(0)], [])
                 repl = ast.Call(ast.Attribute(where, "sum", ast.Load()), [], [])
             target = uses[0]
+            sname = f"__gm_s_{self.owner.next_tmp()}"
 
             class _Sub(ast.NodeTransformer):
                 done = 0
@@ -212,7 +227,7 @@ class _FunctionLowerer:
                     if (isinstance(f, ast.Attribute) and f.attr == "sum" and f.value is target
                             and not node.args and not node.keywords):
                         _Sub.done += 1
-                        return ast.copy_location(copy.deepcopy(repl), node)
+                        return ast.copy_location(ast.Name(sname, ast.Load()), node)
                     return self.generic_visit(node)
 
             new_tail = [_Sub().visit(s) for s in out[i + 1:]]
@@ -220,8 +235,12 @@ class _FunctionLowerer:
                 i += 1
                 continue
             self.owner.dyn_lowered.append((var, op))
-            out = out[:i] + new_tail
+            defn = ast.copy_location(ast.Assign(targets=[ast.Name(sname, ast.Store())], value=repl), out[i])
+            defn.end_lineno, defn.end_col_offset = out[i].end_lineno, out[i].end_col_offset
+            self.loads.append(((target.lineno, target.col_offset), sname))
+            out = out[:i] + [defn] + new_tail
             ast.fix_missing_locations(self.fn)
+            i += 1
         return out
 
     def _fusable(self, e: ast.expr) -> bool:
@@ -493,12 +512,18 @@ def lower(text: str) -> tuple[Lowered, "_Lowerer"]:
     return lw.run(), lw
 
 
-def load(text: str, name: str | None = None, runtime=None) -> tuple[types.ModuleType, Lowered]:
+def load(text: str, name: str | None = None, runtime=None, allow_eager: bool = False
+         ) -> tuple[types.ModuleType, Lowered]:
     """Lower `text` and execute it as a fresh module whose `__gm_rt` is the
-    module runtime (logring.ModuleRuntime)."""
+    module runtime (logring.ModuleRuntime).  With `allow_eager`, a region
+    whose arguments leave the fused subset (e.g. CPU tensors) runs its
+    original statements with PyTorch; by default it raises
+    region.RegionUnsupported."""
     from .logring import ModuleRuntime
 
     lowered, lw = lower(text)
+    for r in lowered.regions:
+        r.allow_eager = allow_eager
     mod_name = name or f"_gm_b200_prog_{next(_module_ids)}"
     filename = f"<gm-b200:{mod_name}>"
     module = types.ModuleType(mod_name)

@@ -7,12 +7,14 @@ current CUDA stream and returns the live-out tensors.  Launches are
 stream-ordered and graph-capturable; no call synchronises with the host.
 
 When the arguments leave the fusable subset (integer tensors, CPU tensors,
-shapes that do not broadcast to one iteration space, ...), the region runs
-its original statements with PyTorch instead — the exact code the reference
-transform emitted (`fallback`), on the device the tensors live on.  Every
-such decision is recorded in `Region.stats` so tests can assert that the
-fused kernel is what ran.  Missing native code is never a fallback: a
-NativeError propagates.
+shapes that do not broadcast to one iteration space, ...), the call raises
+`RegionUnsupported` — there is no silent fallback.  A caller that opts in
+(`allow_eager=True`: `lowering.load(..., allow_eager=True)`, the CPU
+equivalence tests) gets the region's original statements run with PyTorch
+instead — the exact code the reference transform emitted (`fallback`), on
+the device the tensors live on; every such decision is recorded in
+`Region.stats`.  Missing native code is never a fallback: a NativeError
+propagates.
 """
 
 from __future__ import annotations
@@ -27,11 +29,12 @@ import torch
 
 from . import _native as nat
 from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
-from .ir import Graph, Node, Unsupported
+from .ir import Graph, Node, Unsupported, fold_host_predicates
 
 SCRATCH_PARTIALS = 2432  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
 SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [speculative launches, mispredictions]
 SCRATCH_PRED = 288      # GM_SCRATCH_PRED: int predicted decisions
+SCRATCH_SUBCNT = 384    # GM_SCRATCH_SUBCNT: arrival sub-counters
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
 _kernel_lock = threading.Lock()
 
@@ -96,6 +99,77 @@ def arg_key(a) -> tuple:
     return ("o", type(a))
 
 
+class RegionUnsupported(nat.NativeError):
+    """The region's arguments leave the fused subset and the caller did not
+    opt into running its statements with PyTorch (allow_eager)."""
+
+
+_aux_streams: dict = {}
+
+
+def _aux_stream(dev: torch.device):
+    k = dev.index
+    if k not in _aux_streams:
+        _aux_streams[k] = torch.cuda.Stream(dev)
+    return _aux_streams[k]
+
+
+def stream_key(dev: torch.device) -> tuple[int, int]:
+    """(stream, capture id) of the current stream: the owner of a scratch
+    buffer.  Eager launches on one stream are ordered; every CUDA-graph
+    capture gets its own key, so two graphs (or two streams) replaying the
+    same specialisation never share an arrival counter."""
+    s = torch.cuda.current_stream(dev).cuda_stream
+    return s, nat.capture_id(s)
+
+
+def zeroed(nbytes: int, dev: torch.device) -> torch.Tensor:
+    """A zero-filled device buffer.  Under CUDA-graph capture the fill runs on
+    a side stream outside the capture (so it is not replayed); the capture
+    driver synchronises the device before the graph's first replay."""
+    if torch.cuda.is_current_stream_capturing():
+        with torch.cuda.stream(_aux_stream(dev)):
+            return torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    return torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+
+
+# every (spec, scratch, status word) ever handed to a launch: check_status()
+# reads their status words from the mapped page without synchronising
+_status_owners: list = []
+
+
+def _status_slot() -> int:
+    n = len(_status_owners)
+    if n >= nat.STATUS_WORDS:
+        raise nat.NativeError("out of region status words")
+    return n
+
+
+def check_status() -> None:
+    """Raise if any region launch hit the grid-barrier timeout (status = 1:
+    CTAs were not co-resident, so partials may have been stale and the
+    outputs of that launch are wrong).  Non-blocking when all is well (a read
+    of mapped host memory); on an error the device is synchronised, the
+    affected counters and status words are reset, and NativeError names the
+    regions."""
+    if not _status_owners:
+        return
+    page, _ = nat.status_page()
+    bad = [o for o in _status_owners if page[o[2]]]
+    if not bad:
+        return
+    torch.cuda.synchronize()
+    names = []
+    for spec, t, idx in bad:
+        t[:SCRATCH_STATS].zero_()
+        t[SCRATCH_SUBCNT:SCRATCH_PARTIALS].zero_()
+        page[idx] = 0
+        names.append(spec.name)
+    torch.cuda.synchronize()
+    raise nat.NativeError(f"grid-barrier timeout in region(s) {sorted(set(names))}: the CTAs were not co-resident; "
+                          "the outputs of those launches are invalid (counters reset)")
+
+
 @dataclass
 class RegionStats:
     launches: int = 0
@@ -110,7 +184,10 @@ class _Spec:
         dev = next(a.device for a in args if torch.is_tensor(a) and a.device.type == "cuda")
         self.device = dev
         sms, smem_optin = nat.init(dev.index if dev.index is not None else torch.cuda.current_device())
-        plan = Plan(region.graph, region.out_nodes, args, name=region.name, device_info=(sms, smem_optin))
+        graph, outs = fold_host_predicates(region.graph, region.out_nodes, args)
+        if any(o.op == "const" for o in outs):
+            raise Unsupported("a live-out folds to a host constant")
+        plan = Plan(graph, outs, args, name=region.name, device_info=(sms, smem_optin))
         self.plan = plan
         self.kernel = compiled_kernel(plan.source, plan.kernel)
         n = plan.n
@@ -128,20 +205,21 @@ class _Spec:
         self.nred = len(plan.reductions)
         self.nscal = len(plan.scalars)
         # scratch: counter/epoch/status/results (192 B, see gm_region.cuh) |
-        # partials | scalar mirror (+1 KB: the GM_PROFILE timeline at scal_out + 64 u64)
+        # partials | scalar mirror (+1 KB: the GM_PROFILE timeline at scal_out + 64 u64);
+        # one buffer per (stream, graph capture), see stream_key()
         part_bytes = 8 * max(1, self.nred) * grid
-        self.scratch = torch.zeros(SCRATCH_PARTIALS + part_bytes + 8 * 64 + 8 * 64 + 8 * max(1, self.nscal),
-                                   dtype=torch.uint8, device=dev)
-        base = self.scratch.data_ptr()
+        self.part_bytes = part_bytes
+        self.scratch_bytes = SCRATCH_PARTIALS + part_bytes + 8 * 64 + 8 * 64 + 8 * max(1, self.nscal)
+        self.name = region.name
+        self._scratches: dict = {}
+        self.scratch: torch.Tensor | None = None
+        self.status_idx = -1
+        self.bind_scratch()
         P = nat.Params()
         P.n = n
         P.nvec = nvec
         P.vpc = vpc
         P.piece_vecs = 1  # (bulk-copy staging: gm_branch_select_f32 only)
-        P.barrier = base
-        P.status = base + 16
-        P.partials = base + SCRATCH_PARTIALS
-        P.scal_out = base + SCRATCH_PARTIALS + part_bytes
         self.template = P
         self.in_slots = []  # (slot, free_index, mode)
         for ip in plan.inputs:
@@ -176,6 +254,20 @@ class _Spec:
                 k += 1
         self.shape = tuple(plan.shape)
 
+    def bind_scratch(self) -> torch.Tensor:
+        """The scratch buffer of the current (stream, capture) — created
+        zeroed on first use — made the one `scalars()` / `spec_stats()` read."""
+        key = stream_key(self.device)
+        sc = self._scratches.get(key)
+        if sc is None:
+            t = zeroed(self.scratch_bytes, self.device)
+            idx = _status_slot()
+            _status_owners.append((self, t, idx))
+            sc = (t, idx)
+            self._scratches[key] = sc
+        self.scratch, self.status_idx = sc
+        return self.scratch
+
     def run(self, args: list, pdl: bool | None = None):
         """Launch on the current stream.  `pdl` (default: GM_PDL, on) makes it
         a programmatic dependent launch: the CTAs become resident while the
@@ -183,6 +275,11 @@ class _Spec:
         before reading anything."""
         P = nat.Params()
         ctypes.memmove(ctypes.byref(P), ctypes.byref(self.template), ctypes.sizeof(P))
+        base = self.bind_scratch().data_ptr()
+        P.barrier = base
+        P.status = nat.status_page()[1] + 4 * self.status_idx
+        P.partials = base + SCRATCH_PARTIALS
+        P.scal_out = base + SCRATCH_PARTIALS + self.part_bytes
         for slot, fi in self.in_slots:
             P.inp[slot].ptr = args[fi].data_ptr()
         for j, fi in enumerate(self.hs_index):
@@ -255,8 +352,9 @@ class _Spec:
         return int(v[0]), int(v[1])
 
     def status(self) -> int:
-        """Grid-barrier status word (syncs; diagnostics only)."""
-        return int(self.scratch[16:20].view(torch.int32).item())
+        """Grid-barrier status word of the current scratch (a read of mapped
+        host memory: no sync; the launch it reports on may still be running)."""
+        return int(nat.status_page()[0][self.status_idx])
 
     def scalars(self) -> list[float]:
         """Scalar slots mirrored by CTA 0 of the last launch (syncs; tests)."""
@@ -286,6 +384,9 @@ class Region:
         # around the kernel launch; captured into a CUDA graph they time the
         # kernel inside every replay (bench.py's roofline measurement)
         self.probe = None
+        # run the original statements with PyTorch when specialisation fails
+        # (opt-in; the default raises RegionUnsupported)
+        self.allow_eager = False
 
     def __call__(self, *args):
         if self.trace is not None:
@@ -296,6 +397,10 @@ class Region:
             spec = self._specialise(list(args))
             self.specs[key] = spec
         if isinstance(spec, str):
+            if not self.allow_eager:
+                raise RegionUnsupported(f"region {self.name}: {spec} (the fused kernel cannot run these arguments; "
+                                        f"load the program with allow_eager=True to run its statements with "
+                                        f"PyTorch)")
             self.stats.fallbacks += 1
             return self.fallback(*args)
         self.stats.launches += 1

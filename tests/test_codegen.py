@@ -13,7 +13,7 @@ from paper_2509_16248_b200.logring import ModuleRuntime
 
 
 def _plan(programs, name, dtype, shape, idx=0):
-    mod, low = lowering.load(programs[name]["transformed"])
+    mod, low = lowering.load(programs[name]["transformed"], allow_eager=True)
     r = low.regions[idx]
     args = []
     for fv in r.graph.frees:

@@ -2,6 +2,8 @@
 GraphMend-transformed program lowers Dynamo's FX graphs into fused regions
 (paper_2509_16248_b200/dynamo.py)."""
 
+import functools
+
 import pytest
 import torch
 
@@ -29,7 +31,8 @@ def test_backend_on_cpu_equals_eager(programs, name):
     for spec in prog["inputs"]:
         args = make_args(spec["args"], spec["seed"], shapes=shapes)
         ref = fn(*[a.clone() for a in args])
-        out = torch.compile(fn, backend="gm_b200")(*[a.clone() for a in args])
+        out = torch.compile(fn, backend=functools.partial(dynamo.gm_b200_backend, allow_eager=True))(
+            *[a.clone() for a in args])
         assert torch.equal(out, ref)
 
 

@@ -65,7 +65,7 @@ def test_name_mangling_safe():
     src = ("import torch\nclass M(torch.nn.Module):\n    def forward(self, x):\n        __gm_pred_0 = x.sum() > 0\n"
            "        __gm_then_y_0 = x + 1\n        __gm_else_y_0 = x - 1\n"
            "        y = torch.where(__gm_pred_0, __gm_then_y_0, __gm_else_y_0)\n        return y * 2\nm = M()\n")
-    mod, low = lowering.load(src)
+    mod, low = lowering.load(src, allow_eager=True)
     x = torch.randn(5)
     assert torch.equal(mod.m(x), torch.where(x.sum() > 0, x + 1, x - 1) * 2)
 
@@ -85,7 +85,7 @@ def test_lowered_equals_transformed_on_cpu(programs, name):
             shapes = [[4, 1, 768]]
         args = orc.make_args(spec["args"], spec["seed"], shapes=shapes)
         ref, rt = orc.run_reference(p["transformed"], p["callable"], args)
-        mod, low = lowering.load(p["transformed"])
+        mod, low = lowering.load(p["transformed"], allow_eager=True)
         out, t = orc.call_captured(getattr(mod, p["callable"]), args)
         assert t == rt
         assert torch.equal(out, ref) if isinstance(ref, torch.Tensor) else out == ref
@@ -97,7 +97,7 @@ def test_lowered_equals_transformed_on_cpu(programs, name):
 def test_region_codegen_compiles_for_sm100a(programs, name, dtype):
     """Every region of the BASELINE-shaped programs specialises and its
     generated source compiles with NVRTC for sm_100a (no GPU needed)."""
-    mod, low = lowering.load(programs[name]["transformed"])
+    mod, low = lowering.load(programs[name]["transformed"], allow_eager=True)
     for r in low.regions:
         args = []
         for fv in r.graph.frees:
@@ -117,7 +117,7 @@ def test_uniform_select_guards_untaken_arm(programs, monkeypatch):
     sits under the negated predicate and never happens when the then arm is
     selected (the reference evaluates both arms, transform.py:404-412) — in
     the speculative pass and in the exact fallback passes alike."""
-    mod, low = lowering.load(programs["bigbird_like"]["transformed"])
+    mod, low = lowering.load(programs["bigbird_like"]["transformed"], allow_eager=True)
     r = low.regions[0]
     args = [torch.randn(8, 64, 768), 0.125, torch.randn(8, 64, 768)]
     plan = codegen.Plan(r.graph, r.out_nodes, args, r.name, allow_cpu=True)
@@ -174,3 +174,45 @@ def test_linear_relu_cpu_fallback_is_exact():
     lin = torch.nn.Linear(16, 8)
     x = torch.randn(3, 5, 16)
     assert torch.equal(ModuleRuntime.linear_relu(lin, x), torch.relu(lin(x)))
+
+
+def test_dynamic_shape_def_evaluated_at_its_site():
+    """`idx = nonzero(x > 0.5); x = x * 0.1; idx.sum()` —
+    the fixed-shape replacement is evaluated where `idx` was defined, so the
+    rebinding of `x` in between cannot change it (eager: 1097.2-style sums,
+    not the rebound x's)."""
+    src = ("import torch\n\ndef f(x):\n    idx = torch.nonzero(x > 0.5)\n    x = x * 0.1\n"
+           "    m = torch.masked_select(x, x > 0.01)\n    x = x + 1\n    return idx.sum() + m.sum() + x.sum()\n")
+    mod, low = lowering.load(src, allow_eager=True)
+    assert sorted(op for _, op in low.dynamic_shape_lowered) == ["masked_select", "nonzero"]
+    torch.manual_seed(0)
+    x = torch.rand(64, 32)
+    ns = {}
+    exec(compile(src, "f", "exec"), ns)
+    ref = ns["f"](x.clone())
+    out = mod.f(x.clone())
+    assert torch.equal(out, ref), (out, ref)
+
+
+def test_names_read_by_nested_scopes_stay_live():
+    """a lambda defined before `h` is assigned reads it
+    when called later — `h` must stay a region output."""
+    src = ("import torch\n\ndef f(x):\n    g = lambda: h * 2\n    h = x + 1\n    y = h * 3\n    return g() + y\n")
+    mod, low = lowering.load(src, allow_eager=True)
+    x = torch.randn(16)
+    assert torch.equal(mod.f(x), (x + 1) * 2 + (x + 1) * 3)
+    assert any("h" in r.out_names for r in low.regions)
+
+
+def test_unsupported_region_raises_without_allow_eager():
+    """No silent fallback: CPU tensors (or any argument the fused kernel
+    cannot take) raise RegionUnsupported unless the caller opts in."""
+    from paper_2509_16248_b200.region import RegionUnsupported
+
+    src = "import torch\n\ndef f(x):\n    y = x * 2 + 1\n    return y\n"
+    mod, low = lowering.load(src)
+    with pytest.raises(RegionUnsupported):
+        mod.f(torch.randn(8))
+    mod, low = lowering.load(src, allow_eager=True)
+    assert torch.equal(mod.f(torch.ones(8)), torch.full((8,), 3.0))
+    assert low.regions[0].stats.fallbacks == 1
