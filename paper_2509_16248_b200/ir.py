@@ -443,6 +443,43 @@ def infer(graph: Graph, args: list, needed: list[Node]) -> None:
             raise Unsupported(f"value of type {type(v).__name__}")
 
 
+def evaluate(roots: list[Node], args: list) -> dict[int, Any]:
+    """Evaluate the DAG eagerly with PyTorch on the arguments' device — the
+    same operators, in the same order and dtypes, that the transformed
+    statements run in eager mode.  Test infrastructure: the parity tests
+    evaluate a region's statistics and branch decisions on CPU (the oracle's
+    arithmetic) to compare with the fused kernel's scalar slots.  Returns
+    {node.uid: value}."""
+    vals: dict[int, Any] = {}
+    for node in topo(roots):
+        if node.op == "free":
+            v = args[node.value]
+        elif node.op == "const":
+            v = node.value
+        else:
+            a = [vals[x.uid] for x in node.args]
+            if node.op == "clamp":
+                v = _meta_clamp(node, a)
+            elif node.op == ITEM:
+                v = a[0].item()
+            elif node.op == BOOL_NOT:
+                v = torch.logical_not(a[0]) if torch.is_tensor(a[0]) else (not a[0])
+            elif node.op in (BOOL_AND, BOOL_OR):
+                if torch.is_tensor(a[0]) or torch.is_tensor(a[1]):
+                    f = torch.logical_and if node.op == BOOL_AND else torch.logical_or
+                    v = f(torch.as_tensor(a[0]), torch.as_tensor(a[1]))
+                else:
+                    v = (a[0] and a[1]) if node.op == BOOL_AND else (a[0] or a[1])
+            elif node.op in (IS_NONE, IS_NOT_NONE):
+                v = (a[0] is None) == (node.op == IS_NONE)
+            elif node.op == NZSUM:
+                v = torch.nonzero(a[0]).sum()
+            else:
+                v = META_FNS[node.op](*a)
+        vals[node.uid] = v
+    return vals
+
+
 def fold_host_predicates(graph: Graph, outputs: list[Node], args: list) -> tuple[Graph, list[Node]]:
     """Resolve `is None` / `is not None` of the region's free values for these
     arguments (the specialisation key includes each argument's type) and

@@ -28,3 +28,13 @@ def programs():
     from paper_2509_16248_b200.harness import programs as load
 
     return load()
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Decision margins |stat - threshold| logged by parity.check_scalars go
+    to $GM_MARGINS_OUT (JSON lines) when set (tools/gpu_round.sh sets it)."""
+    out = os.environ.get("GM_MARGINS_OUT")
+    if out:
+        from parity import dump_margins
+
+        dump_margins(out)

@@ -88,9 +88,14 @@ def test_bool_and_scalar_live_outs_and_integer_reductions():
     assert torch.equal(out[0].cpu(), ref[0])
     assert out[1].dtype == ref[1].dtype == torch.int64 and int(out[1]) == int(ref[1])
     assert int(out[2]) == int(ref[2])
-    # fp32 mean/norm: the B200 statistic is the correctly rounded value, the
-    # CPU one carries fp32 accumulation drift (see test_gpu_kernels)
-    assert math.isclose(float(out[3]), float(ref[3]), rel_tol=1e-3)
+    # fp32 mean/norm: the B200 statistic is accumulated in fp64 and rounded
+    # once; torch's CPU fp32 reductions over 6.3 M elements drift.  The bound
+    # is the north_star 1e-5 relative plus that drift, MEASURED here against
+    # the same expression evaluated in fp64 on CPU
+    ref64 = float(x.double().mean() + x.double().norm())
+    drift = abs(float(ref[3]) - ref64)
+    assert abs(float(out[3]) - float(ref[3])) <= 1e-5 * abs(float(ref[3])) + drift, (float(out[3]), float(ref[3]), drift)
+    assert abs(float(out[3]) - ref64) <= 2e-7 * abs(ref64) + 1e-6, (float(out[3]), ref64)
 
 
 @pytest.mark.gpu
@@ -241,3 +246,59 @@ def t(x):
     ulp = (o[fin].view(torch.int16).int() - r[fin].view(torch.int16).int()).abs()
     assert int(ulp.max()) <= 1
     assert float((ulp != 0).float().mean()) < 1e-3
+
+
+PRED = '''import torch
+
+def f(x):
+    __gm_pred_0 = RED
+    __gm_then_y_0 = x * 2 + 1
+    __gm_else_y_0 = x - 3
+    y = torch.where(__gm_pred_0, __gm_then_y_0, __gm_else_y_0)
+    return y
+'''
+
+
+def _pm1(neg: int, twos: int, shape=(8, 1024, 768)) -> torch.Tensor:
+    """+-1 with `neg` negative entries and `twos` entries 2.0: the product is
+    +-2^twos exactly in any evaluation order (no order-dependent rounding)."""
+    g = torch.Generator().manual_seed(neg * 7 + twos)
+    n = math.prod(shape)
+    x = torch.ones(n)
+    perm = torch.randperm(n, generator=g)
+    x[perm[:neg]] = -1.0
+    x[perm[neg:neg + twos]] = 2.0
+    return x.view(shape)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("red,make,want", [
+    ("x.prod() > 0", lambda: _pm1(1000, 5), True),
+    ("x.prod() > 0", lambda: _pm1(1001, 5), False),
+    ("x.prod() >= 32.0", lambda: _pm1(2, 5), True),
+    ("x.prod() >= 64.0", lambda: _pm1(2, 5), False),
+    ("(x > 3.5).any()", lambda: torch.randn(8, 1024, 768, generator=torch.Generator().manual_seed(5)), True),
+    ("(x > 6.5).any()", lambda: torch.randn(8, 1024, 768, generator=torch.Generator().manual_seed(5)), False),
+    ("(x > -6.5).all()", lambda: torch.randn(8, 1024, 768, generator=torch.Generator().manual_seed(6)), True),
+    ("(x > -3.0).all()", lambda: torch.randn(8, 1024, 768, generator=torch.Generator().manual_seed(6)), False),
+    ("x.any()", lambda: torch.zeros(8, 1024, 768), False),
+    ("x.all()", lambda: _pm1(7, 0), True),
+], ids=["prod_pos", "prod_neg", "prod_ge32", "prod_ge64", "any_t", "any_f", "all_t", "all_f", "any_zero", "all_pm1"])
+def test_prod_any_all_predicates(red, make, want, dtype):
+    """prod / any / all predicates (data/attr_table.cfg:8-9,14) at
+    [8,1024,768] as fused reductions: decision and output equal the
+    reference's CPU eager execution of the same transformed text."""
+    from parity import check_scalars
+
+    text = PRED.replace("RED", red)
+    x = make().to(dtype)
+    ref = orc.reference_callable(text, "f")(x.clone())
+    ex, mod, low = compile_program(text, "f")
+    out = ex(x.cuda())
+    torch.cuda.synchronize()
+    assert low.regions[0].stats.launches >= 1 and low.regions[0].stats.fallbacks == 0
+    ref_decision = bool(orc.reference_callable("import torch\n\ndef p(x):\n    return " + red + "\n", "p")(x.clone()))
+    assert ref_decision == want
+    assert check_scalars(low, text, "f", [x], dtype, what=red) == 1
+    assert_parity(out, ref, dtype, what=red)

@@ -100,3 +100,28 @@ def test_workload_equivalence_original_vs_transformed(programs, name):
         assert ta == tb
         abs_d, rel_d = orc.diffs(a, b)
         assert rel_d <= orc.FLOAT_RTOL or abs_d <= orc.FLOAT_ATOL
+
+
+@pytest.mark.parametrize("name", sorted(FIX_RATE_TABLE) + ["toy", "bigbird_like", "bart_step"])
+def test_count_breaks_per_case(programs, name):
+    """runner.py:171-177 `count_breaks`, executed per case on the manifest's
+    explain input (runner.py:216-225): the original program's graph splits
+    equal `expected_breaks_before` and the transformed program's equal
+    `expected_breaks_after` (pkg/corpus/*/manifest.json) — for the stand-ins
+    the transformed count equals the reference's predicted residual (0).
+    Small shapes: break counts do not depend on sizes."""
+    p = programs[name]
+    spec = p["inputs"][p["explain_input"]]
+    shapes = None
+    if name == "bigbird_like":
+        shapes = [[1, 64, 768]]
+    elif name == "bart_step":
+        shapes = [[4, 1, 768]]
+    args = orc.make_args(spec["args"], spec["seed"], shapes=shapes)
+    before = orc.count_breaks(orc.reference_callable(p["original"], p["callable"]), args)
+    after = orc.count_breaks(orc.reference_callable(p["transformed"], p["callable"]), args)
+    if "expected_breaks_after" in p:
+        assert (before, after) == (p["expected_breaks_before"], p["expected_breaks_after"]), (name, before, after)
+    else:
+        assert after == p["expected"]["predicted_residual"], (name, before, after)
+        assert before > 0, (name, before)   # the original does split
