@@ -1,18 +1,24 @@
 """Bench: forward latency / throughput of a GraphMend-transformed program on
 the B200 path (BASELINE.json metric; config 2 = BigBird-like layer, seq 1024,
-batch 8, bf16, random-init weights, synthetic inputs).
+batch 8, fp32 — the reference harness's own precision, runner.py:114-125 —
+random-init weights, synthetic inputs).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--dtype bf16|fp32]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--dtype fp32|bf16]
     python bench.py --impl reference ...     # the reference's CPU path on the host cores
 
-A step = one forward of the transformed program over one batch.  `value` is
-whole-job samples/s with inputs resident in HBM (graph replay only, device
-timed per step with CUDA events, L2 flushed between steps); `e2e` is the same
-forward through the public API (B200Executor.__call__) from pinned host
-buffers with the H2D input copy and D2H output read inside the timed region.
-Multi-GPU: independent replicas (every predicate is a global
-reduction, so the path does not shard), one process per GPU; the timing is
-the max over ranks.
+A step = one forward of the transformed program over one batch.  The
+manifest's inputs (bigbird_like: seeds 63 / 61 / 62, whose branch decisions
+differ) ROTATE through every timed loop, so speculation is measured with
+changing decisions and the hit rate is reported.  `value` is whole-job
+samples/s with inputs resident in HBM (graph replay only, device timed per
+step with CUDA events, L2 flushed between steps); `e2e` is the same forward
+through the public API (B200Executor) from pinned host buffers with the H2D
+input copy and D2H output read inside the timed region.  `compile` is the
+north_star comparator: the UNTRANSFORMED program under torch.compile
+(default and reduce-overhead) on the same GPU and inputs.  Multi-GPU:
+independent replicas (every predicate is a global reduction, so
+the path does not shard), one process per GPU, gloo only for the timing
+barrier and the max over ranks — no NCCL.
 """
 
 from __future__ import annotations
@@ -33,6 +39,7 @@ METRIC = "p50 forward latency (ms) & samples/s per model; host syncs per forward
 WORKLOADS = {
     "bigbird_like": ("config 2: BigBird-RoBERTa-base-shaped layer, seq 1024, batch 8", None),
     "bart_step": ("config 4: BART-base-shaped decoder step, batch 32", None),
+    "gemm_arms": ("config 2 variant: BigBird-shaped layer whose predicated arms each hold a GEMM", None),
     "phi4_like": ("config 5: corpus phi4_like at [8,1024,768]", [[8, 1024, 768]]),
     "qwen_audio_like": ("config 5: corpus qwen_audio_like at [8,1024,768]", [[8, 1024, 768]]),
     "longformer_like": ("config 3: corpus longformer_like at [4,4096,768]", [[4, 4096, 768]]),
@@ -99,14 +106,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def max_over_ranks(x: float, dist_mod, device=None) -> float:
-    """Max of a per-rank duration across replicas (all-reduce MAX on a 1-elem
-    tensor: plumbing for the timing, not a data-path collective)."""
+def max_over_ranks(x: float, dist_mod) -> float:
+    """Max of a per-rank duration across replicas (gloo all-reduce MAX of a
+    1-element CPU tensor: plumbing for the timing, not a data-path
+    collective; no NCCL)."""
     if dist_mod is None or not dist_mod.is_initialized() or dist_mod.get_world_size() == 1:
         return x
     import torch
 
-    t = torch.tensor([x], dtype=torch.float64, device=device or "cpu")
+    t = torch.tensor([x], dtype=torch.float64)
     dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
     return float(t)
 
@@ -165,78 +173,191 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _inputs(prog, shapes, dtype):
+def _all_inputs(prog, shapes, dtype):
+    """Every manifest input (runner.py:114-125 draws), in manifest order."""
     from paper_2509_16248_b200.harness import make_args
 
-    spec = prog["inputs"][0]
-    return make_args(spec["args"], spec["seed"], dtype, shapes)
+    return [make_args(spec["args"], spec["seed"], dtype, shapes) for spec in prog["inputs"]]
+
+
+def _config(args, x0) -> dict:
+    """Identical in both arms (the driver compares them)."""
+    prog_inputs = _programs()[args.workload]["inputs"]
+    return {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": int(x0.shape[0]),
+            "shape": list(x0.shape),
+            "inputs": "manifest draws rotated every step: " + ", ".join(
+                f"seed {sp['seed']} ({sp.get('note', '')})" for sp in prog_inputs)}
+
+
+def _programs():
+    from paper_2509_16248_b200.harness import programs
+
+    return programs()
+
+
+def _cpu_rate(prog, xs, dtype, budget_s: float, max_forwards: int = 100000):
+    """The reference's CPU path — the reference-transformed program executed
+    eagerly on CPU in the harness call shape (runner.py:154-157), all host
+    threads — over the rotating inputs for `budget_s` seconds.
+    Returns (samples/s, forwards, p50 ms, threads)."""
+    import torch
+
+    from oracle import executor as orc
+
+    threads = len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    fn = orc.reference_callable(prog["transformed"], prog["callable"], dtype)
+    orc.call_captured(fn, xs[0])
+    times = []
+    t_end = time.perf_counter() + budget_s
+    k = 0
+    while (time.perf_counter() < t_end or not times) and len(times) < max_forwards:
+        t0 = time.perf_counter()
+        orc.call_captured(fn, xs[k % len(xs)])
+        times.append(time.perf_counter() - t0)
+        k += 1
+    batch = int(xs[0][0].shape[0])
+    return batch * len(times) / sum(times), len(times), 1e3 * statistics.median(times), threads
 
 
 def run_reference(args, ws, rank):
-    """The reference's CPU path: the reference-transformed program executed
-    eagerly on CPU (harness call shape, runner.py:154-157) with all host
-    threads; rank 0 only."""
+    """`--impl reference`: the reference's CPU path on the box's host cores,
+    rank 0 only (the other ranks exit without work).  Each of the K timed
+    steps is a bounded sample: eager forwards over the rotating inputs for
+    ~10 s / K, so the whole run is a ~10 s window like `cpu_baseline`."""
     if rank != 0:
         return
     import torch
 
-    from oracle import executor as orc
-    from paper_2509_16248_b200.harness import programs
-
-    threads = len(os.sched_getaffinity(0))
-    torch.set_num_threads(threads)
     dtype = {"bf16": torch.bfloat16, "fp32": torch.float32}[args.dtype]
-    prog = programs()[args.workload]
-    shapes = WORKLOADS[args.workload][1]
-    x = _inputs(prog, shapes, dtype)
+    prog = _programs()[args.workload]
+    xs = _all_inputs(prog, WORKLOADS[args.workload][1], dtype)
+    from oracle import executor as orc
+
     fn = orc.reference_callable(prog["transformed"], prog["callable"], dtype)
-    for _ in range(args.warmup):
-        orc.call_captured(fn, x)
-    times = []
+    torch.set_num_threads(len(os.sched_getaffinity(0)))
+    for k in range(args.warmup):
+        orc.call_captured(fn, xs[k % len(xs)])
+    per_step = 10.0 / max(1, args.steps)
+    total_s, forwards, step_ms, p50s = 0.0, 0, [], []
+    threads = len(os.sched_getaffinity(0))
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        orc.call_captured(fn, x)
-        times.append(time.perf_counter() - t0)
-    batch = int(x[0].shape[0])
-    total = sum(times)
-    value = batch * len(times) / total
+        v, n, p50, threads = _cpu_rate(prog, xs, dtype, per_step)
+        batch = int(xs[0][0].shape[0])
+        dt = batch * n / v
+        total_s += dt
+        forwards += n
+        step_ms.append(1e3 * dt)
+        p50s.append(p50)
+    batch = int(xs[0][0].shape[0])
+    value = batch * forwards / total_s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "p50_ms": 1e3 * statistics.median(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (manifest seed/dist), random-init weights",
-        "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
-                   "shape": list(x[0].shape)},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port", "cpu_model": _cpu_model(),
-                         "sample": f"{len(times)} full forwards of the reference-transformed program, eager "
-                                   f"torch CPU, {threads} threads"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms),
+        "p50_ms": statistics.median(p50s), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": DATA,
+        "config": _config(args, xs[0][0]),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "cpu_model": _cpu_model(),
+                         "sample": f"{args.steps} steps x ~{per_step:.2f} s: {forwards} eager forwards of the "
+                                   f"reference-transformed program over the rotating manifest inputs, torch CPU, "
+                                   f"{threads} threads"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+DATA = "synthetic inputs (manifest seeds/dists at the BASELINE shape, rotated), random-init weights (seed 0)"
 
 
 def cpu_baseline(prog, shapes, dtype, budget_s=10.0):
     """Bounded CPU-oracle sample on the box's host cores (rank 0, N=1)."""
     import torch
 
+    xs = _all_inputs(prog, shapes, dtype)
+    v, n, p50, threads = _cpu_rate(prog, xs, dtype, budget_s)
+    return {"value": v, "unit": "samples/s", "cores": threads, "kind": "port", "cpu_model": _cpu_model(),
+            "sample": f"{n} eager forwards of the reference-transformed program over the rotating manifest inputs "
+                      f"(~{budget_s:.0f} s), torch CPU, {threads} threads; p50 {p50:.2f} ms"}
+
+
+def _wall_p50(fn, xs, iters: int, warm: int = 3) -> float:
+    """p50 wall-clock ms of fn(*x) + synchronize, inputs rotating."""
+    import torch
+
+    for k in range(warm):
+        fn(*xs[k % len(xs)])
+    torch.cuda.synchronize()
+    ts = []
+    for k in range(iters):
+        x = xs[k % len(xs)]
+        t0 = time.perf_counter()
+        fn(*x)
+        torch.cuda.synchronize()
+        ts.append(1e3 * (time.perf_counter() - t0))
+    return statistics.median(ts)
+
+
+def compile_comparator(prog, dtype, xs_dev, ex, iters: int) -> dict:
+    """north_star's comparator: the UNTRANSFORMED original program under
+    torch.compile (Inductor; default and reduce-overhead), same GPU, weights
+    (seed 0) and rotating inputs, vs the B200 user-facing call
+    (B200Executor(*device inputs): input copy + graph replay).  p50 of wall
+    clock around a synchronised call; inference (no_grad) on both sides."""
+    import logging
+
+    import torch
+
     from oracle import executor as orc
 
-    threads = len(os.sched_getaffinity(0))
-    torch.set_num_threads(threads)
-    x = _inputs(prog, shapes, dtype)
-    fn = orc.reference_callable(prog["transformed"], prog["callable"], dtype)
-    orc.call_captured(fn, x)
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end and len(times) < 2000:
-        t0 = time.perf_counter()
-        orc.call_captured(fn, x)
-        times.append(time.perf_counter() - t0)
-    batch = int(x[0].shape[0])
-    return {"value": batch * len(times) / sum(times), "unit": "samples/s", "cores": threads, "kind": "port",
-            "cpu_model": _cpu_model(),
-            "sample": f"{len(times)} forwards of the reference-transformed program (same inputs), eager torch "
-                      f"CPU, {threads} threads; p50 {1e3 * statistics.median(times):.2f} ms"}
+    res = {"how": "p50 wall clock of call + cuda.synchronize, device-resident rotating inputs, warm; "
+                  "untransformed original under torch.compile vs B200Executor(*inputs) on the transformed text"}
+    logging.disable(logging.CRITICAL)
+    try:
+        with torch.no_grad():
+            res["b200_call_p50_ms"] = _wall_p50(lambda *a: ex(*a), xs_dev, iters)
+            ex.flush()
+            for mode in ("default", "reduce-overhead"):
+                torch._dynamo.reset()
+                try:
+                    fn = orc.reference_callable(prog["original"], prog["callable"], dtype)
+                    if isinstance(fn, torch.nn.Module):
+                        fn.to(xs_dev[0][0].device)
+                    c = torch.compile(fn, mode=None if mode == "default" else mode)
+                    t0 = time.perf_counter()
+                    for x in xs_dev:
+                        c(*x)
+                    torch.cuda.synchronize()
+                    res[f"{mode}_cold_ms"] = 1e3 * (time.perf_counter() - t0)
+                    res[f"{mode}_p50_ms"] = _wall_p50(c, xs_dev, iters)
+                except Exception as exc:  # report, keep the bench line
+                    res[f"{mode}_error"] = repr(exc)[:300]
+            torch._dynamo.reset()
+    finally:
+        logging.disable(logging.NOTSET)
+    if res.get("default_p50_ms"):
+        res["speedup_vs_compile"] = res["default_p50_ms"] / res["b200_call_p50_ms"]
+    if res.get("reduce-overhead_p50_ms"):
+        res["speedup_vs_compile_reduce_overhead"] = res["reduce-overhead_p50_ms"] / res["b200_call_p50_ms"]
+    return res
+
+
+def profile_syncs(ex, x_dev) -> dict:
+    """torch.profiler count, inside one user-facing forward, of host-blocking
+    CUDA calls and device-to-host copies."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    ex(*x_dev)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        ex(*x_dev)
+    torch.cuda.synchronize()
+    names = [e.name for e in prof.events()]
+    syncs = sum(1 for n in names if n in ("cudaStreamSynchronize", "cudaDeviceSynchronize", "cudaEventSynchronize"))
+    d2h = sum(1 for n in names if "DtoH" in n or "Device -> Pinned" in n or "Device -> Pageable" in n)
+    return {"cuda_syncs": syncs, "d2h_copies": d2h, "how": "torch.profiler over one B200Executor call "
+            "(device inputs): cudaStream/Device/EventSynchronize calls and DtoH memcpy events"}
 
 
 def main():
@@ -246,8 +367,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="bigbird_like", choices=sorted(WORKLOADS))
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--dtype", default="fp32", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compile", action="store_true", help="skip the torch.compile comparator")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     ws, rank, local = _dist()
@@ -257,29 +379,32 @@ def main():
 
     import torch
 
-    from paper_2509_16248_b200 import compile_program
-    from paper_2509_16248_b200.harness import programs
+    from paper_2509_16248_b200 import compile_program, gemm
+    from paper_2509_16248_b200.region import scratch_owner
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if ws > 1:
+        # replicas only: gloo carries the timing barrier and the max over
+        # ranks (CPU tensors) — there is no NCCL and no data-path collective
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo")
         pg = dist
     dtype = {"bf16": torch.bfloat16, "fp32": torch.float32}[args.dtype]
-    prog = programs()[args.workload]
+    prog = _programs()[args.workload]
     shapes = WORKLOADS[args.workload][1]
-    x_host = [t.pin_memory() for t in _inputs(prog, shapes, dtype)]
-    batch = int(x_host[0].shape[0])
+    xs_host = [[t.pin_memory() for t in x] for x in _all_inputs(prog, shapes, dtype)]
+    xs_dev = [[t.to(dev) for t in x] for x in xs_host]
+    R = len(xs_host)
+    batch = int(xs_host[0][0].shape[0])
 
     t0 = time.perf_counter()
     ex, mod, low = compile_program(prog["transformed"], prog["callable"], device=dev, dtype=dtype)
-    entry = ex.prepare(*[t.to(dev) for t in x_host])
+    entry = ex.prepare(*xs_dev[0])
     torch.cuda.synchronize(dev)
     cold_ms = 1e3 * (time.perf_counter() - t0)
-    entry.load([t.to(dev) for t in x_host])
     info = entry.info
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     flush_rd = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.int64, device=dev)
@@ -297,8 +422,21 @@ def main():
             pg.barrier()
         torch.cuda.synchronize(dev)
 
-    # ---- device-timed replay (inputs resident in HBM)
-    for _ in range(args.warmup):
+    def spec_totals():
+        tot = [0, 0]
+        for r in low.regions:
+            sp = r.last_spec
+            if sp is not None and sp.plan.spec:
+                a, b = sp.spec_stats()
+                tot[0] += a
+                tot[1] += b
+        return tot
+
+    # ---- device-timed replay (inputs resident in HBM, rotating): before
+    #      each step the step's input is copied into the graph's static
+    #      buffers and the L2 is flushed, both outside the timed window
+    for k in range(args.warmup):
+        entry.load(xs_dev[k % R])
         entry.run()
     ex.flush()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -309,22 +447,29 @@ def main():
         # under load, so the clock record covers the timed region
         t_load = time.perf_counter()
         while time.perf_counter() - t_load < 1.0 or len(clocks.rows) < 3:
-            for _ in range(200):
+            for _ in range(50):
                 entry.run()
             torch.cuda.synchronize(dev)
             if time.perf_counter() - t_load > 5.0:
                 break
         barrier()
+        spec0 = spec_totals()
         for i in range(args.steps):
+            entry.load(xs_dev[i % R])
             flush_l2()
             starts[i].record(stream)
             entry.run()
             ends[i].record(stream)
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    spec1 = spec_totals()
     ex.flush()
-    total_ms = max_over_ranks(sum(step_ms), pg, dev)
+    total_ms = max_over_ranks(sum(step_ms), pg)
     value = replica_value(batch, args.steps, ws, total_ms / 1e3)
+    speculation = {"launches": spec1[0] - spec0[0], "mispredictions": spec1[1] - spec0[1],
+                   "how": f"speculative region launches in the timed loop, inputs rotating over {R} manifest draws"}
+    if speculation["launches"]:
+        speculation["hit_rate"] = 1.0 - speculation["mispredictions"] / speculation["launches"]
 
     # ---- each fused kernel timed on its own stream, cold L2: a CUDA graph of
     #      R x [256 MB L2 flush, region launch] minus a graph of R x [flush],
@@ -339,8 +484,6 @@ def main():
              "passes": spec.plan.npass, "speculative": spec.plan.spec,
              "how": "graph of 20 x (L2 flush + launch) minus 20 x flush; cold L2"}
         if spec.plan.spec:
-            launches, misses = spec.spec_stats()
-            k["spec_launches"], k["spec_misses"] = launches, misses
             k["ms_mispredicted"] = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev, mispredict=True)
         kernels.append(k)
     dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
@@ -351,40 +494,43 @@ def main():
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": _ncu_traffic(dom["name"].split(" ")[0]), "kernel": dom["name"],
                     "bytes_alg": dom["bytes"], "kernel_ms": dom["ms"],
-                    "peak_kind": peak_kind, "share_of_step": dom["ms"] / statistics.mean(step_ms)}
+                    "peak_kind": peak_kind, "share_of_step": dom["ms"] / statistics.mean(step_ms),
+                    "traffic_how": "ncu dram__bytes_read+write per launch from the committed profiles/ capture"}
 
     # ---- end to end through the public API, host buffers in and out:
     # (a) single call latency: executor(*pinned host inputs) -> D2H into a
     #     pinned host tensor, synchronised; (b) throughput: the executor's
-    #     pipelined host path (H2D / forward / D2H overlapped, 3 graph slots).
-    h2d = sum(t.numel() * t.element_size() for t in x_host)
-    out0 = ex(*x_host)
+    #     pipelined host path (H2D / forward / D2H overlapped, 3 graph slots),
+    #     inputs rotating so each slot's graph sees changing decisions
+    h2d = sum(t.numel() * t.element_size() for t in xs_host[0])
+    out0 = ex(*xs_host[0])
     out_pinned = torch.empty(out0.shape, dtype=out0.dtype, pin_memory=True)
     e2e_ms = []
     for i in range(args.steps + 3):
         e0 = time.perf_counter()
-        out = ex(*x_host)
+        out = ex(*xs_host[i % R])
         out_pinned.copy_(out, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
         if i >= 3:
             e2e_ms.append(1e3 * (time.perf_counter() - e0))
     ex.flush()
-    host_batches = [tuple(x_host)] * args.steps
+    S = 3
+    host_batches = [tuple(xs_host[(k // S) % R]) for k in range(args.steps)]
     # results land in a ring of 8 pinned host buffers (step k -> buffer k % 8:
     # the D2H copies into one buffer are ordered on the copy stream), so N
-    # replicas do not pin N x steps x 12.6 MB of host memory
+    # replicas do not pin N x steps x the output of host memory
     ring = [torch.empty(out0.shape, dtype=out0.dtype, pin_memory=True) for _ in range(min(8, args.steps))]
     outs = [ring[k % len(ring)] for k in range(args.steps)]
-    ex.run_host_pipelined(host_batches[:4], out=outs[:4])  # build the graph slots, warm
+    ex.run_host_pipelined(host_batches[:4], out=outs[:4], slots=S)  # build the graph slots, warm
     ex.flush()
     barrier()
     t_e2e = time.perf_counter()
-    ex.run_host_pipelined(host_batches, out=outs)
+    ex.run_host_pipelined(host_batches, out=outs, slots=S)
     barrier()
-    e2e_total = max_over_ranks(time.perf_counter() - t_e2e, pg, dev)
+    e2e_total = max_over_ranks(time.perf_counter() - t_e2e, pg)
     # the same pipelined H2D / D2H traffic with no forward: the PCIe
     # bound the end-to-end number sits against
-    pcie_s = _copy_only_pipeline(x_host, outs, dev, args.steps)
+    pcie_s = _copy_only_pipeline(list(host_batches[0]), outs, dev, args.steps)
     ex.flush()
     d2h = out_pinned.numel() * out_pinned.element_size()
 
@@ -399,12 +545,17 @@ def main():
     c0 = nat_.launch_count
     logging.disable(logging.CRITICAL)
     try:
-        with torch.no_grad(), contextlib.redirect_stdout(io.StringIO()):  # its deferred prints run now
+        with torch.no_grad(), contextlib.redirect_stdout(io.StringIO()), scratch_owner(entry):
             ex.fn(*entry.static)
             torch.cuda.synchronize(dev)
     finally:
         logging.disable(logging.NOTSET)
-    gpu_launches = args.steps * (nat_.launch_count - c0)
+    per_forward = nat_.launch_count - c0
+    gpu_launches = args.steps * per_forward
+    syncs = profile_syncs(ex, xs_dev[0])
+    comparator = None
+    if not args.no_compile and rank == 0:
+        comparator = compile_comparator(prog, dtype, xs_dev, ex, iters=max(50, args.steps))
     line = {
         "metric": METRIC,
         "value": value,
@@ -417,23 +568,29 @@ def main():
         "cold_ms": cold_ms,
         "transform_ms_one_time": _transform_ms(args.workload),
         "host_syncs_per_forward": info.host_syncs,
+        "host_syncs_profiler": syncs,
         "mode": info.mode,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": args.dtype,
-        "data": "synthetic inputs (manifest seed/dist at the BASELINE shape), random-init weights (seed 0)",
-        "config": {"workload": f"{args.workload} ({WORKLOADS[args.workload][0]})", "batch": batch,
-                   "shape": list(x_host[0].shape), "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2": "flushed between timed steps: 256 MB write, then 256 MB read (cold, clean L2)"},
+        "data": DATA,
+        "config": _config(args, xs_host[0][0]),
+        "parallelism": f"{ws} independent replicas (gloo timing barrier, no NCCL)" if ws > 1 else "single GPU",
+        "l2": "flushed between timed steps: 256 MB write, then 256 MB read (cold, clean L2)",
+        "speculation": speculation,
+        "compile": comparator,
         "e2e": {"value": replica_value(batch, args.steps, ws, e2e_total), "unit": "samples/s",
-                "how": "B200Executor.run_host_pipelined: pinned host inputs -> H2D -> graph replay -> D2H into "
-                       "pinned host outputs, 3 rotating graph slots; wall clock, max over ranks",
+                "how": "B200Executor.run_host_pipelined: pinned host inputs (rotating) -> H2D -> graph replay -> D2H "
+                       "into pinned host outputs, 3 rotating graph slots; wall clock, max over ranks",
                 "p50_ms_single_call": statistics.median(e2e_ms),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "copy_only_samples_per_s": replica_value(batch, args.steps, ws, pcie_s),
                 "copy_only_how": "same pipeline (two copy streams, pinned buffers) with the forward removed"},
         "gpu_launches": gpu_launches,
+        "gpu_launches_per_forward": per_forward,
+        "gemm": {"backend": "cuBLASLt 12.9 BF16x9 emulation (fp32)" if args.dtype == "fp32" else "torch cuBLAS",
+                 "calls": dict(gemm.stats)},
         "roofline": roofline,
         "kernels": kernels,
         "clocks": clocks.summary(),
@@ -484,9 +641,9 @@ def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5
     import torch
 
     nd = len(spec.plan.decisions) if spec.plan.spec else 0
-    from paper_2509_16248_b200.region import SCRATCH_PRED
+    from paper_2509_16248_b200.region import SCRATCH_PRED, scratch_owner
 
-    pred = spec.scratch[SCRATCH_PRED: SCRATCH_PRED + 4 * nd].view(torch.int32) if nd else None
+    owner = object()   # this measurement's own barrier scratch, zeroed before the captures
     wrong = None
     if mispredict and nd:
         vals = spec.scalars()
@@ -495,13 +652,14 @@ def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5
 
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
-    with torch.cuda.stream(side):
-        spec.run(args, pdl=False)  # warm (allocator, module)
+    with torch.cuda.stream(side), scratch_owner(owner):
+        spec.run(args, pdl=False)  # warm (allocator, module, this owner's scratch)
+        pred = spec.scratch[SCRATCH_PRED: SCRATCH_PRED + 4 * nd].view(torch.int32) if nd else None
     torch.cuda.current_stream(dev).wait_stream(side)
     torch.cuda.synchronize(dev)
     g_both, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     keep = []
-    with torch.cuda.graph(g_both):
+    with torch.cuda.graph(g_both), scratch_owner(owner):
         for _ in range(reps):
             flush()
             if wrong is not None:

@@ -118,6 +118,16 @@ _SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_double,
       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
       ctypes.c_void_p]),
+    ("gm_gemm_open", ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),
+    ("gm_gemm_close", ctypes.c_int, [ctypes.c_void_p]),
+    ("gm_gemm_version", ctypes.c_size_t, []),
+    ("gm_gemm_run", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+      ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+      ctypes.c_size_t, ctypes.c_void_p]),
+    ("gm_select_copy", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+      ctypes.c_void_p]),
     ("gm_logring_open", ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     ("gm_logring_close", ctypes.c_int, [ctypes.c_void_p]),
     ("gm_logring_host_ptr", ctypes.c_void_p, [ctypes.c_void_p]),

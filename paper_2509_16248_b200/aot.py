@@ -26,6 +26,7 @@ B200 = B200_DEVICE   # SMs, max opt-in dynamic shared memory per block
 # (program, dtype, shapes) — BASELINE configs 2-5 plus the corpus at its own shapes
 SPECS = [("bigbird_like", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("bart_step", d, None) for d in (torch.bfloat16, torch.float32)] + \
+        [("gemm_arms", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("toy", torch.float32, None)]
 
 
@@ -47,7 +48,7 @@ def collect_sources(specs=None, progs=None) -> list[str]:
     torch.manual_seed(0)
     for name, dtype, shapes in specs:
         prog = progs[name]
-        mod, low = load(prog["transformed"])
+        mod, low = load(prog["transformed"], allow_eager=True)
         fn = getattr(mod, prog["callable"])
         if isinstance(fn, torch.nn.Module):
             fn.to(dtype)

@@ -101,6 +101,9 @@ int g_cc_major = 0, g_cc_minor = 0, g_num_sms = 0, g_smem_optin = 0, g_device = 
 
 }  // namespace
 
+// shared with gm_gemm.cu: one thread-local error slot behind gm_last_error()
+int gm_internal_fail(int code, const char* msg) { return fail(code, "%s", msg); }
+
 struct gm_region_s {
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;

@@ -36,7 +36,7 @@ import torch
 from torch.utils._pytree import tree_flatten, tree_unflatten
 
 from . import logring
-from .region import check_status
+from .region import check_status, scratch_owner
 
 _SYNC_MSG = "synchroniz"
 
@@ -125,9 +125,13 @@ class _Entry:
         # warm-up runs: their deferred calls are discarded, and any immediate
         # print/log output (sites the reference did not defer) is swallowed
         # and counted
+        # the last warm-up runs under this entry as scratch owner, so the
+        # buffers the captured graph uses (barrier scratch, GEMM workspace,
+        # distinct-sum tables) are allocated and zeroed before the capture
         with torch.cuda.stream(side), _watch_side_effects() as (se, buf):
-            for _ in range(ex.warmup):
-                with logring.step(dev, discard=True) as st:
+            for k in range(ex.warmup):
+                with logring.step(dev, discard=True) as st, \
+                        (scratch_owner(self) if k == ex.warmup - 1 else contextlib.nullcontext()):
                     _, n = count_syncs(ex.fn, *self.static)
                 ring.enqueue(st.template)
                 syncs = max(syncs, n)
@@ -141,7 +145,7 @@ class _Entry:
         if ex.use_graphs and syncs == 0 and not side_effects:
             g = torch.cuda.CUDAGraph()
             try:
-                with torch.cuda.graph(g, pool=ex.pool), _watch_side_effects():
+                with torch.cuda.graph(g, pool=ex.pool), _watch_side_effects(), scratch_owner(self):
                     with logring.step(dev, discard=False) as st:
                         self.outputs = ex.fn(*self.static)
                 self.template = st.template
@@ -173,7 +177,7 @@ class _Entry:
             self.graph.replay()
             self.ring.enqueue(self.template)
             return self.outputs
-        with logring.step(ex.device) as st:
+        with logring.step(ex.device) as st, scratch_owner(self):
             out = ex.fn(*self.static)
         self.ring.enqueue(st.template)
         return out

@@ -37,6 +37,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _native as nat
+from . import gemm
 from .region import stream_key, zeroed
 
 EDGEITEMS = 3      # torch._tensor_str.PRINT_OPTS defaults
@@ -183,8 +184,9 @@ class LogRing:
                 self.gathers += 1
                 tmpl.gathers += 1
                 gf = a.grad_fn
-                out.append(TensorRef(off, a.dtype, shape, counts, heads,
-                                     type(gf).__name__ if gf is not None else None, a.requires_grad))
+                # gemm.py records the grad_fn name the eager op would have had
+                name = getattr(a, "_gm_grad_fn", None) or (type(gf).__name__ if gf is not None else None)
+                out.append(TensorRef(off, a.dtype, shape, counts, heads, name, a.requires_grad))
             elif torch.is_tensor(a):
                 out.append(a.detach().clone() if not a.requires_grad else a)
             else:
@@ -386,11 +388,36 @@ class ModuleRuntime:
     # -- fixed-shape replacements of dynamic-shape ops whose
     #    only consumer is a full sum (see lowering._lower_dynamic_shape)
     @staticmethod
+    def call(mod, x):
+        """`self.<sub>(x)`: an nn.Linear runs gemm.linear (fp32: cuBLASLt
+        BF16x9 on the tensor cores), any other module as written."""
+        return gemm.module_call(mod, x)
+
+    @staticmethod
+    def matmul(a, b):
+        """`a @ b` / torch.matmul(a, b): gemm.matmul."""
+        return gemm.matmul(a, b)
+
+    @staticmethod
+    def linear(x, w, b=None):
+        """torch.nn.functional.linear(x, w, b): gemm.linear."""
+        return gemm.linear(x, w, b)
+
+    @staticmethod
+    def select_gemm(pred, kind, then_ops, else_ops):
+        """The one GEMM a GEMM-bearing predicated block needs (gemm.select_gemm)."""
+        return gemm.select_gemm(pred, kind, then_ops, else_ops)
+
+    @staticmethod
     def linear_relu(mod, x):
         """relu(mod(x)).  For an nn.Linear with bias on a CUDA tensor: one
-        cuBLASLt GEMM with the RELU_BIAS epilogue (torch._addmm_activation)
-        instead of a GEMM and a separate relu launch — relu commutes with
-        the rounding of the output, so the value is relu(Linear(x))."""
+        GEMM with a RELU_BIAS epilogue (fp32: gemm.linear on cuBLASLt BF16x9;
+        16-bit: torch._addmm_activation) instead of a GEMM and a separate
+        relu launch — relu commutes with the rounding of the output, so the
+        value is relu(Linear(x))."""
+        if (type(mod) is torch.nn.Linear and not mod._forward_hooks and not mod._forward_pre_hooks
+                and torch.is_tensor(x) and x.dtype == torch.float32 and x.is_cuda):
+            return gemm.linear(x, mod.weight, mod.bias, relu=True)
         if (isinstance(mod, torch.nn.Linear) and mod.bias is not None and torch.is_tensor(x) and x.is_cuda
                 and x.dim() >= 2 and x.dtype == mod.weight.dtype and x.shape[-1] == mod.in_features):
             y = torch._addmm_activation(mod.bias, x.reshape(-1, mod.in_features), mod.weight.t())

@@ -56,6 +56,7 @@ class Lowered:
     sites: list[ReplaySite] = field(default_factory=list)
     region_sources: list[str] = field(default_factory=list)
     dynamic_shape_lowered: list = field(default_factory=list)
+    gemm_arms: list = field(default_factory=list)
 
 
 def _torch_aliases(tree: ast.Module) -> tuple[set[str], set[str]]:
@@ -270,7 +271,7 @@ class _FunctionLowerer:
                 lr = self._linear_relu(e)
                 if lr is not None:
                     e = lr
-                if isinstance(e, ast.BinOp):
+                if isinstance(e, ast.BinOp) and not isinstance(e.op, ast.MatMult):
                     return ast.BinOp(split(e.left), e.op, split(e.right))
                 if isinstance(e, ast.UnaryOp):
                     return ast.UnaryOp(e.op, split(e.operand))
@@ -318,11 +319,162 @@ class _FunctionLowerer:
         return ast.Call(ast.Attribute(ast.Name(GM_RT, ast.Load()), "linear_relu", ast.Load()),
                         [inner.func, inner.args[0]], [])
 
+    # -- dense contractions -----------------------------------------------------
+    def _gemm_call(self, e: ast.expr) -> ast.expr | None:
+        """`a @ b`, `torch.matmul(a, b)`, `torch.nn.functional.linear(x, w[, b])`
+        and `self.<sub>(x)` -> the module runtime's GEMM entry points (gemm.py:
+        fp32 on cuBLASLt BF16x9; everything else as written)."""
+        rt = lambda name: ast.Attribute(ast.Name(GM_RT, ast.Load()), name, ast.Load())  # noqa: E731
+        if isinstance(e, ast.BinOp) and isinstance(e.op, ast.MatMult):
+            return ast.Call(rt("matmul"), [e.left, e.right], [])
+        if not isinstance(e, ast.Call) or e.keywords or any(isinstance(a, ast.Starred) for a in e.args):
+            return None
+        chain = attr_chain(e.func)
+        if chain is None:
+            return None
+        tn, fn = self.owner.torch_names, self.owner.functional_names
+        if len(chain) == 2 and chain[0] in tn and chain[1] == "matmul" and len(e.args) == 2:
+            return ast.Call(rt("matmul"), list(e.args), [])
+        is_f = (len(chain) == 2 and chain[0] in fn) or (len(chain) == 4 and chain[0] in tn
+                                                        and chain[1:3] == ["nn", "functional"])
+        if is_f and chain[-1] == "linear" and len(e.args) in (2, 3):
+            return ast.Call(rt("linear"), list(e.args), [])
+        if chain[0] == "self" and len(chain) >= 2 and len(e.args) == 1:
+            return ast.Call(rt("call"), [e.func, e.args[0]], [])
+        return None
+
+    def _route_gemms(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
+        outer = self
+
+        class _Route(ast.NodeTransformer):
+            def visit_Lambda(self, node):
+                return node
+
+            def generic_visit(self, node):
+                node = super().generic_visit(node)
+                if isinstance(node, ast.expr):
+                    r = outer._gemm_call(node)
+                    if r is not None:
+                        return ast.copy_location(r, node)
+                return node
+
+        out = []
+        for s in stmts:
+            if isinstance(s, (ast.Assign, ast.AugAssign, ast.AnnAssign, ast.Return)) and s.value is not None \
+                    and _is_replay(s) is None:
+                s.value = _Route().visit(s.value)
+                ast.fix_missing_locations(s)
+            out.append(s)
+        return out
+
+    def _select_gemm_arms(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
+        """SURVEY §8f rank 3.  A predicated block whose arms each hold one
+        GEMM (transform.py:272 admits torch-rooted calls; :404-412 evaluates
+        both arms):
+            __gm_t_a = __gm_rt__.matmul(A1, B1)     # then arm
+            __gm_then_Y_k = __gm_t_a + c1
+            __gm_t_b = __gm_rt__.matmul(A2, B2)     # else arm
+            __gm_else_Y_k = __gm_t_b + c2
+            Y = torch.where(P, __gm_then_Y_k, __gm_else_Y_k)
+        becomes ONE contraction of the operands the predicate selects on the
+        device (gemm.select_gemm), read by both arms:
+            __gm_mm_j = __gm_rt__.select_gemm(P, 'matmul', (A1, B1), (A2, B2))
+            __gm_then_Y_k = __gm_mm_j + c1 ; __gm_else_Y_k = __gm_mm_j + c2
+        Under the `where` only the selected arm's value survives, and in that
+        arm __gm_mm_j is its own GEMM; arms are pure (the purity gate), so
+        the dropped GEMM had no effect."""
+        tn = self.owner.torch_names
+        out = list(stmts)
+
+        def gemm_of(s):
+            if not (isinstance(s, ast.Assign) and len(s.targets) == 1 and isinstance(s.targets[0], ast.Name)
+                    and isinstance(s.value, ast.Call) and not s.value.keywords):
+                return None
+            ch = attr_chain(s.value.func)
+            if ch in ([GM_RT, "matmul"], [GM_RT, "linear"]):
+                return s.targets[0].id, ch[1], s.value.args
+            return None
+
+        def def_index(name, before):
+            for j in range(before - 1, -1, -1):
+                t = out[j]
+                if isinstance(t, ast.Assign) and any(isinstance(x, ast.Name) and x.id == name
+                                                     for tg in t.targets for x in ast.walk(tg)):
+                    return j
+            return None
+
+        def stores(j0, j1):
+            names = set()
+            for t in out[j0:j1 + 1]:
+                names |= {n.id for n in ast.walk(t) if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Store)}
+            return names
+
+        def reads(name):
+            # generated names only (hoisted temps, arm temporaries): all their
+            # reads are in this block
+            if not name.startswith("__gm_"):
+                return [None, None]
+            return [n for t in out for n in ast.walk(t) if isinstance(n, ast.Name) and n.id == name
+                    and isinstance(n.ctx, ast.Load)]
+
+        i = 0
+        while i < len(out):
+            s = out[i]
+            w = s.value if isinstance(s, ast.Assign) else None
+            ch = attr_chain(w.func) if isinstance(w, ast.Call) else None
+            if not (ch and len(ch) == 2 and ch[0] in tn and ch[1] == "where" and len(w.args) == 3
+                    and not w.keywords and all(isinstance(a, ast.Name) for a in w.args)):
+                i += 1
+                continue
+            P, TT, TE = (a.id for a in w.args)
+            found = []
+            for arm in (TT, TE):
+                ja = def_index(arm, i)
+                g = None
+                if ja is not None:
+                    g = gemm_of(out[ja])
+                    if g is None:   # the GEMM is a hoisted temp read once by the arm statement
+                        cands = [n.id for n in ast.walk(out[ja].value) if isinstance(n, ast.Name)]
+                        for c in cands:
+                            jc = def_index(c, ja)
+                            if jc is not None and gemm_of(out[jc]) is not None and len(reads(c)) == 1:
+                                g, ja = gemm_of(out[jc]), jc
+                                break
+                    elif len(reads(arm)) != 1:
+                        g = None
+                found.append((ja, g))
+            (j1, g1), (j2, g2) = found
+            if g1 is None or g2 is None or j1 == j2 or g1[1] != g2[1] or len(g1[2]) != len(g2[2]):
+                i += 1
+                continue
+            lo, hi = min(j1, j2), max(j1, j2)
+            jp = def_index(P, lo + 1)
+            operand_names = {n.id for a in list(g1[2]) + list(g2[2]) for n in ast.walk(a) if isinstance(n, ast.Name)}
+            if (jp is None and P in stores(0, i)) or (jp is not None and jp >= lo) \
+                    or (operand_names | {P}) & stores(lo, hi) - {g1[0], g2[0]}:
+                i += 1
+                continue
+            name = f"__gm_mm_{self.owner.next_tmp()}"
+            call = ast.Call(ast.Attribute(ast.Name(GM_RT, ast.Load()), "select_gemm", ast.Load()),
+                            [ast.Name(P, ast.Load()), ast.Constant(g1[1]),
+                             ast.Tuple(list(g1[2]), ast.Load()), ast.Tuple(list(g2[2]), ast.Load())], [])
+            new = ast.copy_location(ast.Assign(targets=[ast.Name(name, ast.Store())], value=call), out[lo])
+            new.end_lineno, new.end_col_offset = out[lo].end_lineno, out[lo].end_col_offset
+            for old in (g1[0], g2[0]):
+                for n in reads(old):
+                    n.id = name
+                    self.loads.append(((n.lineno, n.col_offset), name))
+            out = out[:lo] + [new] + out[lo + 1:hi] + out[hi + 1:]
+            ast.fix_missing_locations(new)
+            self.owner.gemm_arms.append((P, g1[1]))
+            i = lo + 1
+        return out
+
     def lower_block(self, stmts: list[ast.stmt], in_loop: bool) -> list[ast.stmt]:
         out: list[ast.stmt] = []
         run: list[ast.stmt] = []
         hoist: list[ast.stmt] = []
-        stmts = self._split_calls(self._lower_dynamic_shape(stmts))
+        stmts = self._select_gemm_arms(self._route_gemms(self._split_calls(self._lower_dynamic_shape(stmts))))
         for stmt in self._split_returns(stmts):
             cap = _is_capture(stmt)
             if cap is not None and run:
@@ -434,6 +586,7 @@ class _Lowerer:
         self.sites: list[ReplaySite] = []
         self.fallback_defs: list[ast.FunctionDef] = []
         self.dyn_lowered: list[tuple[str, str]] = []
+        self.gemm_arms: list[tuple[str, str]] = []
 
     def next_tmp(self) -> int:
         self._tmp = getattr(self, "_tmp", 0) + 1
@@ -504,7 +657,8 @@ class _Lowerer:
             fn.body = fl.lower_block(fn.body, in_loop=False)
         ast.fix_missing_locations(self.tree)
         source = ast.unparse(self.tree)
-        return Lowered(self.text, source, self.regions, self.sites, self.region_sources, list(self.dyn_lowered))
+        return Lowered(self.text, source, self.regions, self.sites, self.region_sources, list(self.dyn_lowered),
+                       list(self.gemm_arms))
 
 
 def lower(text: str) -> tuple[Lowered, "_Lowerer"]:

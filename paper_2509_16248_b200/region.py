@@ -104,32 +104,78 @@ class RegionUnsupported(nat.NativeError):
     opt into running its statements with PyTorch (allow_eager)."""
 
 
-_aux_streams: dict = {}
+_owner = threading.local()
 
 
-def _aux_stream(dev: torch.device):
-    k = dev.index
-    if k not in _aux_streams:
-        _aux_streams[k] = torch.cuda.Stream(dev)
-    return _aux_streams[k]
+class scratch_owner:
+    """Context manager: launches inside it key their scratch by `owner`
+    instead of by (stream, capture id).  B200Executor runs its last warm-up
+    AND its capture under the entry as owner, so every buffer the captured
+    graph uses is allocated and zeroed eagerly before the capture starts
+    (nothing is allocated or filled while the stream captures) and belongs
+    to that graph alone."""
+
+    def __init__(self, owner):
+        self.owner = owner
+
+    def __enter__(self):
+        self.prev = getattr(_owner, "v", None)
+        _owner.v = self.owner
+        return self
+
+    def __exit__(self, *exc):
+        _owner.v = self.prev
+        return False
 
 
-def stream_key(dev: torch.device) -> tuple[int, int]:
-    """(stream, capture id) of the current stream: the owner of a scratch
-    buffer.  Eager launches on one stream are ordered; every CUDA-graph
-    capture gets its own key, so two graphs (or two streams) replaying the
-    same specialisation never share an arrival counter."""
+def stream_key(dev: torch.device) -> tuple:
+    """The owner of a scratch buffer: the active scratch_owner, else
+    (stream, capture id) of the current stream.  Eager launches on one
+    stream are ordered; every CUDA-graph capture gets its own key, so two
+    graphs (or two streams) replaying the same specialisation never share an
+    arrival counter."""
+    o = getattr(_owner, "v", None)
+    if o is not None:
+        return ("owner", id(o))
     s = torch.cuda.current_stream(dev).cuda_stream
     return s, nat.capture_id(s)
 
 
+SLAB_BYTES = 16 << 20
+_slabs: dict = {}
+
+
+def _slab_take(nbytes: int, dev: torch.device) -> torch.Tensor | None:
+    """A zeroed piece of the per-device slab (allocated and zeroed outside
+    any capture by the first region specialisation)."""
+    sl = _slabs.get(dev.index)
+    if sl is None:
+        return None
+    t, off = sl
+    n = (nbytes + 255) // 256 * 256
+    if off + n > t.numel():
+        return None
+    _slabs[dev.index] = (t, off + n)
+    return t[off: off + nbytes]
+
+
+def ensure_slab(dev: torch.device) -> None:
+    if dev.index not in _slabs and not torch.cuda.is_current_stream_capturing():
+        _slabs[dev.index] = (torch.zeros(SLAB_BYTES, dtype=torch.uint8, device=dev), 0)
+
+
 def zeroed(nbytes: int, dev: torch.device) -> torch.Tensor:
-    """A zero-filled device buffer.  Under CUDA-graph capture the fill runs on
-    a side stream outside the capture (so it is not replayed); the capture
-    driver synchronises the device before the graph's first replay."""
+    """A zero-filled device buffer.  While the current stream captures a CUDA
+    graph nothing may be allocated or filled outside it: small buffers come
+    from the pre-zeroed slab; larger ones must have been created by an eager
+    run under the same scratch_owner (B200Executor does this)."""
     if torch.cuda.is_current_stream_capturing():
-        with torch.cuda.stream(_aux_stream(dev)):
-            return torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        t = _slab_take(nbytes, dev)
+        if t is None:
+            raise nat.NativeError(
+                f"a {nbytes}-byte scratch buffer is first needed inside a CUDA-graph capture; run the forward once "
+                "eagerly under region.scratch_owner(<graph owner>) before capturing (B200Executor does)")
+        return t
     return torch.zeros(nbytes, dtype=torch.uint8, device=dev)
 
 
@@ -214,6 +260,7 @@ class _Spec:
         self._scratches: dict = {}
         self.scratch: torch.Tensor | None = None
         self.status_idx = -1
+        ensure_slab(dev)
         self.bind_scratch()
         P = nat.Params()
         P.n = n

@@ -26,20 +26,27 @@ def test_reference_arm_line():
     assert d["unit"] == "samples/s" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
-    assert d["config"]["workload"].startswith("bigbird_like")
+    assert d["config"]["workload"].startswith("bigbird_like") and d["dtype"] == "fp32"
+    assert set(d["config"]) == {"workload", "batch", "shape", "inputs"}   # identical keys in both arms
 
 
 @pytest.mark.gpu
 def test_b200_arm_line():
-    d = _run(["--steps", "5", "--warmup", "3", "--no-cpu-baseline"])
+    d = _run(["--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-compile"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
-              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks"):
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks", "speculation"):
         assert k in d, k
-    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["dtype"] == "bf16"
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["dtype"] == "fp32"
+    assert set(d["config"]) == {"workload", "batch", "shape", "inputs"}
     assert d["host_syncs_per_forward"] == 0 and d["mode"] == "graph"
-    assert d["gpu_launches"] == 5 * 2                     # two fused regions per forward
+    assert d["host_syncs_profiler"]["cuda_syncs"] == 0 and d["host_syncs_profiler"]["d2h_copies"] == 0
+    # two fused regions + two fp32 GEMMs (cuBLASLt BF16x9) per forward
+    assert d["gpu_launches_per_forward"] == 4 and d["gpu_launches"] == 5 * 4
+    # the rotating inputs change the branch decisions: some launches mispredict
+    sp = d["speculation"]
+    assert sp["launches"] == 5 * 2 and 0 < sp["mispredictions"] <= sp["launches"]
     e = d["e2e"]
-    assert e["value"] > 0 and e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 8 * 1024 * 768 * 2
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 8 * 1024 * 768 * 4
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5 and r["peak"] > 0
     assert all(k["speculative"] for k in d["kernels"])

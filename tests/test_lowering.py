@@ -158,13 +158,15 @@ def test_boolean_predicates_lowered():
 
 def test_calls_hoisted_out_of_elementwise_expressions(programs):
     """bart_step: `out = self.fc2(f) + h` becomes `t = self.fc2(f); out = t + h`
-    so the add fuses with the epilogue `out * 0.5`; `relu(self.fc1(h))`
-    becomes one cuBLASLt GEMM with a RELU_BIAS epilogue (linear_relu)."""
+    so the add fuses with the epilogue `out * 0.5` (the Linear call itself
+    goes through the runtime's GEMM entry, gemm.module_call);
+    `relu(self.fc1(h))` becomes one cuBLASLt GEMM with a RELU_BIAS epilogue
+    (linear_relu)."""
     low, _ = lowering.lower(programs["bart_step"]["transformed"])
     assert [r.out_names for r in low.regions] == [["h"], ["__gm_ret_0"]]
     body = low.source.split("def forward")[1]
     assert "__gm_rt__.linear_relu(self.fc1, h)" in body
-    assert "= self.fc2(f)" in body and "torch.relu" not in body
+    assert "= __gm_rt__.call(self.fc2, f)" in body and "torch.relu" not in body
 
 
 def test_linear_relu_cpu_fallback_is_exact():
@@ -216,3 +218,22 @@ def test_unsupported_region_raises_without_allow_eager():
     mod, low = lowering.load(src, allow_eager=True)
     assert torch.equal(mod.f(torch.ones(8)), torch.full((8,), 3.0))
     assert low.regions[0].stats.fallbacks == 1
+
+
+def test_gemm_arms_become_one_selected_gemm(programs):
+    """both arms of the gemm_arms block hold a
+    torch.matmul; the lowering replaces the pair by ONE select_gemm read by
+    both arms, whose selects and epilogues fuse into one region; on CPU
+    (allow_eager) the lowered program equals the transformed one."""
+    p = programs["gemm_arms"]
+    low, _ = lowering.lower(p["transformed"])
+    assert low.gemm_arms == [("__gm_pred_0", "matmul")]
+    body = low.source.split("def forward")[1]
+    assert body.count("select_gemm(") == 1 and "torch.matmul" not in body
+    assert "__gm_rt__.call(self.query, hidden)" in body
+    for spec in p["inputs"]:
+        args = orc.make_args(spec["args"], spec["seed"], shapes=[[1, 32, 768]])
+        ref, rt = orc.run_reference(p["transformed"], p["callable"], args)
+        mod, low = lowering.load(p["transformed"], allow_eager=True)
+        out, t = orc.call_captured(getattr(mod, p["callable"]), args)
+        assert t == rt and torch.equal(out, ref)
