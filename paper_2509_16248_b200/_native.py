@@ -42,6 +42,30 @@ class NativeError(RuntimeError):
     """A libgm_b200 call returned a non-zero status."""
 
 
+LOGRING_SLOTS = 64              # GM_LOGRING_SLOTS
+LOGRING_NO_TEMPLATE = 0xFFFFFFFF
+
+
+class GmRecord(ctypes.Structure):
+    """Mirror of gm_record (include/gm_b200.h)."""
+
+    _fields_ = [
+        ("record_id", ctypes.c_uint32),
+        ("dtype", ctypes.c_int32),
+        ("ndim", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
+        ("step", ctypes.c_uint64),
+        ("shape", ctypes.POINTER(ctypes.c_int64)),
+        ("counts", ctypes.POINTER(ctypes.c_int64)),
+        ("heads", ctypes.POINTER(ctypes.c_int64)),
+        ("data", ctypes.c_void_p),
+        ("bytes", ctypes.c_size_t),
+    ]
+
+
+RECORD_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(GmRecord), ctypes.c_void_p)   # gm_record_cb
+
+
 class InDesc(ctypes.Structure):
     _fields_ = [
         ("ptr", ctypes.c_int64),
@@ -139,6 +163,12 @@ _SIGNATURES = [
       ctypes.c_uint64, ctypes.c_void_p]),
     ("gm_logring_commit", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     ("gm_logring_committed", ctypes.c_uint64, [ctypes.c_void_p]),
+    ("gm_logring_begin_step", ctypes.c_int, [ctypes.c_void_p]),
+    ("gm_logring_capture", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
+      ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p]),
+    ("gm_logring_end_step", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32)]),
+    ("gm_logring_drain", ctypes.c_int, [ctypes.c_void_p, RECORD_CB, ctypes.c_void_p]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]

@@ -24,6 +24,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <cstdint>
 
 #include "../../include/gm_b200.h"
 #include "gm_region.cuh"
@@ -110,6 +111,14 @@ struct gm_region_s {
   int smem = 0;
 };
 
+// one record of a step template (gm_logring_capture)
+struct GmRecordDesc {
+  uint32_t id;
+  int dtype, ndim;
+  int64_t shape[GM_MAX_DIMS], counts[GM_MAX_DIMS], heads[GM_MAX_DIMS];
+  uint64_t offset, bytes;
+};
+
 struct gm_logring_s {
   void* host = nullptr;             // pinned, mapped ring
   void* dev = nullptr;              // device alias of `host`
@@ -117,6 +126,14 @@ struct gm_logring_s {
   unsigned long long* dstep = nullptr;       // device step counter
   volatile unsigned long long* hcommit = nullptr;  // mapped: committed steps
   unsigned long long* dcommit = nullptr;     // device alias of hcommit
+  // record-level API: GM_LOGRING_SLOTS slots of slot_bytes, each starting
+  // with a GM_LOGRING_HEADER-byte header the step commit writes
+  uint64_t slot_bytes = 0;
+  std::vector<std::vector<GmRecordDesc>> templates;  // template id -> records
+  std::vector<GmRecordDesc> open;                    // the step being captured
+  bool step_open = false;
+  uint64_t cursor = GM_LOGRING_HEADER;
+  uint64_t drained = 0;                              // steps delivered by gm_logring_drain
 };
 
 // ===========================================================================
@@ -227,6 +244,29 @@ __global__ void gm_logring_gather_kernel(const __grid_constant__ GatherArgs A) {
       default: ((unsigned long long*)dst)[t] = *(const unsigned long long*)s; break;
     }
   }
+}
+
+// Record-level step commit: write the slot header {template id, record
+// count, 1-based step number} behind the step's gathers, then advance the
+// device slot counter and its mapped host mirror.  System-scope fences order
+// the gathered data and the header before the counter the drain polls.
+struct GmSlotHeader {
+  unsigned long long step;
+  unsigned template_id, n_records;
+};
+
+__global__ void gm_logring_commit_step_kernel(unsigned long long* dstep, unsigned long long* dcommit, char* ring_dev,
+                                              unsigned long long slot_bytes, unsigned long long n_slots,
+                                              unsigned template_id, unsigned n_records) {
+  const unsigned long long s = *dstep;
+  GmSlotHeader* h = (GmSlotHeader*)(ring_dev + (s % n_slots) * slot_bytes);
+  h->template_id = template_id;
+  h->n_records = n_records;
+  __threadfence_system();
+  *(volatile unsigned long long*)&h->step = s + 1;
+  *dstep = s + 1;
+  __threadfence_system();
+  *(volatile unsigned long long*)dcommit = s + 1;
 }
 
 // Advance the slot counter after a step's gathers (stream ordered).  The
@@ -960,6 +1000,7 @@ int gm_logring_open(size_t bytes, gm_logring* out) {
   GM_CUDA(cudaMalloc((void**)&r->dstep, 64));
   GM_CUDA(cudaMemset(r->dstep, 0, 64));
   GM_CUDA(cudaDeviceSynchronize());
+  r->slot_bytes = (bytes / GM_LOGRING_SLOTS) & ~(uint64_t)15;
   *out = r;
   return GM_OK;
 }
@@ -1116,6 +1157,120 @@ int gm_unique_sum32(const float* x, int64_t n, float* out, void* scratch, size_t
   gm_sum_partials_kernel<<<1, 1024, 0, s>>>(partials, grid, out);
   GM_CUDA(cudaGetLastError());
   return GM_OK;
+}
+
+// ---- record-level API ------------------------------------------------------
+int gm_logring_begin_step(gm_logring r) {
+  if (!r) return fail(GM_E_INVALID, "gm_logring_begin_step: null ring");
+  if (r->step_open) return fail(GM_E_INVALID, "gm_logring_begin_step: a step is already open");
+  r->step_open = true;
+  r->open.clear();
+  r->cursor = GM_LOGRING_HEADER;
+  return GM_OK;
+}
+
+int gm_logring_capture(gm_logring r, const void* dev_src, const int64_t* shape, const int64_t* stride, int ndim,
+                       int dtype, uint32_t record_id, void* stream) {
+  if (!r || !dev_src || ndim < 0 || ndim > GM_MAX_DIMS || (ndim && (!shape || !stride)))
+    return fail(GM_E_INVALID, "gm_logring_capture: bad argument");
+  if (!r->step_open) return fail(GM_E_INVALID, "gm_logring_capture: no open step (gm_logring_begin_step)");
+  const int es = esize_of(dtype);
+  if (es <= 0) return fail(GM_E_INVALID, "gm_logring_capture: dtype %d", dtype);
+  // torch._tensor_str: numel > threshold (1000) -> edgeitems (3) per side of
+  // every dim longer than 2 * edgeitems
+  int64_t numel = 1;
+  for (int d = 0; d < ndim; ++d) numel *= shape[d];
+  const bool summarize = numel > 1000;
+  GmRecordDesc rec;
+  memset(&rec, 0, sizeof(rec));  // zero padding: templates are compared with memcmp
+  rec.id = record_id;
+  rec.dtype = dtype;
+  rec.ndim = ndim;
+  int64_t total = 1, hl[2 * GM_MAX_DIMS + 2];
+  for (int d = 0; d < ndim; ++d) {
+    rec.shape[d] = shape[d];
+    const bool cut = summarize && shape[d] > 6;
+    rec.counts[d] = cut ? 6 : shape[d];
+    rec.heads[d] = cut ? 3 : shape[d];
+    hl[2 * d] = rec.heads[d];
+    hl[2 * d + 1] = shape[d];
+    total *= rec.counts[d];
+  }
+  rec.offset = (r->cursor + 15) & ~(uint64_t)15;
+  rec.bytes = (uint64_t)total * es;
+  if (rec.offset + rec.bytes > r->slot_bytes)
+    return fail(GM_E_RING_FULL, "gm_logring_capture: step records exceed the %llu-byte slot",
+                (unsigned long long)r->slot_bytes);
+  if (total > 0) {
+    int rc = gm_logring_gather(r, dev_src, dtype, ndim, stride, rec.counts, hl, r->slot_bytes, GM_LOGRING_SLOTS,
+                               rec.offset, stream);
+    if (rc) return rc;
+  }
+  r->cursor = rec.offset + rec.bytes;
+  r->open.push_back(rec);
+  return GM_OK;
+}
+
+int gm_logring_end_step(gm_logring r, void* stream, uint32_t* template_id) {
+  if (!r || !template_id) return fail(GM_E_INVALID, "gm_logring_end_step: bad argument");
+  if (!r->step_open) return fail(GM_E_INVALID, "gm_logring_end_step: no open step");
+  r->step_open = false;
+  if (r->open.empty()) {
+    *template_id = GM_LOGRING_NO_TEMPLATE;
+    return GM_OK;
+  }
+  // an eager forward re-registers the same template every step: reuse it
+  unsigned tid = (unsigned)r->templates.size();
+  for (size_t back = 0; back < 16 && back < r->templates.size(); ++back) {
+    const size_t i = r->templates.size() - 1 - back;
+    const auto& t = r->templates[i];
+    if (t.size() == r->open.size() && !memcmp(t.data(), r->open.data(), t.size() * sizeof(GmRecordDesc))) {
+      tid = (unsigned)i;
+      break;
+    }
+  }
+  if (tid == r->templates.size()) r->templates.push_back(r->open);
+  gm_logring_commit_step_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(
+      r->dstep, r->dcommit, (char*)r->dev, r->slot_bytes, GM_LOGRING_SLOTS, tid, (unsigned)r->open.size());
+  GM_CUDA(cudaGetLastError());
+  r->open.clear();
+  *template_id = tid;
+  return GM_OK;
+}
+
+int gm_logring_drain(gm_logring r, gm_record_cb cb, void* user) {
+  if (!r || !cb) return fail(GM_E_INVALID, "gm_logring_drain: bad argument");
+  const unsigned long long committed = *r->hcommit;
+  int steps = 0;
+  while (r->drained < committed) {
+    const uint64_t s = r->drained + 1;
+    const char* slot = (const char*)r->host + ((s - 1) % GM_LOGRING_SLOTS) * r->slot_bytes;
+    const GmSlotHeader* h = (const GmSlotHeader*)slot;
+    if (*(volatile const unsigned long long*)&h->step != s)
+      return fail(GM_E_RING_FULL, "gm_logring_drain: step %llu was overwritten before it was drained "
+                  "(more than %d steps in flight)", (unsigned long long)s, GM_LOGRING_SLOTS);
+    if (h->template_id >= r->templates.size())
+      return fail(GM_E_INVALID, "gm_logring_drain: unknown template %u", h->template_id);
+    for (const GmRecordDesc& d : r->templates[h->template_id]) {
+      gm_record rec;
+      rec.record_id = d.id;
+      rec.dtype = d.dtype;
+      rec.ndim = d.ndim;
+      rec.pad = 0;
+      rec.step = s;
+      rec.shape = d.shape;
+      rec.counts = d.counts;
+      rec.heads = d.heads;
+      rec.data = slot + d.offset;
+      rec.bytes = d.bytes;
+      const int rc = cb(&rec, user);
+      if (rc) return fail(GM_E_INVALID, "gm_logring_drain: callback returned %d at record %u of step %llu", rc,
+                          d.id, (unsigned long long)s);
+    }
+    r->drained = s;
+    ++steps;
+  }
+  return steps;
 }
 
 int gm_logring_commit(gm_logring r, void* stream) {

@@ -85,27 +85,81 @@ except Exception:  # pragma: no cover - an older / newer Dynamo without the regi
     pass
 
 
+_RED = ("sum", "mean", "max", "min", "norm")
+_CMP = (">", ">=", "<", "<=")
+_bs_programs: dict = {}
+
+
+def _branch_select_program(red: int, cmp: int):
+    """The canonical predicated block as a transformed program (the shape
+    transform.py:359-376 emits), lowered once per (red, cmp) into one fused
+    region: the same codegen and kernels as every other region, any fusable
+    dtype, and barrier scratch per (stream, graph) — nothing allocated or
+    zeroed per call."""
+    key = (red, cmp)
+    if key not in _bs_programs:
+        text = ("import torch\n\ndef branch_select(x, thr, a1, b1, a2, b2):\n"
+                f"    __gm_pred_0 = x.{_RED[red]}() {_CMP[cmp]} thr\n"
+                "    __gm_then_y_0 = x * a1 + b1\n    __gm_else_y_0 = x * a2 + b2\n"
+                "    y = torch.where(__gm_pred_0, __gm_then_y_0, __gm_else_y_0)\n    return y\n")
+        mod, low = load(text)
+        _bs_programs[key] = (mod.branch_select, low)
+    return _bs_programs[key]
+
+
 @torch.library.custom_op("gm::branch_select", mutates_args=())
 def branch_select(x: torch.Tensor, red: int, cmp: int, thr: float, a1: float, b1: float, a2: float,
                   b2: float) -> torch.Tensor:
-    """`torch.where(x.<red>() <cmp> thr, a1*x + b1, a2*x + b2)` for an fp32
-    CUDA tensor in one launch (red: 0 sum, 1 mean, 2 max, 3 min, 4 norm;
-    cmp: 0 >, 1 >=, 2 <, 3 <=) — transform.py:359-376 on the phi4 block shape.
-    Raises NativeError without the library; there is no fallback."""
-    if not (x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()):
-        raise ValueError("gm::branch_select takes a contiguous fp32 CUDA tensor")
-    lib = nat.lib()
-    nat.init(x.device.index if x.device.index is not None else torch.cuda.current_device())
-    out = torch.empty_like(x)
-    scratch = torch.zeros(lib.gm_branch_select_scratch_bytes(), dtype=torch.uint8, device=x.device)
-    nat.count_launches()
-    nat.check(lib.gm_branch_select_f32(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), x.numel(),
-                                       red, cmp, thr, a1, b1, a2, b2, ctypes.c_void_p(scratch.data_ptr()), None,
-                                       ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
-              "gm_branch_select_f32")
-    return out
+    """`torch.where(x.<red>() <cmp> thr, a1*x + b1, a2*x + b2)` for a CUDA
+    tensor of any fusable dtype (fp32 / bf16 / fp16) in ONE fused region
+    launch (red: 0 sum, 1 mean, 2 max, 3 min, 4 norm; cmp: 0 >, 1 >=, 2 <,
+    3 <=) — transform.py:359-376 on the phi4 block shape.  Raises for CPU
+    tensors (no fallback) and NativeError without the library."""
+    if not x.is_cuda:
+        raise ValueError("gm::branch_select takes a CUDA tensor (the B200 path has no CPU fallback)")
+    if not (0 <= red < len(_RED) and 0 <= cmp < len(_CMP)):
+        raise ValueError("gm::branch_select: red in 0..4, cmp in 0..3")
+    fn, _ = _branch_select_program(red, cmp)
+    return fn(x, float(thr), float(a1), float(b1), float(a2), float(b2))
 
 
 @branch_select.register_fake
 def _(x, red, cmp, thr, a1, b1, a2, b2):
     return torch.empty_like(x)
+
+
+@torch.library.custom_op("gm::log_capture", mutates_args=())
+def log_capture(t: torch.Tensor, record_id: int) -> None:
+    """Capture the elements of `t` its repr would print into the device log
+    ring as record `record_id` (gm_logring_capture): one gather kernel, no
+    device-to-host read inside the forward; the drain delivers the record to
+    the handler registered with logring.on_record(record_id, fn).  Inside a
+    B200Executor forward the record joins that forward's step (and its CUDA
+    graph); a bare call opens and commits a one-record step.  Registered as
+    an ORDERED effectful op, so a Dynamo-traced graph keeps it in place
+    (replaces the replay of a deferred print, transform.py:707-708)."""
+    if not t.is_cuda:
+        raise ValueError("gm::log_capture takes a CUDA tensor")
+    from . import logring
+
+    ring = logring.active_ring()
+    if ring is not None and ring.active:
+        ring.capture(t, record_id)
+        return
+    ring = logring.ring_for(t.device)
+    ring.begin()
+    ring.capture(t, record_id)
+    ring.enqueue(ring.end())
+
+
+@log_capture.register_fake
+def _(t, record_id):
+    return None
+
+
+try:
+    from torch._higher_order_ops.effects import _EffectType, _register_effectful_op
+
+    _register_effectful_op(torch.ops.gm.log_capture.default, _EffectType.ORDERED)
+except Exception:  # pragma: no cover - API moved
+    pass

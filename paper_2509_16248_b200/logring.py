@@ -50,6 +50,9 @@ _DT = {
 }
 
 
+_CODE_DT = {code: dt for dt, (code, _) in _DT.items()}
+
+
 def summary_plan(shape: tuple[int, ...]) -> tuple[list[int], list[int]]:
     """(count, head) per dim of the elements torch's repr reads."""
     numel = math.prod(shape)
@@ -67,11 +70,11 @@ def summary_plan(shape: tuple[int, ...]) -> tuple[list[int], list[int]]:
 
 @dataclass
 class TensorRef:
-    offset: int
+    """A tensor argument of a deferred call: captured as record `record_id`
+    (gm_logring_capture); rebuilt from the drained record."""
+    record_id: int
     dtype: torch.dtype
     shape: tuple
-    counts: list
-    heads: list
     grad_fn: str | None
     requires_grad: bool
 
@@ -80,7 +83,8 @@ class TensorRef:
 class StepTemplate:
     calls: list = field(default_factory=list)   # (site, callee, [arg | TensorRef])
     discard: bool = False
-    gathers: int = 0                            # device gathers launched by the step
+    gathers: int = 0                            # records captured by the step
+    template_id: int | None = None              # gm_logring_end_step's id (None: no device work)
 
 
 class _TensorText:
@@ -124,69 +128,82 @@ class _TensorText:
         return format(str(self), spec)
 
 
+RECORD_CB = nat.RECORD_CB
+_record_ids = iter(range(1, 1 << 32))
+# torch.ops.gm.log_capture records: record id -> handler(tensor)
+_record_handlers: dict[int, object] = {}
+
+
+def on_record(record_id: int, handler) -> None:
+    """Deliver every drained record `record_id` (a tensor captured with
+    torch.ops.gm.log_capture) to `handler(tensor)`."""
+    _record_handlers[int(record_id)] = handler
+
+
 class LogRing:
-    """Pinned, device-mapped ring for one device."""
+    """Pinned, device-mapped ring for one device, on the record-level C API:
+    gm_logring_begin_step / gm_logring_capture (one gather per tensor
+    argument) / gm_logring_end_step (slot header + counter) on the producer
+    side, gm_logring_drain (a C callback per record, in commit order) on the
+    consumer side.  The drain never synchronises a stream: completion is the
+    committed-step counter in mapped host memory."""
 
     def __init__(self, device: torch.device, slot_bytes: int = 1 << 20, n_slots: int = 64):
         self.device = device
+        self.n_slots = nat.LOGRING_SLOTS
         self.slot_bytes = slot_bytes
-        self.n_slots = n_slots
         nat.init(device.index)
         h = ctypes.c_void_p()
-        nat.check(nat.lib().gm_logring_open(slot_bytes * n_slots, ctypes.byref(h)), "gm_logring_open")
+        nat.check(nat.lib().gm_logring_open(slot_bytes * self.n_slots, ctypes.byref(h)), "gm_logring_open")
         self.handle = h
-        self.host = nat.lib().gm_logring_host_ptr(h)
         self.lock = threading.RLock()
-        self.pending: deque = deque()        # (step_number, template)
-        self.launched = 0                    # steps queued for the drain
+        self.pending: deque = deque()        # launched steps with deferred calls, in launch order
+        self.arrived: deque = deque()        # drained steps: {record_id: (dtype, shape, counts, heads, bytes)}
+        self.launched = 0
         self.drained = 0
-        self.gather_steps = 0                # steps that advanced the device slot counter
+        self.gather_steps = 0                # steps that commit on the device
         self.drained_gather_steps = 0
         self._active: StepTemplate | None = None
-        self._cursor = 0
         self.gathers = 0
         self._thread = None
         self._stop = False
+        self._cb = RECORD_CB(self._on_record)
+        self._current: dict | None = None
+        self._current_step = None
 
     # -- producer side (forward) ------------------------------------------------
     def begin(self, discard: bool = False) -> None:
         if self._active is not None:
             raise RuntimeError("log ring step already active")
+        nat.check(nat.lib().gm_logring_begin_step(self.handle), "gm_logring_begin_step")
         self._active = StepTemplate(discard=discard)
-        self._cursor = 0
+
+    def capture(self, t: torch.Tensor, record_id: int) -> None:
+        """gm_logring_capture of one CUDA tensor into the open step."""
+        if t.dtype not in _DT:
+            raise TypeError(f"log ring: unsupported dtype {t.dtype}")
+        code, _ = _DT[t.dtype]
+        nd = t.dim()
+        shape = (ctypes.c_int64 * max(1, nd))(*t.shape)
+        stride = (ctypes.c_int64 * max(1, nd))(*t.stride())
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        nat.check(nat.lib().gm_logring_capture(self.handle, ctypes.c_void_p(t.data_ptr()), shape, stride, nd, code,
+                                               int(record_id), ctypes.c_void_p(stream)), "gm_logring_capture")
+        nat.count_launches()
+        self.gathers += 1
+        self._active.gathers += 1
 
     def record(self, site: int, callee, args: tuple) -> None:
         tmpl = self._active
         out = []
-        stream = torch.cuda.current_stream(self.device).cuda_stream
         for a in args:
             if torch.is_tensor(a) and a.device.type == "cuda":
-                if a.dtype not in _DT:
-                    raise TypeError(f"log ring: unsupported dtype {a.dtype}")
-                code, es = _DT[a.dtype]
-                shape = tuple(a.shape)
-                counts, heads = summary_plan(shape)
-                nbytes = math.prod(counts) * es
-                off = (self._cursor + 15) // 16 * 16
-                if off + nbytes > self.slot_bytes:
-                    raise nat.NativeError("log ring slot overflow: raise slot_bytes")
-                self._cursor = off + nbytes
-                nd = len(shape)
-                st = (ctypes.c_int64 * max(1, nd))(*a.stride())
-                ct = (ctypes.c_int64 * max(1, nd))(*counts)
-                hl = (ctypes.c_int64 * max(2, 2 * nd))(*[v for h, s in zip(heads, shape) for v in (h, s)])
-                nat.check(
-                    nat.lib().gm_logring_gather(self.handle, ctypes.c_void_p(a.data_ptr()), code, nd, st, ct, hl,
-                                                self.slot_bytes, self.n_slots, off, ctypes.c_void_p(stream)),
-                    "gm_logring_gather",
-                )
-                nat.count_launches()
-                self.gathers += 1
-                tmpl.gathers += 1
+                rid = next(_record_ids)
+                self.capture(a, rid)
                 gf = a.grad_fn
                 # gemm.py records the grad_fn name the eager op would have had
                 name = getattr(a, "_gm_grad_fn", None) or (type(gf).__name__ if gf is not None else None)
-                out.append(TensorRef(off, a.dtype, shape, counts, heads, name, a.requires_grad))
+                out.append(TensorRef(rid, a.dtype, tuple(a.shape), name, a.requires_grad))
             elif torch.is_tensor(a):
                 out.append(a.detach().clone() if not a.requires_grad else a)
             else:
@@ -194,14 +211,17 @@ class LogRing:
         tmpl.calls.append((site, callee, out))
 
     def end(self) -> StepTemplate:
-        """Close the step.  Only a step that gathered tensors advances the
-        device slot counter (gm_logring_commit); a step whose deferred calls
-        carry host constants only launches nothing at all."""
+        """Close the step (gm_logring_end_step): a step with records launches
+        the commit kernel; a step whose deferred calls carry host constants
+        only launches nothing at all."""
         tmpl = self._active
         self._active = None
-        if tmpl.gathers:
-            stream = torch.cuda.current_stream(self.device).cuda_stream
-            nat.check(nat.lib().gm_logring_commit(self.handle, ctypes.c_void_p(stream)), "gm_logring_commit")
+        tid = ctypes.c_uint32(0)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        nat.check(nat.lib().gm_logring_end_step(self.handle, ctypes.c_void_p(stream), ctypes.byref(tid)),
+                  "gm_logring_end_step")
+        if tid.value != nat.LOGRING_NO_TEMPLATE:
+            tmpl.template_id = tid.value
             nat.count_launches()
         return tmpl
 
@@ -211,72 +231,113 @@ class LogRing:
 
     def enqueue(self, tmpl: StepTemplate) -> None:
         """Register one launched step (eager or graph replay), in stream
-        order.  Completion is a CUDA event recorded behind the step (polled by
-        the drain, never waited on by the forward); steps with nothing to
-        deliver are not queued."""
-        if not tmpl.calls:
+        order.  Steps with records commit on the device; steps without
+        records and without deferred calls are not queued."""
+        if not tmpl.calls and tmpl.template_id is None:
             return
         with self.lock:
-            slot = None
-            if tmpl.gathers:
-                # back-pressure: never run more than n_slots-1 gather steps ahead
+            if tmpl.template_id is not None:
+                # back-pressure: never run more than n_slots-1 committing steps ahead
                 while self.gather_steps - self.drained_gather_steps >= self.n_slots - 1:
                     self._drain_one(block=True)
-                slot = self.gather_steps % self.n_slots
                 self.gather_steps += 1
-            ev = None
-            if tmpl.gathers:
-                ev = torch.cuda.Event()
-                ev.record(torch.cuda.current_stream(self.device))
             self.launched += 1
-            self.pending.append((self.launched, tmpl, ev, slot))
+            self.pending.append((self.launched, tmpl))
 
     # -- consumer side (host) -------------------------------------------------------
     def committed(self) -> int:
         return int(nat.lib().gm_logring_committed(self.handle))
 
-    def _rebuild(self, ref: TensorRef, slot: int):
-        code, es = _DT[ref.dtype]
-        n = math.prod(ref.counts)
-        addr = self.host + slot * self.slot_bytes + ref.offset
-        raw = (ctypes.c_uint8 * (n * es)).from_address(addr)
-        block = torch.frombuffer(bytearray(raw), dtype=ref.dtype).reshape(ref.counts) if n else \
-            torch.empty(ref.counts, dtype=ref.dtype)
-        if list(ref.counts) == list(ref.shape):
+    def _on_record(self, rec_p, _user) -> int:
+        try:
+            rec = rec_p.contents
+            if rec.step != self._current_step:
+                self._current = {}
+                self._current_step = rec.step
+                self.arrived.append(self._current)
+            nd = rec.ndim
+            self._current[rec.record_id] = (rec.dtype, tuple(rec.shape[i] for i in range(nd)),
+                                            tuple(rec.counts[i] for i in range(nd)),
+                                            tuple(rec.heads[i] for i in range(nd)),
+                                            ctypes.string_at(rec.data, rec.bytes) if rec.bytes else b"")
+            return 0
+        except Exception:   # never raise through the C callback
+            return 1
+
+    def _poll(self) -> None:
+        rc = nat.lib().gm_logring_drain(self.handle, self._cb, None)
+        if rc < 0:
+            nat.check(rc, "gm_logring_drain")
+
+    @staticmethod
+    def _rebuild_record(raw, ref: TensorRef | None = None):
+        code, shape, counts, heads, data = raw
+        dtype = _CODE_DT[code]
+        n = math.prod(counts)
+        block = torch.frombuffer(bytearray(data), dtype=dtype).reshape(counts) if n else torch.empty(counts,
+                                                                                                      dtype=dtype)
+        if list(counts) == list(shape):
             full = block.clone()
         else:
-            full = torch.empty(ref.shape, dtype=ref.dtype)
+            full = torch.empty(shape, dtype=dtype)
             idx = []
-            nd = len(ref.shape)
-            for d, (c, h, s) in enumerate(zip(ref.counts, ref.heads, ref.shape)):
-                ix = torch.tensor([k if k < h else s - c + k for k in range(c)], dtype=torch.long)
+            nd = len(shape)
+            for d, (c, h, sz) in enumerate(zip(counts, heads, shape)):
+                ix = torch.tensor([k if k < h else sz - c + k for k in range(c)], dtype=torch.long)
                 view = [1] * nd
                 view[d] = c
                 idx.append(ix.view(view))
             full[tuple(idx)] = block
-        if ref.grad_fn is not None or ref.requires_grad:
+        if ref is not None and (ref.grad_fn is not None or ref.requires_grad):
             return _TensorText(full, ref.grad_fn, ref.requires_grad)
         return full
 
     def _drain_one(self, block: bool) -> bool:
         with self.lock:
             if not self.pending:
+                # records of steps launched outside a step template
+                # (torch.ops.gm.log_capture in a bare call) still arrive
+                self._poll()
+                self._deliver_orphans()
                 return False
-            step, tmpl, ev, slot = self.pending[0]
-            if ev is not None:
-                while not ev.query():
+            step, tmpl = self.pending[0]
+            raw = None
+            if tmpl.template_id is not None:
+                while True:
+                    if not self.arrived:
+                        self._poll()
+                    if self.arrived:
+                        raw = self.arrived.popleft()
+                        break
                     if not block:
                         return False
                     time.sleep(20e-6)
             self.pending.popleft()
+            if raw is not None:
+                self.drained_gather_steps += 1
+                refs = {}
+                for _site, _callee, args in tmpl.calls:
+                    for a in args:
+                        if isinstance(a, TensorRef):
+                            refs[a.record_id] = a
+                for rid, rec in raw.items():
+                    if rid not in refs and rid in _record_handlers and not tmpl.discard:
+                        _record_handlers[rid](self._rebuild_record(rec))
             if not tmpl.discard:
                 for _site, callee, args in tmpl.calls:
-                    real = [self._rebuild(a, slot) if isinstance(a, TensorRef) else a for a in args]
+                    real = [self._rebuild_record(raw[a.record_id], a) if isinstance(a, TensorRef) else a
+                            for a in args]
                     callee(*real)
-            if slot is not None:
-                self.drained_gather_steps += 1
             self.drained = step
             return True
+
+    def _deliver_orphans(self) -> None:
+        while self.arrived:
+            raw = self.arrived.popleft()
+            for rid, rec in raw.items():
+                h = _record_handlers.get(rid)
+                if h is not None:
+                    h(self._rebuild_record(rec))
 
     def flush(self) -> None:
         """Drain every launched step (waits for their commits, in order)."""

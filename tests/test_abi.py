@@ -56,3 +56,19 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(nat, "LIB_PATH", str(tmp_path / "libgm_b200.so"))
     with pytest.raises(nat.NativeError, match="no fallback"):
         nat.lib()
+
+
+def test_record_api_declared_and_mirrored():
+    """the record-level log-ring entry points and the
+    gm_record layout the drain callback receives."""
+    declared = _declared()
+    assert {"gm_logring_begin_step", "gm_logring_capture", "gm_logring_end_step", "gm_logring_drain",
+            "gm_gemm_run", "gm_select_copy", "gm_stream_capture_id", "gm_status_page"} <= declared
+    # gm_record: u32, i32 x3, u64, 3 pointers, const void*, size_t
+    assert ctypes.sizeof(nat.GmRecord) == 4 * 4 + 8 + 3 * 8 + 8 + 8
+    text = open(HEADER).read()
+    assert "#define GM_LOGRING_SLOTS 64" in text and nat.LOGRING_SLOTS == 64
+    lib = nat.lib()
+    # without a ring or an open step the record API refuses with a status code
+    assert lib.gm_logring_begin_step(None) == -1
+    assert lib.gm_logring_drain(None, nat.RECORD_CB(lambda r, u: 0), None) == -1

@@ -51,24 +51,64 @@ def test_backend_on_b200(programs, name, dtype):
     compiled = torch.compile(fn, backend="gm_b200")
     from paper_2509_16248_b200 import _native as nat
 
+    from parity import has_dense_contraction, torch_cuda_reference
+
     for spec in prog["inputs"]:
         args = make_args(spec["args"], spec["seed"], dtype, shapes)
         ref, _ = orc.run_reference(prog["transformed"], prog["callable"], args, dtype)
+        noise = torch_cuda_reference(prog["transformed"], prog["callable"], args, dtype) \
+            if has_dense_contraction(prog["transformed"]) else None
         c0 = nat.launch_count
-        out = compiled(*[a.cuda() for a in args])
-        assert_parity(out, ref, dtype, what=name)
+        with torch.no_grad():
+            out = compiled(*[a.cuda() for a in args])
+        assert_parity(out, ref, dtype, what=name, noise=noise)
         assert nat.launch_count > c0 or spec is not prog["inputs"][0], "no fused region launched"
 
 
 @pytest.mark.gpu
-def test_branch_select_custom_op():
-    """torch.ops.gm.branch_select (the precompiled phi4 block) in eager and
-    under torch.compile (fake implementation for tracing)."""
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16], ids=["fp32", "bf16", "fp16"])
+def test_branch_select_custom_op(dtype):
+    """torch.ops.gm.branch_select (the canonical phi4 block as one fused
+    region, any fusable dtype) in eager and under torch.compile (fake
+    implementation for tracing); CPU tensors raise."""
     torch.manual_seed(0)
-    x = torch.randn(8, 1024, 768, device="cuda") + 0.01
-    ref = torch.where(x.sum() > 0, x * 1.0 + 1.0, x * 1.0 - 1.0)
-    out = torch.ops.gm.branch_select(x, 0, 0, 0.0, 1.0, 1.0, 1.0, -1.0)
-    assert torch.equal(out, ref)
-    f = torch.compile(lambda t: torch.ops.gm.branch_select(t, 0, 0, 0.0, 1.0, 1.0, 1.0, -1.0) * 2, backend="gm_b200",
+    x = (torch.randn(8, 1024, 768) + 0.01).to(dtype)
+    ref = torch.where(x.sum() > 0, x * 1.5 + 1.0, x * 0.5 - 1.0)       # torch CPU eager
+    out = torch.ops.gm.branch_select(x.cuda(), 0, 0, 0.0, 1.5, 1.0, 0.5, -1.0)
+    assert_parity(out, ref, dtype, what="branch_select")
+    for red, cmp in ((1, 1), (2, 2), (3, 3), (4, 0)):
+        got = torch.ops.gm.branch_select(x.cuda(), red, cmp, 0.25, 2.0, 0.0, 1.0, 0.0)
+        stat = [x.sum, x.mean, x.max, x.min, x.norm][red]()
+        pred = [stat > 0.25, stat >= 0.25, stat < 0.25, stat <= 0.25][cmp]
+        assert_parity(got, torch.where(pred, x * 2.0 + 0.0, x * 1.0 + 0.0), dtype, what=f"red{red} cmp{cmp}")
+    f = torch.compile(lambda t: torch.ops.gm.branch_select(t, 0, 0, 0.0, 1.5, 1.0, 0.5, -1.0) * 2, backend="gm_b200",
                       fullgraph=True)
-    assert torch.equal(f(x), ref * 2)
+    with torch.no_grad():
+        assert_parity(f(x.cuda()), ref * 2, dtype, what="compiled")
+    with pytest.raises(ValueError):
+        torch.ops.gm.branch_select(x, 0, 0, 0.0, 1.0, 1.0, 1.0, -1.0)
+
+
+@pytest.mark.gpu
+def test_backend_returns_fresh_outputs_and_keeps_autograd():
+    """torch.compile semantics: a kept output is not overwritten
+    by the next call, and with grad enabled on inputs that require grad the
+    call runs the FX graph itself, so gradients flow."""
+    torch._dynamo.reset()
+
+    def f(x):
+        __gm_pred_0 = x.sum() > 0
+        y = torch.where(__gm_pred_0, x * 2, x - 1)
+        return y
+
+    c = torch.compile(f, backend="gm_b200")
+    with torch.no_grad():
+        a = torch.ones(1024, device="cuda")
+        y1 = c(a)
+        y2 = c(-a)
+    assert torch.equal(y1, torch.full((1024,), 2.0, device="cuda"))
+    assert torch.equal(y2, torch.full((1024,), -2.0, device="cuda"))
+    x = torch.ones(1024, device="cuda", requires_grad=True)
+    y = c(x)
+    y.sum().backward()
+    assert torch.equal(x.grad, torch.full((1024,), 2.0, device="cuda"))
