@@ -348,16 +348,26 @@ def profile_syncs(ex, x_dev) -> dict:
     import torch
     from torch.profiler import ProfilerActivity, profile
 
+    from torch.profiler import record_function
+
     ex(*x_dev)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-        ex(*x_dev)
+        with record_function("gm_forward"):
+            ex(*x_dev)
     torch.cuda.synchronize()
-    names = [e.name for e in prof.events()]
-    syncs = sum(1 for n in names if n in ("cudaStreamSynchronize", "cudaDeviceSynchronize", "cudaEventSynchronize"))
-    d2h = sum(1 for n in names if "DtoH" in n or "Device -> Pinned" in n or "Device -> Pageable" in n)
+    evs = list(prof.events())
+    fwd = [e for e in evs if e.name == "gm_forward"]
+    lo, hi = fwd[0].time_range.start, fwd[0].time_range.end
+    inside = [e for e in evs if e.device_type == torch.autograd.DeviceType.CPU
+              and lo <= e.time_range.start <= hi]
+    syncs = sum(1 for e in inside
+                if e.name in ("cudaStreamSynchronize", "cudaDeviceSynchronize", "cudaEventSynchronize"))
+    d2h = sum(1 for e in evs if ("DtoH" in e.name or "Device -> Pinned" in e.name or "Device -> Pageable" in e.name))
     return {"cuda_syncs": syncs, "d2h_copies": d2h, "how": "torch.profiler over one B200Executor call "
-            "(device inputs): cudaStream/Device/EventSynchronize calls and DtoH memcpy events"}
+            "(device inputs): cudaStream/Device/EventSynchronize calls whose CPU start lies inside the "
+            "forward's record_function range (the profiler's own stop-time cudaDeviceSynchronize is "
+            "outside it), and DtoH memcpy events anywhere in the trace"}
 
 
 def main():

@@ -538,6 +538,11 @@ class Plan:
         elif op in ("maximum", "minimum"):
             fn = "gm::nmax" if op == "maximum" else "gm::nmin"
             body = wrap(f"{fn}({ev(a[0], 0)}, {ev(a[1], 1)})")
+        elif op in ("floordiv", "mod", "fmod"):
+            if not node.dtype.is_floating_point:
+                raise Unsupported(f"{op} on {node.dtype}")
+            fn = {"floordiv": "gm::floordiv", "mod": "gm::pymod", "fmod": "fmodf"}[op]
+            body = wrap(f"{fn}({ev(a[0], 0)}, {ev(a[1], 1)})")
         elif op == "logical_and":
             body = f"((({ev(a[0])}) != 0.f && ({ev(a[1])}) != 0.f) ? 1.f : 0.f)"
         elif op == "logical_or":
@@ -640,6 +645,14 @@ class Plan:
                 e = f"({rcast}({sv(a[0])}) {sym} {rcast}({sv(a[1])}))"
             else:
                 e = f"({sv(a[0])} {sym} {sv(a[1])})"
+            return f"{dst} = {R}({e});" if R else f"{dst} = {e};"
+        if op in ("floordiv", "mod", "fmod"):
+            fn = {"floordiv": "gm::floordiv_t", "mod": "gm::pymod_t", "fmod": "fmod"}[op]
+            if node.kind == "dscalar" and node.dtype == torch.float32:
+                e = f"(double){fn.replace('_t', '')}((float){sv(a[0])}, (float){sv(a[1])})" if op != "fmod" \
+                    else f"(double)fmodf((float){sv(a[0])}, (float){sv(a[1])})"
+            else:
+                e = f"{fn}({sv(a[0])}, {sv(a[1])})" if op == "fmod" else f"{fn}<double>({sv(a[0])}, {sv(a[1])})"
             return f"{dst} = {R}({e});" if R else f"{dst} = {e};"
         if op == "pow":
             e = f"pow({sv(a[0])}, {sv(a[1])})"
@@ -950,8 +963,17 @@ class Plan:
             self._emit_epilogue(w, "    ", miss=False)
             w("    return;")
             w("  }")
-            w("  // misprediction: the exact multi-pass path (inputs re-read)")
+            w("  // misprediction: the exact passes from the first mispredicted level (inputs re-read)")
         for p in range(self.npass):
+            if self.spec:
+                # restart at the first mispredicted level (decisions have
+                # level >= 1, so pass 0 never reruns)
+                if p == 0:
+                    continue
+                w(f"  if (s_miss <= {p}) {{")
+                self._emit_ctx(w, p)
+                w("  }")
+                continue
             if p in self.hoisted and not self.spec:
                 self._emit_hoist_guard(w, p)
                 w(f"  if (!s_hoist{p}) {{  // hoisting guard failed: the exact sweep")
@@ -1126,10 +1148,15 @@ class Plan:
                     for n in self.scalars:
                         if self.avail[n.uid] == p + 1 and n.op not in REDUCE:
                             w("      " + self._scalar_code(n))
-                w("      int miss_ = 0;")
+                # s_miss = the lowest scalar level holding a mispredicted
+                # decision (0: every prediction held).  Passes below it ran
+                # under correct decisions, so their reductions and outputs
+                # are exact and the miss path restarts at that pass.
+                w("      int miss_ = 0x7fffffff;")
                 for j, d in enumerate(self.decisions):
-                    w(f"      miss_ |= ((s_scal[{self.slot[d.uid]}] != 0.0) != (s_pred[{j}] != 0)) ? 1 : 0;")
-                w("      s_miss = miss_;")
+                    w(f"      if ((s_scal[{self.slot[d.uid]}] != 0.0) != (s_pred[{j}] != 0)) "
+                      f"miss_ = min(miss_, {self.avail[d.uid]});")
+                w("      s_miss = miss_ == 0x7fffffff ? 0 : miss_;")
                 w("    }")
                 w("    __syncthreads();")
             else:

@@ -130,6 +130,46 @@ __device__ __forceinline__ float sigmoid(float a) {
   return y;
 }
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
+// Python-style `%` and `//` on floats, as torch's CPU kernels compute them
+// (remainder: fmod, then + b when the signs differ; floor_divide:
+// div_floor_floating — (a - fmod(a, b)) / b, corrected and rounded to an
+// integer value, copysign(0, a / b) for a zero quotient)
+template <typename T>
+__device__ __forceinline__ T pymod_t(T a, T b) {
+  T m = fmod(a, b);
+  if (m != (T)0 && ((b < (T)0) != (m < (T)0))) m += b;
+  return m;
+}
+template <typename T>
+__device__ __forceinline__ T floordiv_t(T a, T b) {
+  if (b == (T)0) return a / b;
+  const T m = fmod(a, b);
+  T d = (a - m) / b;
+  if (m != (T)0 && ((b < (T)0) != (m < (T)0))) d -= (T)1;
+  if (d != (T)0) {
+    T f = floor(d);
+    if (d - f > (T)0.5) f += (T)1;
+    return f;
+  }
+  return copysign((T)0, a / b);
+}
+__device__ __forceinline__ float pymod(float a, float b) {
+  float m = fmodf(a, b);
+  if (m != 0.f && ((b < 0.f) != (m < 0.f))) m = __fadd_rn(m, b);
+  return m;
+}
+__device__ __forceinline__ float floordiv(float a, float b) {
+  if (b == 0.f) return __fdiv_rn(a, b);
+  const float m = fmodf(a, b);
+  float d = __fdiv_rn(__fsub_rn(a, m), b);
+  if (m != 0.f && ((b < 0.f) != (m < 0.f))) d = __fsub_rn(d, 1.f);
+  if (d != 0.f) {
+    float f = floorf(d);
+    if (__fsub_rn(d, f) > 0.5f) f = __fadd_rn(f, 1.f);
+    return f;
+  }
+  return copysignf(0.f, __fdiv_rn(a, b));
+}
 __device__ __forceinline__ float neg(float a) { return -a; }
 __device__ __forceinline__ double dmax(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a > b ? a : b)); }
 __device__ __forceinline__ double dmin(double a, double b) { return (a != a) ? a : ((b != b) ? b : (a < b ? a : b)); }
@@ -586,6 +626,37 @@ __device__ __forceinline__ void store8(const OutDesc& o, i64 e, int nv, const fl
   }
 }
 
+// ---------------------------------------------------------------------------
+// row regions (rowgen.py): a thread group of TPR threads owns one row of the
+// innermost dimension; its vectors start at column (u * TPR + t) * 8, so a
+// vector never crosses a row.  When the row length is not a multiple of 8
+// the vectors are not 16-byte aligned and every lane is accessed alone.
+// ---------------------------------------------------------------------------
+template <int DT>
+__device__ __forceinline__ void load8_elems(const InDesc& d, i64 e, int nv, float (&x)[8]) {
+#pragma unroll
+  for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? Elem<DT>::ld((const void*)d.ptr, e + k) : 0.f;
+}
+template <int DT>
+__device__ __forceinline__ void load8_periodic_elems(const InDesc& d, i64 e, int nv, float (&x)[8]) {
+  const i64 period = d.size[0];
+#pragma unroll
+  for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? Elem<DT>::ld((const void*)d.ptr, (e + k) % period) : 0.f;
+}
+template <int DT>
+__device__ __forceinline__ void store8_elems(const OutDesc& o, i64 e, int nv, const float (&y)[8]) {
+#pragma unroll
+  for (int k = 0; k < GM_VEC; ++k)
+    if (k < nv) Elem<DT>::st((void*)o.ptr, e + k, y[k]);
+}
+template <int DT>
+__device__ __forceinline__ float load_at(const InDesc& d, i64 i) {
+  return Elem<DT>::ld((const void*)d.ptr, i);
+}
+template <int DT>
+__device__ __forceinline__ void store_at(const OutDesc& o, i64 i, float v) {
+  Elem<DT>::st((void*)o.ptr, i, v);
+}
 template <int DT>
 __device__ __forceinline__ void store_scalar(const OutDesc& o, double v) {
   Elem<DT>::st((void*)o.ptr, 0, (float)v);
@@ -699,6 +770,28 @@ __device__ __forceinline__ double red_combine(int op, double a, double b) {
     default: return a + b;
   }
 }
+
+// combine of a row statistic over the TPR threads of a row group: xor
+// shuffles inside a warp, then (TPR > 32) the warps of the group through
+// shared memory in a fixed order.  Every thread of the CTA must call it.
+template <int TPR, int OP>
+__device__ __forceinline__ double row_combine(double v, double* s_rw) {
+  constexpr int W = TPR < 32 ? TPR : 32;
+#pragma unroll
+  for (int off = W / 2; off > 0; off >>= 1) v = red_combine(OP, v, __shfl_xor_sync(0xffffffffu, v, off));
+  if (TPR > 32) {
+    constexpr int G = TPR > 32 ? TPR / 32 : 1;  // warps per row group
+    const int warp = threadIdx.x >> 5, g0 = (warp / G) * G;
+    if ((threadIdx.x & 31) == 0) s_rw[warp] = v;
+    __syncthreads();
+    v = s_rw[g0];
+#pragma unroll
+    for (int i = 1; i < G; ++i) v = red_combine(OP, v, s_rw[g0 + i]);
+    __syncthreads();
+  }
+  return v;
+}
+
 
 __device__ __forceinline__ u64 atom_add_acq_rel64(u64* p, u64 v) {
   u64 old;

@@ -39,9 +39,17 @@ UNARY = {
     "silu", "square", "reciprocal", "logical_not",
 }
 BINARY = {"add", "sub", "mul", "div", "pow", "maximum", "minimum", "gt", "ge", "lt", "le", "eq", "ne",
-          "logical_and", "logical_or"}
+          "logical_and", "logical_or", "floordiv", "mod", "fmod"}
 COMPARE = {"gt", "ge", "lt", "le", "eq", "ne"}
 REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_nonzero", "nzsum", "argmax", "argmin"}
+# Row operators over the innermost dimension (pure_ops.cfg: softmax; the
+# attr_table reductions sum/mean/max/min called with `dim`, transform.py:
+# 265-289 admits any torch.* call in an arm).  They run in the row-region
+# kernel (rowgen.py), one row per thread group, the row held on chip.
+# Node.value = (dim, keepdim) as written; infer() checks dim is the last one.
+ROW_RED = {"row_sum": "sum", "row_mean": "mean", "row_amax": "amax", "row_amin": "amin"}
+ROW_NORM = {"softmax", "log_softmax"}
+ROW_OPS = set(ROW_RED) | ROW_NORM
 # reductions whose result is an integer count/sum: accumulated exactly in fp64
 INT_REDUCE = {"count_nonzero", "nzsum"}
 # `torch.nonzero(m).sum()` lowered to a reduction: the sum over the positions
@@ -68,12 +76,15 @@ _TORCH_FUNCS = {
     "clip": "clamp", "sum": "sum", "mean": "mean", "amax": "amax", "amin": "amin", "prod": "prod",
     "any": "any", "all": "all", "count_nonzero": "count_nonzero", "norm": "norm",
     "argmax": "argmax", "argmin": "argmin", "max": "max", "min": "min",
+    "softmax": "softmax", "log_softmax": "log_softmax",
+    "floor_divide": "floordiv", "remainder": "mod", "fmod": "fmod",
 }
 # Tensor.<name>(...) spellings (pure_ops.cfg plus the attr_table reductions)
 _METHODS = dict(_TORCH_FUNCS)
 _METHODS.update({"clamp_min": "clamp_min", "clamp_max": "clamp_max", "item": ITEM})
 
-_BINOP = {ast.Add: "add", ast.Sub: "sub", ast.Mult: "mul", ast.Div: "div", ast.Pow: "pow"}
+_BINOP = {ast.Add: "add", ast.Sub: "sub", ast.Mult: "mul", ast.Div: "div", ast.Pow: "pow",
+          ast.FloorDiv: "floordiv", ast.Mod: "mod"}
 _CMPOP = {ast.Gt: "gt", ast.GtE: "ge", ast.Lt: "lt", ast.LtE: "le", ast.Eq: "eq", ast.NotEq: "ne"}
 
 
@@ -153,6 +164,50 @@ class Builder:
     def op(self, name: str, *args: Node, value=None) -> Node:
         return self.g.add(Node(name, tuple(args), value=value))
 
+    # -- row operators ------------------------------------------------------------
+    def _const_int(self, e) -> int:
+        """A literal int (possibly negated) from an AST argument or a const node."""
+        if isinstance(e, Node):
+            if e.op == "const" and isinstance(e.value, int) and not isinstance(e.value, bool):
+                return e.value
+            if e.op == "neg" and len(e.args) == 1:
+                return -self._const_int(e.args[0])
+            raise Unsupported("non-constant dim")
+        if isinstance(e, ast.Constant) and isinstance(e.value, int) and not isinstance(e.value, bool):
+            return e.value
+        if isinstance(e, ast.UnaryOp) and isinstance(e.op, ast.USub):
+            return -self._const_int(e.operand)
+        if isinstance(e, (ast.Tuple, ast.List)) and len(e.elts) == 1:
+            return self._const_int(e.elts[0])
+        raise Unsupported("non-constant dim")
+
+    def _dim_arg(self, pos: list, kw: dict, names: tuple) -> int:
+        if pos:
+            return self._const_int(pos[0])
+        for k in names:
+            if k in kw:
+                return self._const_int(kw[k])
+        raise Unsupported("missing dim")
+
+    def _row_reduce(self, name: str, args: list, kw: dict) -> Node:
+        """x.sum(-1, keepdim=True) / x.mean(dim=-1) / x.amax(-1) / torch.sum(x, -1)."""
+        extra = set(kw) - {"dim", "keepdim"}
+        if extra or len(args) > 3:
+            raise Unsupported(f"{name} arguments {sorted(extra)}")
+        dim = self._dim_arg(args[1:2], kw, ("dim",))
+        keep = False
+        if len(args) == 3:
+            kn = args[2]
+            if kn.op != "const" or not isinstance(kn.value, bool):
+                raise Unsupported("non-constant keepdim")
+            keep = kn.value
+        elif "keepdim" in kw:
+            v = kw["keepdim"]
+            if not (isinstance(v, ast.Constant) and isinstance(v.value, bool)):
+                raise Unsupported("non-constant keepdim")
+            keep = v.value
+        return self.op("row_" + name, args[0], value=(dim, keep))
+
     # -- expressions ------------------------------------------------------------
     def expr(self, e: ast.expr) -> Node:
         if isinstance(e, ast.Name):
@@ -211,7 +266,38 @@ class Builder:
             return self.op(name, self.expr(e.left), self.expr(e.comparators[0]))
         if isinstance(e, ast.Call):
             return self.call(e)
+        if isinstance(e, ast.Subscript):
+            return self.subscript(e)
         raise Unsupported(type(e).__name__)
+
+    def subscript(self, e: ast.Subscript) -> Node:
+        """Basic indexing of a value read from the enclosing scope
+        (`x[..., :k]`, `x[:, 0]`, `x[None]`; transform.py:245-254 admits
+        subscripts in arms) is a view: the region reads it as a free value —
+        the subscript is evaluated by the caller when the region is called
+        (no copy, no kernel) and the kernel reads the view's strides.
+        Subscripts of region values, tensor indices and names assigned in the
+        region stay unfused."""
+        chain = attr_chain(e.value)
+        if chain is None or chain[0] in self.env or chain[0] in self.torch_names \
+                or chain[0] in self.functional_names:
+            raise Unsupported("subscript of a region value")
+
+        def basic(x: ast.expr) -> bool:
+            if isinstance(x, ast.Constant):
+                return x.value is None or x.value is Ellipsis or (isinstance(x.value, int)
+                                                                  and not isinstance(x.value, bool))
+            if isinstance(x, ast.UnaryOp) and isinstance(x.op, ast.USub):
+                return basic(x.operand)
+            if isinstance(x, ast.Slice):
+                return all(v is None or basic(v) for v in (x.lower, x.upper, x.step))
+            if isinstance(x, ast.Tuple):
+                return all(basic(v) for v in x.elts)
+            return False
+
+        if not basic(e.slice):
+            raise Unsupported("subscript with a non-constant index")
+        return self.free(ast.unparse(e))
 
     def call(self, c: ast.Call) -> Node:
         func = c.func
@@ -250,9 +336,17 @@ class Builder:
         if name in ("max", "min"):
             if len(args) == 1 and not kw:
                 return self.op("amax" if name == "max" else "amin", args[0])
-            if len(args) == 2 and not kw:
+            if len(args) == 2 and not kw and args[1].op != "const":
                 return self.op("maximum" if name == "max" else "minimum", args[0], args[1])
+            # max(dim) / min(dim) return (values, indices): not a tensor
             raise Unsupported(f"{name} with dim")
+        if name in ("sum", "mean", "amax", "amin") and (len(args) > 1 or kw):
+            return self._row_reduce(name, args, kw)
+        if name in ("softmax", "log_softmax"):
+            dim = self._dim_arg(args[1:], kw, ("dim",))
+            if len(args) > 2:
+                raise Unsupported(f"{name} arguments")
+            return self.op(name, args[0], value=(dim, True))
         if name in REDUCE:
             if len(args) != 1 or kw:
                 raise Unsupported(f"{name} with arguments")
@@ -353,7 +447,22 @@ META_FNS = {
     "argmax": lambda a: a.argmax(),
     "argmin": lambda a: a.argmin(),
     "nzsum": lambda a: torch.zeros((), dtype=torch.int64, device=a.device),
+    "floordiv": lambda a, b: a // b,
+    "mod": lambda a, b: a % b,
+    "fmod": lambda a, b: torch.fmod(a, b),
 }
+
+
+def _meta_row(node: Node, a):
+    """Row operators: torch's own result; the dim must be the innermost."""
+    dim, keep = node.value
+    if not torch.is_tensor(a) or a.dim() == 0:
+        raise Unsupported(f"{node.op} of a scalar")
+    if dim not in (-1, a.dim() - 1):
+        raise Unsupported(f"{node.op} over dim {dim} (only the innermost dim is fused)")
+    if node.op in ROW_NORM:
+        return getattr(torch, node.op)(a, -1)
+    return getattr(a, ROW_RED[node.op])(-1, keepdim=keep)
 
 
 def _meta_bool(op: str, vals):
@@ -419,9 +528,12 @@ def infer(graph: Graph, args: list, needed: list[Node]) -> None:
                     v = _meta_item(vals[0])
                 elif node.op in (BOOL_AND, BOOL_OR, BOOL_NOT):
                     v = _meta_bool(node.op, vals)
+                elif node.op in ROW_OPS:
+                    v = _meta_row(node, vals[0])
                 else:
                     if all(not torch.is_tensor(x) for x in vals) and node.op not in (
                         "add", "sub", "mul", "div", "pow", "neg", "pos", "abs", "gt", "ge", "lt", "le", "eq", "ne",
+                        "floordiv", "mod",
                     ):
                         # torch functions on Python numbers: compute on a 0-d tensor
                         raise Unsupported(f"{node.op} of host scalars")
@@ -474,6 +586,8 @@ def evaluate(roots: list[Node], args: list) -> dict[int, Any]:
                 v = (a[0] is None) == (node.op == IS_NONE)
             elif node.op == NZSUM:
                 v = torch.nonzero(a[0]).sum()
+            elif node.op in ROW_OPS:
+                v = _meta_row(node, a[0])
             else:
                 v = META_FNS[node.op](*a)
         vals[node.uid] = v

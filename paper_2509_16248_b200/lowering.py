@@ -32,7 +32,7 @@ import linecache
 import types
 from dataclasses import dataclass, field
 
-from .ir import Builder, Graph, Unsupported, attr_chain
+from .ir import NZSUM, REDUCE, ROW_OPS, Builder, Graph, Unsupported, attr_chain
 from .region import Region
 
 GM_RT = "__gm_rt__"  # dunder suffix: exempt from private-name mangling in class bodies
@@ -125,6 +125,15 @@ def _dyn_def(stmt: ast.stmt, torch_names: set[str]):
     return stmt.targets[0].id, f.attr, operands
 
 
+def _row_mixing(g: Graph) -> bool:
+    """A run may hold grid-wide reductions (one grid region, codegen.Plan) or
+    row operators (one row region, rowgen.RowPlan), not both: a predicated
+    block `p = x.sum() > 0; t = softmax(x, -1); y = where(p, t, x)` becomes a
+    grid region for `p` followed by a row region that reads it."""
+    ops = {n.op for n in g.nodes}
+    return bool(ops & ROW_OPS) and bool(ops & (REDUCE | {NZSUM}))
+
+
 def _names_read(node: ast.AST) -> set[str]:
     return {n.id for n in ast.walk(node) if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Load)}
 
@@ -175,10 +184,10 @@ class _FunctionLowerer:
         if not self._eligible(stmt):
             return False
         try:
-            self._build(run + [stmt])
+            g, _ = self._build(run + [stmt])
         except Unsupported:
             return False
-        return True
+        return not _row_mixing(g)
 
     def _lower_dynamic_shape(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
         """a dynamic-shape op whose only consumer is a full
@@ -549,8 +558,16 @@ class _FunctionLowerer:
         last = run[-1]
         end = (last.end_lineno, last.end_col_offset)
         live = [n for n in assigned if in_loop or self.read_after(n, end)]
+        # a live-out whose final binding is a constant (`a = x.sum(); a = 3`,
+        # the reference's taint_kill fixture) is assigned after the region
+        consts = [ast.copy_location(ast.Assign(targets=[ast.Name(n, ast.Store())],
+                                               value=ast.Constant(b.env[n].value)), last)
+                  for n in live if b.env[n].op == "const"]
+        live = [n for n in live if b.env[n].op != "const"]
         out_nodes = [b.env[n] for n in live]
         if not live or not any(n.op not in ("free", "const") for n in graph.nodes):
+            if consts and not live:
+                return list(hoist) + consts
             return list(hoist) + list(run)
         rid = len(self.owner.regions)
         src = "\n".join(ast.unparse(s) for s in run)
@@ -573,7 +590,7 @@ class _FunctionLowerer:
             target = ast.Tuple([ast.Name(n, ast.Store()) for n in live], ast.Store())
         stmt = ast.Assign(targets=[target], value=call)
         ast.copy_location(stmt, run[0])
-        return list(hoist) + [stmt]
+        return list(hoist) + [stmt] + consts
 
 
 class _Lowerer:

@@ -30,6 +30,7 @@ import torch
 from . import _native as nat
 from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
 from .ir import Graph, Node, Unsupported, fold_host_predicates
+from .rowgen import RowPlan, has_row_ops
 
 SCRATCH_PARTIALS = 2432  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
 SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [speculative launches, mispredictions]
@@ -233,7 +234,8 @@ class _Spec:
         graph, outs = fold_host_predicates(region.graph, region.out_nodes, args)
         if any(o.op == "const" for o in outs):
             raise Unsupported("a live-out folds to a host constant")
-        plan = Plan(graph, outs, args, name=region.name, device_info=(sms, smem_optin))
+        plan_cls = RowPlan if has_row_ops(outs) else Plan
+        plan = plan_cls(graph, outs, args, name=region.name, device_info=(sms, smem_optin))
         self.plan = plan
         self.kernel = compiled_kernel(plan.source, plan.kernel)
         n = plan.n
@@ -294,7 +296,7 @@ class _Spec:
             if o.op == "free":
                 self.out_specs.append((j, "alias", o.value, None))
             elif o.kind == "elem":
-                self.out_specs.append((j, "elem", o.dtype, k))
+                self.out_specs.append((j, "elem", (o.dtype, tuple(o.shape)), k))
                 k += 1
             else:
                 self.out_specs.append((j, "scalar", o.dtype, k))
@@ -336,7 +338,7 @@ class _Spec:
             if kind == "alias":
                 outs[j] = args[info]
             elif kind == "elem":
-                t = torch.empty(self.shape, dtype=info, device=self.device)
+                t = torch.empty(info[1], dtype=info[0], device=self.device)
                 P.out[k].ptr = t.data_ptr()
                 outs[j] = t
             else:
@@ -372,7 +374,7 @@ class _Spec:
                 total += t.numel() * t.element_size()
         for j, kind, info, k in self.out_specs:
             if kind == "elem":
-                total += int(torch.Size(self.shape).numel()) * torch.empty((), dtype=info).element_size()
+                total += int(torch.Size(info[1]).numel()) * torch.empty((), dtype=info[0]).element_size()
         return total
 
     def timeline(self) -> list[int] | None:

@@ -1,0 +1,451 @@
+"""Row regions: fused kernels for arms that reduce along the innermost dim.
+
+The purity gate admits `softmax` (data/pure_ops.cfg:18) and any torch.* call
+in an arm (transform.py:265-289), and the attr_table reductions
+(sum/mean/max/min, attr_table.cfg:4-7) are also written with a `dim`
+(`x - x.amax(-1, keepdim=True)`, `x / x.sum(-1, keepdim=True)`).  The
+grid-stride region kernel (codegen.Plan) cannot express those: its vectors
+are spread over the whole grid, not over rows.  A row region is a run of
+statements whose row operators (ir.ROW_OPS) all reduce the innermost dim of
+one iteration space S = [..., C]:
+
+  * a group of TPR threads owns one row (TPR a power of two, the smallest
+    that keeps U = ceil(C / 8 / TPR) <= 4 vectors per thread); thread t of
+    the group holds the row's vectors u*TPR + t, so the group's loads of one
+    u are one contiguous stretch of the row (coalesced 128-bit accesses);
+  * the whole row stays in registers: a row statistic is a per-thread
+    partial, an xor-shuffle tree inside the warp and, for TPR > 32, a fixed
+    order combine of the group's warps through shared memory — every thread
+    of the group ends with the same value, and the elementwise code after
+    it reads the row from registers (one HBM read and one write per element
+    for `softmax(x * s)`, against eager's five passes);
+  * values with one element per row (`x.sum(-1, keepdim=True)`, a [..., 1]
+    input) are one register per thread (`rs<uid>`);
+  * scalar predicates of `torch.where` (0-d tensors computed by a preceding
+    grid region, host numbers) are uniform: the untaken arm's row operators
+    and loads are skipped by a branch, as in the grid kernel.
+
+A row region holds no grid-wide reduction (the lowering splits the
+statements, lowering._row_mixing): the predicate statistic runs in a grid
+region before it, whose 0-d output the row kernel reads.
+
+Numerics follow torch's CPU kernels for the last dim (aten/src/ATen/native/
+cpu/SoftMaxKernel.cpp `_vec_softmax_lastdim` / `_vec_log_softmax_lastdim`,
+ReduceOps): max, then exp(x - max) in the input's float type, its sum, then
+x * (1 / sum) (softmax) or x - max - log(sum) (log_softmax); sums accumulate
+in fp32 per thread and fp64 across threads, rounded once to the dtype; mean
+= (float)sum / C rounded once.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import torch
+
+from .codegen import (B200_DEVICE, DT_CODE, DT_SIZE, MODE_FULL, MODE_PERIODIC, MODE_SCALAR, MODE_STRIDED, InputPlan,
+                      Plan, _round_f)
+from . import _native as nat
+from .ir import ROW_NORM, ROW_OPS, ROW_RED, Graph, Node, Unsupported, infer, is_fusable_dtype, topo
+
+MODE_ROWIN = "row"        # one value per row ([..., 1]-shaped input)
+
+
+def _bcast_to(a: tuple, target: tuple) -> bool:
+    try:
+        return tuple(torch.broadcast_shapes(a, target)) == tuple(target)
+    except RuntimeError:
+        return False
+UMAX = 4                  # vectors per thread (registers: U x 8 floats per live node)
+MAX_TPR = 1024
+CTA_THREADS = 256
+
+
+def has_row_ops(outputs: list[Node]) -> bool:
+    return any(n.op in ROW_OPS for n in topo(outputs))
+
+
+class RowPlan(Plan):
+    """One specialisation of a row region (same interface as codegen.Plan:
+    source, kernel, grid, threads, smem_bytes, inputs, outputs, scalars)."""
+
+    def __init__(self, graph: Graph, outputs: list[Node], args: list, name: str = "region",
+                 device_info: tuple[int, int] = B200_DEVICE, allow_cpu: bool = False):
+        self.device_info = device_info
+        self.allow_cpu = allow_cpu
+        self.graph = graph
+        self.outputs = outputs
+        self.name = name
+        infer(graph, args, outputs)
+        self.order = topo(outputs)
+        self.host_exact = {n.uid: self._bf16_exact(args[n.value]) for n in self.order
+                           if n.op == "free" and n.kind == "host"}
+        self._classify_rows(args)
+        self._scalars_rows()
+        self._inputs(args)
+        self.hoisted = {}
+        self.decisions = []
+        self.spec = False
+        self.source = self._emit_rows()
+        digest = hashlib.sha1(self.source.encode()).hexdigest()[:16]
+        self.kernel = f"gm_row_{digest}"
+        self.source = self.source.replace("GM_KERNEL_NAME", self.kernel)
+
+    # -- classification -----------------------------------------------------------
+    def _classify_rows(self, args) -> None:
+        rowops = [n for n in self.order if n.op in ROW_OPS]
+        if not rowops:
+            raise Unsupported("row region without a row operator")
+        shapes = {tuple(n.args[0].shape) for n in rowops}
+        if len(shapes) != 1:
+            raise Unsupported(f"row operators over different shapes {shapes}")
+        S = next(iter(shapes))
+        if len(S) < 1 or math.prod(S) == 0:
+            raise Unsupported("empty or 0-d row operand")
+        self.shape = S
+        self.C = S[-1]
+        self.R = math.prod(S[:-1]) if len(S) > 1 else 1
+        self.n = self.R * self.C
+        keep = S[:-1] + (1,)
+        nokeep = S[:-1]
+        # rowval: one value per row; full: one value per element of S
+        self.rowval: set[int] = set()
+        for node in self.order:
+            if node.kind == "elem":
+                if not is_fusable_dtype(node.dtype):
+                    raise Unsupported(f"elementwise dtype {node.dtype}")
+                shp = tuple(node.shape)
+                if node.op in ROW_RED:
+                    if tuple(node.args[0].shape) != S:
+                        raise Unsupported("row reduction of a non-full operand")
+                    if shp == nokeep and len(S) < 2:
+                        raise Unsupported("row reduction of a 1-d tensor to a 0-d one")
+                    self.rowval.add(node.uid)
+                    continue
+                if node.op in ROW_NORM:
+                    continue
+                if node.op == "free":
+                    t = args[node.value]
+                    if t.device.type != "cuda" and not self.allow_cpu:
+                        raise Unsupported("tensor not on a CUDA device")
+                    if not _bcast_to(shp, S):
+                        raise Unsupported("input does not broadcast to the row space")
+                    if t.numel() == 1 or (len(shp) >= 1 and shp[-1] == 1 and self.C != 1):
+                        self.rowval.add(node.uid)
+                    continue
+                elem_args = [a for a in node.args if a.kind == "elem"]
+                if elem_args and all(a.uid in self.rowval for a in elem_args):
+                    # computed from row values (and scalars) only
+                    if shp not in (keep, nokeep) and not _bcast_to(shp, keep):
+                        raise Unsupported(f"row value of shape {shp}")
+                    self.rowval.add(node.uid)
+                    continue
+                if not _bcast_to(shp, S):
+                    raise Unsupported("node does not broadcast to the row space")
+                for a in elem_args:
+                    if a.uid in self.rowval and tuple(a.shape) == nokeep and nokeep != keep and len(S) >= 2:
+                        raise Unsupported("a keepdim=False row value broadcast against the full rows")
+            elif node.kind == "dscalar":
+                if any(a.kind == "elem" for a in node.args):
+                    raise Unsupported("grid reduction inside a row region")
+                if node.dtype not in (torch.float32, torch.bfloat16, torch.float16, torch.bool, torch.int64,
+                                      torch.int32):
+                    raise Unsupported(f"scalar dtype {node.dtype}")
+        for o in self.outputs:
+            if o.kind == "host":
+                raise Unsupported("host-only output")
+            if o.kind == "elem" and o.op != "free":
+                if o.uid in self.rowval:
+                    if tuple(o.shape) not in (keep, nokeep):
+                        raise Unsupported(f"row output of shape {tuple(o.shape)}")
+                elif tuple(o.shape) != S:
+                    raise Unsupported("output shape differs from the row space")
+        if self.n >= 2 ** 62:
+            raise Unsupported("row space too large")
+        # geometry
+        self.vec8 = self.C % nat.VEC == 0
+        nv_row = -(-self.C // nat.VEC)
+        tpr = 1
+        while -(-nv_row // tpr) > UMAX and tpr < MAX_TPR:
+            tpr *= 2
+        if -(-nv_row // tpr) > UMAX:
+            raise Unsupported(f"row of {self.C} elements exceeds the on-chip row ({MAX_TPR * UMAX * 8})")
+        self.TPR = tpr
+        self.U = -(-nv_row // tpr)
+        self.threads = max(CTA_THREADS, tpr)
+        self.RPC = self.threads // tpr
+        self.grid = -(-self.R // self.RPC)
+        if self.grid >= 2 ** 31:
+            raise Unsupported("too many rows")
+        self.K = self.U
+        self.smem_bytes = 0
+        self.smem_off = {}
+        self.minb = 1
+
+    def _scalars_rows(self) -> None:
+        self.reductions = []
+        self.npass = 1
+        self.avail = {}
+        self.need = {}
+        for node in self.order:
+            if node.kind in ("host", "dscalar"):
+                self.avail[node.uid] = 0
+            elif node.kind == "elem":
+                self.need[node.uid] = 0
+        self.pass_outputs = {0: [(j, o) for j, o in enumerate(self.outputs) if o.kind == "elem" and o.op != "free"]}
+        self.pass_reds = {0: []}
+        self.scalars = [n for n in self.order if n.kind in ("host", "dscalar") and n.op != "const"]
+        self.slot = {n.uid: i for i, n in enumerate(self.scalars)}
+
+    def _mode(self, t: torch.Tensor) -> str:
+        S = tuple(self.shape)
+        if t.numel() == 1:
+            return MODE_SCALAR
+        shp = tuple(t.shape)
+        if shp[-1:] == (1,) and S[-1] != 1:
+            return MODE_ROWIN
+        if shp == S and t.is_contiguous() and t.data_ptr() % 16 == 0:
+            return MODE_FULL
+        trail = list(shp)
+        while trail and trail[0] == 1:
+            trail.pop(0)
+        if t.is_contiguous() and trail and tuple(trail) == S[len(S) - len(trail):] and t.data_ptr() % 16 == 0:
+            return MODE_PERIODIC
+        return MODE_STRIDED
+
+    def row_offsets(self, t: torch.Tensor) -> list[tuple[int, int]]:
+        """(size, element stride) of the leading dims of a [..., 1] input
+        expanded to S (stride 0 where it broadcasts), outer..inner."""
+        S = tuple(self.shape)
+        ex = t.expand(S[:-1] + (1,)) if len(S) > 1 else t.reshape(1)
+        return list(zip(S[:-1], ex.stride()[:-1])) if len(S) > 1 else []
+
+    # -- emission ---------------------------------------------------------------------
+    def _ev(self, node: Node, lane: str, u) -> str:
+        if node.kind == "elem" and node.uid in self.rowval:
+            return f"rs{node.uid}"
+        return super()._ev(node, lane, u)
+
+    def _uniform_select(self, node: Node, u) -> list[str]:
+        c, ta, ea = node.args
+        R = _round_f(node.dtype) if node.dtype != torch.bool else ""
+
+        def val(x: Node) -> str:
+            if x.kind == "elem":
+                s = self._ev(x, "l", u)
+                return f"{R}({s})" if (R and x.dtype != node.dtype) else s
+            s = self._sf(x)
+            return f"{R}({s})" if R else s
+
+        return [
+            f"if (sb{c.uid}) {{\n#pragma unroll\nfor (int l = 0; l < GM_VEC; ++l) n{node.uid}_{u}[l] = {val(ta)};\n}} "
+            f"else {{\n#pragma unroll\nfor (int l = 0; l < GM_VEC; ++l) n{node.uid}_{u}[l] = {val(ea)};\n}}"
+        ]
+
+    def _free_full(self, node: Node, u: int) -> str:
+        ip = self.in_by_uid[node.uid]
+        dt, k = DT_CODE[ip.dtype], ip.slot
+        dst = f"n{node.uid}_{u}"
+        if ip.mode == MODE_FULL:
+            fn = "load8_gmem" if self.vec8 else "load8_elems"
+        elif ip.mode == MODE_PERIODIC:
+            fn = "load8_periodic" if self.vec8 else "load8_periodic_elems"
+        else:
+            fn = "load8_strided"
+        return f"gm::{fn}<{dt}>(P.in[{k}], e{u}, nv{u}, {dst});"
+
+    def _emit_rows(self) -> str:
+        out: list[str] = []
+        w = out.append
+        U, TPR = self.U, self.TPR
+        nscal = max(1, len(self.scalars))
+        if self.threads != nat.THREADS:
+            w(f"#define GM_THREADS {self.threads}")
+        w('#include "gm_region.cuh"')
+        w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
+        w("#define gm_trunc(x) ((double)(long long)(x))")
+        w(f"// row region {self.name}: rows {self.R} x {self.C}, {TPR} thread(s)/row, {U} vector(s)/thread, "
+          f"{self.RPC} row(s)/CTA, grid {self.grid} x {self.threads}{'' if self.vec8 else ', per-lane access'}")
+        w(f'extern "C" __global__ void __launch_bounds__({self.threads})')
+        w("GM_KERNEL_NAME(const __grid_constant__ gm::Params P) {")
+        w("  using namespace gm;")
+        w(f"  __shared__ double s_scal[{nscal}];")
+        w(f"  __shared__ double s_rw[{max(1, self.threads // 32)}];")
+        w("  (void)s_rw;")
+        w('  asm volatile("griddepcontrol.wait;" ::: "memory");')
+        self._emit_scalar_level(w, 0)
+        roots = [o for _, o in self.pass_outputs[0]]
+        nodes = self._nodes(roots)
+        guards = self._guards_roots(roots)
+        for s in self._used_scalars(nodes, guards):
+            w(f"  const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
+            w(f"  const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
+        w(f"  const int tr_ = threadIdx.x % {TPR};")
+        w(f"  const i64 row_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
+        w(f"  const bool rok_ = row_ < {self.R}ll;")
+        w(f"  const i64 rb_ = row_ * {self.C}ll;")
+        w("  (void)tr_; (void)rok_;")
+        for u in range(U):
+            w(f"  const i64 c{u} = ((i64){u} * {TPR} + tr_) * GM_VEC;")
+            w(f"  const int nv{u} = rok_ ? (int)max(0ll, min((i64)GM_VEC, {self.C}ll - c{u})) : 0;")
+            w(f"  const i64 e{u} = rb_ + c{u}; (void)e{u}; (void)nv{u};")
+        # inputs read once per row / once per launch
+        for ip in self.inputs:
+            if ip.node.kind != "elem" or ip.node not in nodes:
+                continue
+            dt = DT_CODE[ip.dtype]
+            if ip.mode == MODE_SCALAR:
+                w(f"  const float rs{ip.node.uid} = gm::load_scalar<{dt}>(P.in[{ip.slot}]);")
+            elif ip.mode == MODE_ROWIN:
+                terms = []
+                idx = "row_"
+                div = 1
+                for size, stride in reversed(self._row_layout[ip.slot]):
+                    if stride:
+                        t = f"(({idx} / {div}ll) % {size}ll) * {stride}ll" if div != 1 else f"({idx} % {size}ll) * {stride}ll"
+                        terms.append(t)
+                    div *= size
+                off = " + ".join(terms) if terms else "0ll"
+                w(f"  const float rs{ip.node.uid} = rok_ ? gm::load_at<{dt}>(P.in[{ip.slot}], {off}) : 0.f;")
+        # every unguarded full-size input's vectors are loaded first
+        TRUE = frozenset({frozenset()})
+        first = [n for n in nodes if n.op == "free" and n.uid not in self.rowval
+                 and not self._guard_expr(guards.get(n.uid, TRUE))]
+        # every value is declared here: guarded blocks only assign
+        for n in nodes:
+            if n.uid in self.rowval:
+                if n.op != "free":
+                    w(f"  float rs{n.uid} = 0.f;")
+            else:
+                w(f"  float {', '.join(f'n{n.uid}_{u}[GM_VEC]' for u in range(U))};")
+        for n in first:
+            for u in range(U):
+                w("  " + self._free_full(n, u))
+        rest = [n for n in nodes if n not in first]
+        cur = None
+        for n in rest:
+            g = self._guard_expr(guards.get(n.uid, TRUE))
+            if g != cur:
+                if cur:
+                    w("  }")
+                if g:
+                    w(f"  if ({g}) {{")
+                cur = g
+            self._emit_node(w, n)
+        if cur:
+            w("  }")
+        # stores
+        for j, o in self.pass_outputs[0]:
+            k = self._out_slot(j)
+            dt = DT_CODE[o.dtype]
+            if o.uid in self.rowval:
+                w(f"  if (rok_ && tr_ == 0) gm::store_at<{dt}>(P.out[{k}], row_, rs{o.uid});")
+            else:
+                fn = "store8" if self.vec8 else "store8_elems"
+                for u in range(U):
+                    w(f"  if (nv{u}) gm::{fn}<{dt}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
+        # scalar outputs and the scalar mirror (CTA 0)
+        w("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
+        for j, o in enumerate(self.outputs):
+            if o.kind == "dscalar":
+                k = self._out_slot(j)
+                val = self._sv(o)
+                if o.dtype == torch.int64:
+                    w(f"    *(long long*)P.out[{k}].ptr = (long long){val};")
+                elif o.dtype == torch.int32:
+                    w(f"    *(int*)P.out[{k}].ptr = (int){val};")
+                else:
+                    w(f"    gm::store_scalar<{DT_CODE[o.dtype]}>(P.out[{k}], {val});")
+        w(f"    if (P.scal_out) for (int i = 0; i < {len(self.scalars)}; ++i) ((double*)P.scal_out)[i] = s_scal[i];")
+        w("  }")
+        w("}")
+        return "\n".join(out) + "\n"
+
+    def _inputs(self, args) -> None:
+        super()._inputs(args)
+        self._row_layout = {}
+        for ip in self.inputs:
+            if ip.mode == MODE_ROWIN:
+                t = args[ip.free_index]
+                self._row_layout[ip.slot] = self.row_offsets(t)
+
+    def _emit_node(self, w, n: Node) -> None:
+        U = self.U
+        if n.op == "free":
+            if n.uid in self.rowval:
+                return  # loaded above (rs<uid>)
+            for u in range(U):
+                w("  " + self._free_full(n, u))
+            return
+        if n.op in ROW_RED:
+            self._emit_row_reduce(w, n)
+            return
+        if n.op in ROW_NORM:
+            self._emit_row_norm(w, n)
+            return
+        if n.uid in self.rowval:
+            # one value per row: computed once per thread
+            w("  {")
+            w(f"  float n{n.uid}_r[GM_VEC];")
+            for line in self._elem_code(n, "r"):
+                w("  " + line.replace("\n", "\n  "))
+            w(f"  rs{n.uid} = n{n.uid}_r[0];")
+            w("  }")
+            return
+        for u in range(U):
+            for line in self._elem_code(n, u):
+                w("  " + line.replace("\n", "\n  "))
+
+    def _row_stat(self, w, name: str, x: Node, op: str, expr=None) -> None:
+        """float `name` = the row's max/min (NaN-propagating) or sum of
+        expr(x lane) over its valid lanes; sums: fp32 per thread, fp64 across
+        threads, rounded once to fp32."""
+        U, TPR = self.U, self.TPR
+        ident = {"max": "__int_as_float(0xff800000)", "min": "__int_as_float(0x7f800000)", "sum": "0.f"}[op]
+        w(f"  float {name}_t = {ident}; (void){name}_t;")
+        for u in range(U):
+            v = f"n{x.uid}_{u}[l]" if expr is None else expr(u)
+            if op == "sum":
+                upd = f"{name}_t = gm::add({name}_t, {v});"
+            else:
+                upd = f"{name}_t = gm::n{op}({name}_t, {v});"
+            w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) if (l < nv{u}) {upd}")
+        code = {"sum": "GM_R_SUM", "max": "GM_R_MAX", "min": "GM_R_MIN"}[op]
+        w(f"  const float {name} = (float)gm::row_combine<{TPR}, {code}>((double){name}_t, s_rw);")
+
+    def _emit_row_reduce(self, w, n: Node) -> None:
+        x = n.args[0]
+        fn = ROW_RED[n.op]
+        R = _round_f(n.dtype)
+        if fn in ("amax", "amin"):
+            self._row_stat(w, f"st{n.uid}", x, "max" if fn == "amax" else "min")
+            w(f"  rs{n.uid} = st{n.uid};")
+            return
+        if x.dtype == torch.bool:
+            raise Unsupported("row sum of a bool tensor")
+        self._row_stat(w, f"st{n.uid}", x, "sum")
+        val = f"st{n.uid}" if fn == "sum" else f"__fdiv_rn(st{n.uid}, {float(self.C)!r}f)"
+        w(f"  rs{n.uid} = {R}({val});" if R else f"  rs{n.uid} = {val};")
+
+    def _emit_row_norm(self, w, n: Node) -> None:
+        x = n.args[0]
+        U = self.U
+        R = _round_f(n.dtype)
+        m = f"mx{n.uid}"
+        self._row_stat(w, m, x, "max")
+        for u in range(U):
+            w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = "
+              f"expf(gm::sub(n{x.uid}_{u}[l], {m}));")
+        s = f"sm{n.uid}"
+        self._row_stat(w, s, n, "sum")
+        if n.op == "softmax":
+            w(f"  const float iv{n.uid} = gm::div(1.f, {s});")
+            body = f"gm::mul(n{n.uid}_{{u}}[l], iv{n.uid})"
+        else:
+            w(f"  const float ls{n.uid} = logf({s});")
+            body = f"gm::sub(gm::sub(n{x.uid}_{{u}}[l], {m}), ls{n.uid})"
+        for u in range(U):
+            b = body.format(u=u)
+            w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = {R}({b});" if R else
+              f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = {b};")
