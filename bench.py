@@ -40,6 +40,8 @@ WORKLOADS = {
     "bigbird_like": ("config 2: BigBird-RoBERTa-base-shaped layer, seq 1024, batch 8", None),
     "bart_step": ("config 4: BART-base-shaped decoder step, batch 32", None),
     "gemm_arms": ("config 2 variant: BigBird-shaped layer whose predicated arms each hold a GEMM", None),
+    "bigbird_attn": ("config 2 with attention: BigBird-RoBERTa-base-shaped self-attention, 12 heads, "
+                     "block-sparse / full softmax over [8,12,1024,1024] scores", None),
     "phi4_like": ("config 5: corpus phi4_like at [8,1024,768]", [[8, 1024, 768]]),
     "qwen_audio_like": ("config 5: corpus qwen_audio_like at [8,1024,768]", [[8, 1024, 768]]),
     "longformer_like": ("config 3: corpus longformer_like at [4,4096,768]", [[4, 4096, 768]]),
@@ -392,8 +394,11 @@ def main():
     from paper_2509_16248_b200 import compile_program, gemm
     from paper_2509_16248_b200.region import scratch_owner
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one replica per GPU; on a box with fewer GPUs than ranks (the 1-GPU
+    # test box) replicas share devices round-robin
+    gpu = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     pg = None
     if ws > 1:
         # replicas only: gloo carries the timing barrier and the max over
@@ -433,13 +438,14 @@ def main():
         torch.cuda.synchronize(dev)
 
     def spec_totals():
-        tot = [0, 0]
+        tot = [0, 0, 0]
         for r in low.regions:
             sp = r.last_spec
             if sp is not None and sp.plan.spec:
                 a, b = sp.spec_stats()
                 tot[0] += a
                 tot[1] += b
+                tot[2] += sp.exact_entries()
         return tot
 
     # ---- device-timed replay (inputs resident in HBM, rotating): before
@@ -452,7 +458,7 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(gpu) as clocks:
         # keep the GPU busy (untimed replays) until nvidia-smi has sampled it
         # under load, so the clock record covers the timed region
         t_load = time.perf_counter()
@@ -477,24 +483,34 @@ def main():
     total_ms = max_over_ranks(sum(step_ms), pg)
     value = replica_value(batch, args.steps, ws, total_ms / 1e3)
     speculation = {"launches": spec1[0] - spec0[0], "mispredictions": spec1[1] - spec0[1],
+                   "exact_entries": spec1[2] - spec0[2],
                    "how": f"speculative region launches in the timed loop, inputs rotating over {R} manifest draws"}
     if speculation["launches"]:
-        speculation["hit_rate"] = 1.0 - speculation["mispredictions"] / speculation["launches"]
+        speculated = speculation["launches"] - speculation["exact_entries"]
+        speculation["speculated"] = speculated
+        speculation["hit_rate"] = (1.0 - speculation["mispredictions"] / speculated) if speculated else None
 
     # ---- each fused kernel timed on its own stream, cold L2: a CUDA graph of
     #      R x [256 MB L2 flush, region launch] minus a graph of R x [flush],
     #      both replayed between CUDA events (no host work inside the window)
     fused = [r for r in low.regions if r.last_spec is not None]
+    live = _live_kernel_ms(ex, low, xs_dev, flush_l2, dev, args.steps)
     kernels = []
     for r in fused:
         spec = r.last_spec
-        ms = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev)
-        k = {"name": f"{spec.plan.kernel} ({r.name})", "ms": ms,
-             "bytes": spec.bytes_alg(list(r.last_args)), "grid": spec.grid, "smem": spec.smem,
+        nbytes = spec.bytes_alg(list(r.last_args))
+        k = {"name": f"{spec.plan.kernel} ({r.name})", "ms": live.get(r.rid, float("nan")),
+             "bytes": nbytes, "grid": spec.grid, "smem": spec.smem,
              "passes": spec.plan.npass, "speculative": spec.plan.spec,
-             "how": "graph of 20 x (L2 flush + launch) minus 20 x flush; cold L2"}
+             "how": "live: CUDA events captured around the launch inside the forward's graph, replayed over the "
+                    "rotating inputs with the L2 flushed before every step (the timed loop's conditions), mean",
+             "ms_isolated": _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev),
+             "isolated_how": "graph of 20 x (L2 flush + launch) minus 20 x flush; cold L2; one input"}
         if spec.plan.spec:
-            k["ms_mispredicted"] = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev, mispredict=True)
+            k["ms_isolated"] = k["ms_isolated"]
+            k["ms_spec_hit"] = k.pop("ms_isolated")
+            k["ms_spec_miss"] = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev, mode="miss")
+            k["ms_exact_entry"] = _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev, mode="exact")
         kernels.append(k)
     dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
     peak, peak_kind = _peaks()
@@ -644,42 +660,84 @@ def _copy_only_pipeline(x_host, outs, dev, steps: int) -> float:
     return time.perf_counter() - t0
 
 
-def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5, mispredict: bool = False) -> float:
-    """Average duration (ms) of one region launch with a cold L2.  With
-    `mispredict`, every launch of a speculative region is handed the wrong
-    predictions (the exact fallback path runs)."""
+def _live_kernel_ms(ex, low, xs_dev, flush, dev, steps: int) -> dict:
+    """Per-region kernel duration (ms, mean) inside the forward's own CUDA
+    graph under the timed loop's conditions: a fresh graph slot is captured
+    with a pair of external CUDA events around every region launch, then
+    replayed `steps` times over the rotating inputs with the L2 flushed
+    before each step; the events are read after each replay."""
+    import torch
+
+    regions = [r for r in low.regions if r.last_spec is not None]
+    for r in regions:
+        r.probe = (torch.cuda.Event(enable_timing=True, external=True),
+                   torch.cuda.Event(enable_timing=True, external=True))
+    try:
+        entry = ex.prepare(*xs_dev[0], slot="probe")
+    finally:
+        probes = {r.rid: r.probe for r in regions}
+        for r in regions:
+            r.probe = None
+    acc = {rid: [] for rid in probes}
+    R = len(xs_dev)
+    for i in range(steps):
+        entry.load(xs_dev[i % R])
+        flush()
+        entry.run()
+        torch.cuda.synchronize(dev)
+        if i < 3:
+            continue   # the slot's first launches (its confidence counters start at 0)
+        for rid, (a, b) in probes.items():
+            acc[rid].append(a.elapsed_time(b))
+    ex.flush()
+    return {rid: statistics.mean(v) for rid, v in acc.items() if v}
+
+
+def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5, mode: str = "hit") -> float:
+    """Average duration (ms) of one region launch with a cold L2.  For a
+    speculative region `mode` picks the path every launch takes: "hit"
+    (speculation on the correct decisions), "miss" (speculation on the wrong
+    decisions, then the restart) or "exact" (the exact staged entry)."""
     import torch
 
     nd = len(spec.plan.decisions) if spec.plan.spec else 0
-    from paper_2509_16248_b200.region import SCRATCH_PRED, scratch_owner
+    from paper_2509_16248_b200.region import SCRATCH_CONF, SCRATCH_PRED, scratch_owner
 
     owner = object()   # this measurement's own barrier scratch, zeroed before the captures
-    wrong = None
-    if mispredict and nd:
+    want_pred = want_conf = None
+    if nd:
         vals = spec.scalars()
-        wrong = torch.tensor([0 if vals[spec.plan.slot[d.uid]] != 0.0 else 1 for d in spec.plan.decisions],
-                             dtype=torch.int32, device=dev)
+        dec = [1 if vals[spec.plan.slot[d.uid]] != 0.0 else 0 for d in spec.plan.decisions]
+        if mode == "miss":
+            dec = [1 - v for v in dec]
+        want_pred = torch.tensor(dec, dtype=torch.int32, device=dev)
+        want_conf = torch.tensor([0 if mode == "exact" else 3], dtype=torch.int32, device=dev)
 
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(side), scratch_owner(owner):
         spec.run(args, pdl=False)  # warm (allocator, module, this owner's scratch)
         pred = spec.scratch[SCRATCH_PRED: SCRATCH_PRED + 4 * nd].view(torch.int32) if nd else None
+        conf = spec.scratch[SCRATCH_CONF: SCRATCH_CONF + 4].view(torch.int32) if nd else None
     torch.cuda.current_stream(dev).wait_stream(side)
     torch.cuda.synchronize(dev)
     g_both, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     keep = []
+
+    def force():
+        if want_pred is not None:
+            pred.copy_(want_pred)
+            conf.copy_(want_conf)
+
     with torch.cuda.graph(g_both), scratch_owner(owner):
         for _ in range(reps):
             flush()
-            if wrong is not None:
-                pred.copy_(wrong)
+            force()
             keep.append(spec.run(args, pdl=False))  # the kernel's own duration
     with torch.cuda.graph(g_flush):
         for _ in range(reps):
             flush()
-            if wrong is not None:
-                pred.copy_(wrong)
+            force()
 
     def t(g):
         g.replay()

@@ -20,6 +20,7 @@ from .harness import make_args, programs
 from .ir import Unsupported
 from .lowering import load
 from .region import aot_compile
+from .rowgen import RowPlan, has_row_ops
 
 B200 = B200_DEVICE   # SMs, max opt-in dynamic shared memory per block
 
@@ -27,6 +28,7 @@ B200 = B200_DEVICE   # SMs, max opt-in dynamic shared memory per block
 SPECS = [("bigbird_like", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("bart_step", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("gemm_arms", d, None) for d in (torch.bfloat16, torch.float32)] + \
+        [("bigbird_attn", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("toy", torch.float32, None)]
 
 
@@ -70,7 +72,8 @@ def collect_sources(specs=None, progs=None) -> list[str]:
         for r in low.regions:
             for rargs in r.trace[:1]:
                 try:
-                    plan = Plan(r.graph, r.out_nodes, list(rargs), name=r.name, device_info=B200, allow_cpu=True)
+                    cls = RowPlan if has_row_ops(r.out_nodes) else Plan
+                    plan = cls(r.graph, r.out_nodes, list(rargs), name=r.name, device_info=B200, allow_cpu=True)
                 except Unsupported:
                     continue
                 sources.append(plan.source)

@@ -62,6 +62,10 @@ B200_DEVICE = (148, 232448)  # SMs, opt-in dynamic shared memory per block
 DATA_REGS = int(os.environ.get("GM_DATA_REGS", "40"))  # raw-vector registers per thread: register stage + one block's loads
 VEC_REGS = {torch.float32: 8, torch.bfloat16: 4, torch.float16: 4, torch.bool: 2}
 MAX_DECISIONS = 24      # predicted decisions per speculative region (scratch ints at barrier + 288)
+# adaptive speculation: speculate once the confidence counter reaches
+# SPEC_CONFIDENT (two launches in a row that repeated their decisions)
+SPEC_CONFIDENT = int(os.environ.get("GM_SPEC_CONFIDENT", "2"))
+SPEC_CONF_MAX = 3
 
 
 def _round_f(dtype) -> str:
@@ -134,7 +138,7 @@ class Plan:
 
     # -- classification -----------------------------------------------------
     def _classify(self, args) -> None:
-        elem_roots = [o for o in self.outputs if o.kind == "elem"]
+        elem_roots = [o for o in self.outputs if o.kind == "elem" and o.op != "free"]  # (free: an alias)
         red_nodes = [n for n in self.order if n.op in REDUCE]
         for n in red_nodes:
             if n.args[0].kind != "elem":
@@ -146,11 +150,18 @@ class Plan:
         self.n = math.prod(self.shape) if shapes else 0
         if self.n >= 2 ** 32 and any(n.op in ("argmax", "argmin") for n in red_nodes):
             raise Unsupported("argmax/argmin keys carry a 32-bit index")
+        read = {a.uid for n in self.order for a in n.args}
         for node in self.order:
+            if node.op == "free" and node.uid not in read:
+                continue  # only passed through as an output alias
             if node.kind == "elem":
                 if not is_fusable_dtype(node.dtype):
                     raise Unsupported(f"elementwise dtype {node.dtype}")
-                if torch.broadcast_shapes(node.shape, self.shape) != tuple(self.shape):
+                try:
+                    ok = tuple(torch.broadcast_shapes(node.shape, self.shape)) == tuple(self.shape)
+                except RuntimeError:
+                    ok = False
+                if not ok:
                     raise Unsupported("node does not broadcast to the iteration space")
             elif node.kind == "dscalar":
                 if node.dtype not in (torch.float32, torch.bfloat16, torch.float16, torch.bool, torch.int64,
@@ -159,7 +170,7 @@ class Plan:
         for o in self.outputs:
             if o.kind == "host":
                 raise Unsupported("host-only output")
-            if o.kind == "elem" and tuple(o.shape) != tuple(self.shape):
+            if o.kind == "elem" and o.op != "free" and tuple(o.shape) != tuple(self.shape):
                 raise Unsupported("output shape differs from the iteration space")
         for node in self.order:
             if node.op == "free" and node.kind == "elem":
@@ -795,7 +806,7 @@ class Plan:
         self.smem_bytes = 0
         self.decisions = self._decisions()
         self.spec = self._spec_ok()
-        if self.spec or not self.reductions or self.npass < 2 or not self.K \
+        if not self.reductions or self.npass < 2 or not self.K \
                 or os.environ.get("GM_STAGING", "1") == "0":
             return
         full = [ip for ip in self.inputs if ip.mode == MODE_FULL and ip.passes]
@@ -940,7 +951,9 @@ class Plan:
             if self.stage[ip.slot] == "reg":
                 for u in range(self.K):
                     w(f"  gm::Raw<{DT_CODE[ip.dtype]}> rs{ip.slot}_{u};")
-        if self.prefetch:
+        def prefetch():
+            if not self.prefetch:
+                return
             # cp.async of every vector a later pass reads into its stash slot
             for slot in sorted(self.prefetch):
                 ip = self.inputs[slot]
@@ -951,29 +964,53 @@ class Plan:
                   f"GM_VEC * {DT_SIZE[ip.dtype]}), P.in[{slot}], v * GM_VEC);")
                 w("  }")
             w("  gm::cp_async_commit();")
-        self._emit_scalar_level(w, 0)
+
         self.red_index = {r.uid: i for i, r in enumerate(self.reductions)}
-        if self.spec:
+        if not self.spec:
+            prefetch()
+            self._emit_scalar_level(w, 0)
+        else:
+            # Adaptive speculation.  A confidence counter in the scratch
+            # (+56) picks the entry: >= 2 speculates on the last launch's
+            # decisions; below, the exact staged passes run (one HBM read of
+            # each input, kept on chip across the grid barriers) and the
+            # counter grows while consecutive launches repeat their decisions.
+            # A hit keeps the counter, a miss resets it: inputs whose decisions
+            # alternate settle on the exact entry instead of paying a
+            # speculative sweep plus a restart on most launches.
             nd = len(self.decisions)
             w(f"  __shared__ int s_pred[{nd}];")
             w("  __shared__ int s_miss;")
-            w("  int* pred_ = (int*)(P.barrier + GM_SCRATCH_PRED);  // predicted decisions (last launch's)")
+            w("  __shared__ int s_mode;  // 1: speculate on the predicted decisions")
+            w("  int* pred_ = (int*)(P.barrier + GM_SCRATCH_PRED);  // last launch's decisions")
+            w("  int* conf_ = (int*)(P.barrier + GM_SCRATCH_CONF);  // prediction confidence")
+            w("  if (threadIdx.x == 0) {")
+            w("    int c_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(c_) : \"l\"(conf_));")
+            w(f"    s_mode = c_ >= {SPEC_CONFIDENT} ? 1 : 0;")
+            w("  }")
+            self._emit_scalar_level(w, 0)
+            w("  if (s_mode) {")
+            saved = (self.stage, self.prefetch)
+            self.stage = {k: "none" for k in self.stage}
+            self.prefetch = set()
             self._emit_ctx(w, "spec")
             w("  if (!s_miss) {")
-            self._emit_epilogue(w, "    ", miss=False)
+            self._emit_epilogue(w, "    ", mode="hit")
             w("    return;")
             w("  }")
             w("  // misprediction: the exact passes from the first mispredicted level (inputs re-read)")
-        for p in range(self.npass):
-            if self.spec:
-                # restart at the first mispredicted level (decisions have
-                # level >= 1, so pass 0 never reruns)
-                if p == 0:
-                    continue
+            for p in range(1, self.npass):
+                # decisions have level >= 1, so pass 0 never reruns
                 w(f"  if (s_miss <= {p}) {{")
                 self._emit_ctx(w, p)
                 w("  }")
-                continue
+            self._emit_epilogue(w, "  ", mode="miss")
+            w("  return;")
+            w("  }")
+            self.stage, self.prefetch = saved
+            w("  // exact entry: every pass, inputs staged on chip")
+            prefetch()
+        for p in range(self.npass):
             if p in self.hoisted and not self.spec:
                 self._emit_hoist_guard(w, p)
                 w(f"  if (!s_hoist{p}) {{  // hoisting guard failed: the exact sweep")
@@ -985,13 +1022,15 @@ class Plan:
         if prof:
             w("  __syncthreads();")
             w("  if (threadIdx.x == 0) atomicMax(&prof_[63], gm::globaltimer());")
-        self._emit_epilogue(w, "  ", miss=self.spec)
+        self._emit_epilogue(w, "  ", mode="exact" if self.spec else "plain")
         w("}")
         return "\n".join(out) + "\n"
 
-    def _emit_epilogue(self, w, ind: str, miss: bool) -> None:
+    def _emit_epilogue(self, w, ind: str, mode: str) -> None:
         """Scalar outputs, the debug mirror and (speculative kernels) the
-        prediction update + hit/miss counters, by CTA 0 thread 0."""
+        prediction and confidence update + launch / miss / exact-entry
+        counters, by one thread.  `mode`: "plain" (no speculation), "hit",
+        "miss" (after the restart) or "exact" (the exact entry)."""
         w(f"{ind}if (s_epi_ && threadIdx.x == 0) {{")
         for j, o in enumerate(self.outputs):
             if o.kind == "dscalar":
@@ -1007,10 +1046,20 @@ class Plan:
         w(f"{ind}    for (int i = 0; i < {len(self.scalars)}; ++i) ((double*)P.scal_out)[i] = s_scal[i];")
         w(f"{ind}  }}")
         if self.spec:
-            w(f"{ind}  u64* st_ = (u64*)(P.barrier + GM_SCRATCH_STATS);  // [launches, mispredictions]")
+            w(f"{ind}  u64* st_ = (u64*)(P.barrier + GM_SCRATCH_STATS);  // [launches, mispredictions, exact entries]")
             w(f"{ind}  st_[0] += 1;")
-            if miss:
+            if mode == "hit":
+                w(f"{ind}  *conf_ = min(*conf_ + 1, {SPEC_CONF_MAX});")
+            elif mode == "miss":
                 w(f"{ind}  st_[1] += 1;")
+                w(f"{ind}  *conf_ = 0;")
+            else:
+                w(f"{ind}  st_[2] += 1;")
+                w(f"{ind}  int same_ = 1;")
+                for j, d in enumerate(self.decisions):
+                    w(f"{ind}  same_ &= ((s_scal[{self.slot[d.uid]}] != 0.0) == (pred_[{j}] != 0)) ? 1 : 0;")
+                w(f"{ind}  *conf_ = same_ ? min(*conf_ + 1, {SPEC_CONF_MAX}) : 0;")
+            if mode in ("miss", "exact"):
                 for j, d in enumerate(self.decisions):
                     w(f"{ind}  pred_[{j}] = (s_scal[{self.slot[d.uid]}] != 0.0) ? 1 : 0;")
         w(f"{ind}}}")

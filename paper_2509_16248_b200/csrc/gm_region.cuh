@@ -812,10 +812,12 @@ __device__ __forceinline__ void st_release64(u64* p, u64 v) {
 // arrivals and the broadcast sit on separate 128-byte lines:
 //   +0    u64 arrival counter (monotonic across launches and passes)
 //   +16   int status (1 = barrier timeout)
-//   +32   u64 [speculative launches, mispredictions] (CTA 0, kernel end)
+//   +32   u64 [launches, mispredictions, exact entries] (speculative regions)
+//   +56   int prediction confidence (speculate when >= 2)
 //   +288  int predicted decisions of a speculative region
 // and P.partials = double[slot][gridDim.x] at +GM_SCRATCH_PARTIALS.
-#define GM_SCRATCH_STATS 32     // u64 [speculative launches, mispredictions]
+#define GM_SCRATCH_STATS 32     // u64 [launches, mispredictions, exact entries] (speculative regions)
+#define GM_SCRATCH_CONF 56      // int prediction confidence (adaptive speculation)
 #define GM_SCRATCH_FLAG 128     // (free: tools/barrier_bench.py protocol variants)
 #define GM_SCRATCH_RESULTS 136
 #define GM_SCRATCH_PRED 288     // int[24] predicted decisions (speculative regions)

@@ -19,6 +19,7 @@ torch.library custom op with a fake implementation, so it traces.
 
 from __future__ import annotations
 
+import ast
 import ctypes
 import functools
 import textwrap
@@ -46,7 +47,7 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
     unless `allow_eager` (then the lowered statements run eagerly with
     PyTorch, bit-identical to the graph): there is no silent CPU path.
     `functools.partial(gm_b200_backend, allow_eager=True)` opts in."""
-    module, lowered = load(_PRELUDE + textwrap.dedent(gm.code), allow_eager=allow_eager)
+    module, lowered = load(_PRELUDE + _fx_source(gm), allow_eager=allow_eager)
     forward = functools.partial(module.forward, gm)
     on_cuda = any(torch.is_tensor(a) and a.is_cuda for a in example_inputs)
     if not on_cuda:
@@ -75,6 +76,56 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
     run.lowered = lowered
     run.stats = stats
     return run
+
+
+def _fx_source(gm: torch.fx.GraphModule) -> str:
+    """The graph's Python source as the lowering wants it.  Traced with
+    `capture_scalar_outputs` / `capture_dynamic_output_shape_ops` (gm_compile)
+    the graph keeps `.item()` and nonzero / unique / masked_select inside, with
+    runtime asserts on the unbacked sizes (`_assert_scalar(sym_size(v) >= 0)`):
+    those are dropped (the lowering gives every such value a fixed shape, so
+    no size is ever unbacked), dead size computations are eliminated, and the
+    `v = None` frees FX emits are removed — they would read as rebindings."""
+    g = gm.graph
+    changed = False
+    for node in list(g.nodes):
+        if node.op == "call_function" and node.target in (torch.ops.aten._assert_scalar.default,
+                                                          getattr(torch.ops.aten, "_assert_async", None)):
+            g.erase_node(node)
+            changed = True
+    if changed:
+        g.eliminate_dead_code()
+        gm.recompile()
+    tree = ast.parse(textwrap.dedent(gm.code))
+
+    class _Frees(ast.NodeTransformer):
+        def visit_Assign(self, node):
+            if isinstance(node.value, ast.Constant) and node.value.value is None \
+                    and all(isinstance(t, ast.Name) for t in node.targets):
+                return None
+            return node
+
+    tree = ast.fix_missing_locations(_Frees().visit(tree))
+    return ast.unparse(tree) + "\n"
+
+
+def gm_compile(model, **kwargs):
+    """`torch.compile(model, backend="gm_b200")` traced so that GraphMend's
+    residual breaks do not split the graph: `.item()` reads and dynamic-shape
+    ops (the reference reports them unfixable, analysis.py:597-605,
+    data/dynamic_shape_ops.cfg) are captured into the FX graph, where the
+    lowering turns them into device scalars and fixed-shape reductions
+    (SURVEY §8f ranks 1-2).  The whole forward is then one FX graph, one
+    CUDA graph, no host sync — as on the direct path (compile_program)."""
+    compiled = torch.compile(model, backend="gm_b200", **kwargs)
+
+    @functools.wraps(getattr(model, "forward", model))
+    def call(*args, **kw):
+        with torch._dynamo.config.patch(capture_scalar_outputs=True, capture_dynamic_output_shape_ops=True):
+            return compiled(*args, **kw)
+
+    call.compiled = compiled
+    return call
 
 
 try:  # `torch.compile(model, backend="gm_b200")`

@@ -32,7 +32,7 @@ import linecache
 import types
 from dataclasses import dataclass, field
 
-from .ir import NZSUM, REDUCE, ROW_OPS, Builder, Graph, Unsupported, attr_chain
+from .ir import ITEM, NZSUM, REDUCE, ROW_OPS, Builder, Graph, Unsupported, attr_chain
 from .region import Region
 
 GM_RT = "__gm_rt__"  # dunder suffix: exempt from private-name mangling in class bodies
@@ -253,6 +253,87 @@ class _FunctionLowerer:
             i += 1
         return out
 
+    def _rematerialise(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
+        """A cheap elementwise value read both by a grid reduction and by a
+        row operator (`scores = t / 8.0; p = scores.abs().mean() > c;
+        probs = softmax(scores + bias, -1)`) would be written to HBM by the
+        grid region and read back by the row region that follows it
+        (lowering._row_mixing splits them).  It is substituted into its uses
+        instead — each region recomputes it from its inputs, with the same
+        operators in the same order (identical values), and the full-size
+        intermediate is never materialised.  Only single-assignment names
+        whose every read is in a later top-level statement of this block,
+        with inputs not rebound before the last read."""
+        out = list(stmts)
+        i = 0
+        while i < len(out):
+            s = out[i]
+            if not self._eligible(s) or s.targets[0].id in self.always_live:
+                i += 1
+                continue
+            V = s.targets[0].id
+            try:
+                g, _ = self._build([s])
+            except Unsupported:
+                i += 1
+                continue
+            ops = [n.op for n in g.nodes if n.op not in ("free", "const")]
+            if not ops or len(ops) > 8 or set(ops) & (REDUCE | ROW_OPS | {NZSUM, ITEM}) \
+                    or any("[" in fv.text for fv in g.frees):
+                i += 1
+                continue
+            names = [n for n in ast.walk(self.fn) if isinstance(n, ast.Name) and n.id == V]
+            if sum(isinstance(n.ctx, ast.Store) for n in names) != 1:
+                i += 1
+                continue
+            uses = [j for j in range(i + 1, len(out)) if V in _names_read(out[j])]
+            n_loads = sum(isinstance(n.ctx, ast.Load) for n in names)
+            if not uses or sum(sum(1 for n in ast.walk(out[j]) if isinstance(n, ast.Name) and n.id == V
+                                   and isinstance(n.ctx, ast.Load)) for j in uses) != n_loads:
+                i += 1
+                continue
+            roots = {fv.text.split(".")[0] for fv in g.frees}
+            rebound = {n.id for t in out[i + 1:max(uses) + 1] for n in ast.walk(t)
+                       if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Store)}
+            if roots & rebound:
+                i += 1
+                continue
+            kinds = set()
+            for j in uses:
+                if not self._eligible(out[j]):
+                    continue
+                try:
+                    gj, _ = self._build([out[j]])
+                except Unsupported:
+                    continue
+                oj = {n.op for n in gj.nodes}
+                if oj & ROW_OPS:
+                    kinds.add("row")
+                if oj & REDUCE:
+                    kinds.add("grid")
+            if kinds != {"row", "grid"}:
+                i += 1
+                continue
+            expr = s.value
+
+            class _Sub(ast.NodeTransformer):
+                def visit_Name(self, node):
+                    if node.id == V and isinstance(node.ctx, ast.Load):
+                        e = copy.deepcopy(expr)
+                        for sub in ast.walk(e):
+                            if hasattr(sub, "lineno"):
+                                ast.copy_location(sub, node)
+                        return e
+                    return node
+
+            for j in uses:
+                out[j] = _Sub().visit(out[j])
+                pos = (out[j].lineno, out[j].col_offset + 1)
+                self.loads.extend((pos, r) for r in _names_read(expr))
+            self.owner.rematerialised.append(V)
+            del out[i]
+        return out
+
     def _fusable(self, e: ast.expr) -> bool:
         try:
             Builder(Graph(), self.owner.torch_names, self.owner.functional_names).expr(e)
@@ -285,9 +366,13 @@ class _FunctionLowerer:
                 if isinstance(e, ast.UnaryOp):
                     return ast.UnaryOp(e.op, split(e.operand))
                 if isinstance(e, ast.Call) and not e.keywords and not any(isinstance(a, ast.Starred) for a in e.args):
+                    n_temps = len(temps)
                     cand = ast.Call(e.func, [split(a) for a in e.args], [])
                     if self._fusable(cand):
                         return cand
+                    # the call itself is hoisted: its arguments as written
+                    # (temporaries made for them would be dead)
+                    del temps[n_temps:]
                 name = f"__gm_t_{self.owner.next_tmp()}"
                 temps.append(ast.copy_location(ast.Assign(targets=[ast.Name(name, ast.Store())], value=e), s))
                 self.loads.append(((s.lineno, s.col_offset + 1), name))
@@ -484,6 +569,7 @@ class _FunctionLowerer:
         run: list[ast.stmt] = []
         hoist: list[ast.stmt] = []
         stmts = self._select_gemm_arms(self._route_gemms(self._split_calls(self._lower_dynamic_shape(stmts))))
+        stmts = self._rematerialise(stmts)
         for stmt in self._split_returns(stmts):
             cap = _is_capture(stmt)
             if cap is not None and run:
@@ -604,6 +690,7 @@ class _Lowerer:
         self.fallback_defs: list[ast.FunctionDef] = []
         self.dyn_lowered: list[tuple[str, str]] = []
         self.gemm_arms: list[tuple[str, str]] = []
+        self.rematerialised: list[str] = []
 
     def next_tmp(self) -> int:
         self._tmp = getattr(self, "_tmp", 0) + 1
@@ -667,6 +754,10 @@ class _Lowerer:
     def run(self) -> Lowered:
         fns = [n for n in ast.walk(self.tree) if isinstance(n, (ast.FunctionDef, ast.AsyncFunctionDef))]
         for fn in fns:
+            if fn.name.startswith("__") and fn.name.endswith("__") and fn.name != "__call__":
+                # constructors and other dunders run once on the host (module
+                # set-up: buffers, masks), not on the forward's hot path
+                continue
             # `@torch.compile` entry points (analysis.py entry mechanisms) are
             # executed by the B200 path itself: drop the Dynamo wrapper
             fn.decorator_list = [d for d in fn.decorator_list if not self._is_compile_decorator(d)]

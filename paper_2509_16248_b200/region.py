@@ -33,7 +33,8 @@ from .ir import Graph, Node, Unsupported, fold_host_predicates
 from .rowgen import RowPlan, has_row_ops
 
 SCRATCH_PARTIALS = 2432  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
-SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [speculative launches, mispredictions]
+SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [launches, mispredictions, exact entries]
+SCRATCH_CONF = 56       # GM_SCRATCH_CONF: int prediction confidence (adaptive speculation)
 SCRATCH_PRED = 288      # GM_SCRATCH_PRED: int predicted decisions
 SCRATCH_SUBCNT = 384    # GM_SCRATCH_SUBCNT: arrival sub-counters
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
@@ -396,9 +397,14 @@ class _Spec:
 
     def spec_stats(self) -> tuple[int, int]:
         """(launches, mispredictions) of a speculative region (syncs; tests
-        and bench)."""
+        and bench).  Launches count both entries; see exact_entries()."""
         v = self.scratch[SCRATCH_STATS:SCRATCH_STATS + 16].view(torch.int64).tolist()
         return int(v[0]), int(v[1])
+
+    def exact_entries(self) -> int:
+        """Launches of a speculative region that took the exact entry (the
+        confidence counter was below codegen.SPEC_CONFIDENT; syncs)."""
+        return int(self.scratch[SCRATCH_STATS + 16:SCRATCH_STATS + 24].view(torch.int64).item())
 
     def status(self) -> int:
         """Grid-barrier status word of the current scratch (a read of mapped

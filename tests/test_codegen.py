@@ -113,3 +113,19 @@ def test_unique_sum_cpu_form(dtype):
     got = ModuleRuntime.unique_sum(x)
     ref = x.unique().sum()
     assert math.isclose(float(got), float(ref), rel_tol=1e-2 if dtype == torch.bfloat16 else 1e-6)
+
+
+def test_speculative_region_has_adaptive_entries(programs):
+    """An adaptive speculative region: the confidence counter picks the
+    speculative sweep (then, on a miss, the restart from the first
+    mispredicted level, unstaged) or the exact entry, whose passes keep the
+    input on chip (register / shared-memory staging)."""
+    plan = _plan(programs, "bigbird_like", torch.bfloat16, (8, 1024, 768))
+    assert plan.spec
+    src = plan.source
+    assert "GM_SCRATCH_CONF" in src and "s_mode" in src
+    spec_part, exact_part = src.split("// exact entry")
+    assert "speculative pass" in spec_part and "if (s_miss <= 1)" in spec_part
+    # the restart re-reads global memory; the exact entry may stage
+    assert "rlds" not in spec_part.split("// misprediction")[1]
+    assert any(st in ("reg", "smem") for st in plan.stage.values()) or not plan.reductions

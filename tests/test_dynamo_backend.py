@@ -112,3 +112,58 @@ def test_backend_returns_fresh_outputs_and_keeps_autograd():
     y = c(x)
     y.sum().backward()
     assert torch.equal(x.grad, torch.full((1024,), 2.0, device="cuda"))
+
+
+@pytest.mark.parametrize("name", ["longformer_like", "moe_minicpm_like"])
+def test_gm_compile_keeps_residual_breaks_in_one_graph(programs, name):
+    """gm_compile traces `.item()` and dynamic-shape ops into the FX graph
+    (the residual breaks GraphMend reports unfixable): ONE graph reaches the
+    backend, its runtime asserts on unbacked sizes are dropped, and the
+    lowering turns the sites into device scalars / fixed-shape reductions.
+    CPU, eager lowered statements: equal to the transformed program."""
+    from paper_2509_16248_b200 import lowering
+
+    torch._dynamo.reset()
+    prog = programs[name]
+    fn = _callable(prog)
+    lows = []
+
+    def be(gm, ex):
+        lows.append(lowering.lower(dynamo._PRELUDE + dynamo._fx_source(gm))[0])
+        return dynamo.gm_b200_backend(gm, ex, allow_eager=True)
+
+    args = make_args(prog["inputs"][0]["args"], prog["inputs"][0]["seed"])
+    with torch._dynamo.config.patch(capture_scalar_outputs=True, capture_dynamic_output_shape_ops=True):
+        out = torch.compile(fn, backend=be)(*[a.clone() for a in args])
+    ref = fn(*[a.clone() for a in args])
+    assert len(lows) == 1
+    assert torch.allclose(out, ref, rtol=1e-6, atol=1e-7)
+    src = lows[0].source
+    assert "_assert_scalar" not in src and "sym_size" not in src
+    if name == "moe_minicpm_like":
+        assert len(lows[0].dynamic_shape_lowered) == 15
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["longformer_like", "moe_minicpm_like", "phi4_like", "qwen_audio_like"])
+def test_gm_compile_on_b200_is_one_sync_free_graph(programs, name):
+    """Through the torch.compile front door (gm_compile) the corpus programs
+    with residual breaks run as ONE FX graph -> one CUDA graph with no host
+    sync, matching the reference's CPU execution."""
+    from torch._dynamo.utils import counters
+
+    from paper_2509_16248_b200.dynamo import gm_compile
+
+    torch._dynamo.reset()
+    counters.clear()
+    prog = programs[name]
+    shapes = prog.get("scaled_shapes")
+    fn = _callable(prog)
+    c = gm_compile(fn)
+    for spec in prog["inputs"]:
+        args = make_args(spec["args"], spec["seed"], torch.float32, shapes)
+        ref, _ = orc.run_reference(prog["transformed"], prog["callable"], args, torch.float32)
+        with torch.no_grad():
+            out = c(*[a.cuda() for a in args])
+        assert_parity(out, ref, torch.float32, what=name)
+    assert counters["stats"]["unique_graphs"] == 1, dict(counters["stats"])

@@ -13,7 +13,7 @@ from parity import assert_parity, check_scalars, has_dense_contraction, torch_cu
 
 CORPUS = ["biogpt_like", "blenderbot_like", "flan_t5_like", "longformer_like", "moe_minicpm_like",
           "pegasus_like", "phi4_like", "qwen_audio_like"]
-WORKLOADS = ["toy", "bigbird_like", "bart_step", "gemm_arms"]
+WORKLOADS = ["toy", "bigbird_like", "bart_step", "gemm_arms", "bigbird_attn"]
 
 
 def _run(programs, name, idx, dtype=None, scaled=False):

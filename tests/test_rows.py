@@ -166,3 +166,16 @@ def f(x):
     low, _ = lowering.lower(text)
     assert "s = torch.softmax(x, -1).sum() > 0" in low.source
     assert all(not (ROW_OPS & {n.op for n in r.graph.nodes}) for r in low.regions)
+
+
+def test_bigbird_attn_scores_are_rematerialised(programs):
+    """workloads/bigbird_attn: `scores = QK^T / 8` feeds the predicate's grid
+    reduction and both softmax arms.  It is recomputed in the grid region and
+    the row region instead of being written and read back: the [8,12,1024,1024]
+    intermediate never exists."""
+    low, _ = lowering.lower(programs["bigbird_attn"]["transformed"])
+    fwd = [r for r in low.regions if r.name.startswith("forward")]
+    grid, rows = fwd[0], fwd[1]
+    assert grid.out_names[-1] == "__gm_pred_0" and "scores" not in grid.out_names
+    assert has_row_ops(rows.out_nodes) and rows.out_names == ["probs"]
+    assert "/ 8.0" in rows.source and "/ 8.0" in grid.source
