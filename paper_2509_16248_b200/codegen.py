@@ -806,6 +806,18 @@ class Plan:
         self.smem_bytes = 0
         self.decisions = self._decisions()
         self.spec = self._spec_ok()
+        # exact entry of a speculative region: inputs a later pass reads
+        # first are prefetched into L2 during pass 0 (prefetch.global.L2),
+        # so the pass after the grid barrier reads only L2 and writes HBM.
+        # Nothing is staged in shared memory: on B200 the 126 MB L2 holds
+        # these inputs, and the 96 KB-per-CTA stash measured slower on both
+        # entries (bigbird fp32: speculative hit 12.7 -> 15.2 us, exact
+        # 17.9 -> 18.9 us; tools/ab_spec.sh).
+        self.l2_prefetch: list[InputPlan] = []
+        if self.spec:
+            self.l2_prefetch = [ip for ip in self.inputs if ip.mode == MODE_FULL and ip.passes
+                                and min(ip.passes) > 0 and self._unguarded_in(ip, min(ip.passes))]
+            return
         if not self.reductions or self.npass < 2 or not self.K \
                 or os.environ.get("GM_STAGING", "1") == "0":
             return
@@ -1008,7 +1020,13 @@ class Plan:
             w("  return;")
             w("  }")
             self.stage, self.prefetch = saved
-            w("  // exact entry: every pass, inputs staged on chip")
+            w("  // exact entry: every pass; inputs first read after a grid barrier are pulled into L2 now")
+            for ip in self.l2_prefetch:
+                w(f"  for (int k = 0; k < {self.K}; ++k) {{")
+                w("    const i64 v = t0_ + (i64)k * T_;")
+                w(f"    if (v < VF_) gm::prefetch_l2((const char*)P.in[{ip.slot}].ptr + v * GM_VEC * "
+                  f"{DT_SIZE[ip.dtype]}, {nat.VEC * DT_SIZE[ip.dtype]});")
+                w("  }")
             prefetch()
         for p in range(self.npass):
             if p in self.hoisted and not self.spec:

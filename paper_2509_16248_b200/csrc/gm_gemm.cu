@@ -64,6 +64,7 @@ struct LtApi {
   decltype(&cublasLtMatmulDescSetAttribute) DescSet;
   decltype(&cublasLtMatrixLayoutCreate) LayoutCreate;
   decltype(&cublasLtMatrixLayoutDestroy) LayoutDestroy;
+  decltype(&cublasLtMatrixLayoutSetAttribute) LayoutSet;
   decltype(&cublasLtMatmulPreferenceCreate) PrefCreate;
   decltype(&cublasLtMatmulPreferenceDestroy) PrefDestroy;
   decltype(&cublasLtMatmulPreferenceSetAttribute) PrefSet;
@@ -102,6 +103,7 @@ int load_lt() {
   GM_LT(DescSet, "cublasLtMatmulDescSetAttribute");
   GM_LT(LayoutCreate, "cublasLtMatrixLayoutCreate");
   GM_LT(LayoutDestroy, "cublasLtMatrixLayoutDestroy");
+  GM_LT(LayoutSet, "cublasLtMatrixLayoutSetAttribute");
   GM_LT(PrefCreate, "cublasLtMatmulPreferenceCreate");
   GM_LT(PrefDestroy, "cublasLtMatmulPreferenceDestroy");
   GM_LT(PrefSet, "cublasLtMatmulPreferenceSetAttribute");
@@ -118,7 +120,8 @@ int load_lt() {
 }
 
 // one cached plan per problem
-using Key = std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int>;
+using Key = std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int, int64_t, int64_t, int64_t,
+                       int64_t>;
 struct Plan {
   cublasLtMatmulDesc_t desc = nullptr;
   cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
@@ -156,6 +159,34 @@ __global__ void gm_select_copy_tail_kernel(const unsigned char* __restrict__ pre
   const unsigned char* src = p ? a : b;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     dst[i] = src[i];
+}
+
+// dst (packed, row-major over `sizes`) = src (strides in 16-byte vectors,
+// innermost dim contiguous): one 16-byte vector per thread and step, the
+// vector's source offset decoded from its index (sizes[ndim-1] counts
+// vectors).  Stores are fully coalesced; loads are 16-byte pieces of the
+// source rows (a [b, n, h, d] -> [b, h, n, d] head split reads whole d rows).
+struct CopyDesc {
+  long long size[6];
+  long long stride[6];  // in 16-byte vectors
+  int ndim;
+};
+
+__global__ void __launch_bounds__(256) gm_copy_strided_kernel(const uint4* __restrict__ src,
+                                                              uint4* __restrict__ dst, const CopyDesc d,
+                                                              long long nvec) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
+       v += (long long)gridDim.x * blockDim.x) {
+    long long i = v, off = 0;
+#pragma unroll
+    for (int j = 5; j >= 0; --j) {
+      if (j >= d.ndim) continue;
+      const long long sz = d.size[j];
+      off += (i % sz) * d.stride[j];
+      i /= sz;
+    }
+    dst[v] = __ldg(src + off);
+  }
 }
 
 }  // namespace
@@ -205,15 +236,15 @@ size_t gm_gemm_version(void) {
 // an nn.Linear weight, row stride ldw) or B = w[K,N] (w_kn = 1, row stride
 // ldw), optional bias[N] and relu.  In cuBLASLt's column-major view that is
 // D(N x M) = op(W) (N x K) @ X (K x M).
-int gm_gemm_run(gm_gemm g, int dtype, int w_kn, const void* x, int64_t ldx, const void* w, int64_t ldw,
-                const void* bias, int relu, void* y, int64_t M, int64_t N, int64_t K, void* workspace,
-                size_t ws_bytes, void* stream) {
+static int gemm_impl(gm_gemm g, int dtype, int w_kn, const void* x, int64_t ldx, int64_t sx, const void* w,
+                     int64_t ldw, int64_t sw, const void* bias, int relu, void* y, int64_t sy, int64_t M, int64_t N,
+                     int64_t K, int64_t batch, void* workspace, size_t ws_bytes, void* stream) {
   if (!g || !x || !w || !y) return gfail(GM_E_INVALID, "gm_gemm_run: null argument");
-  if (M <= 0 || N <= 0 || K <= 0) return gfail(GM_E_INVALID, "gm_gemm_run: empty problem");
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return gfail(GM_E_INVALID, "gm_gemm_run: empty problem");
   const int t = lt_type(dtype);
   if (t < 0) return gfail(GM_E_INVALID, "gm_gemm_run: dtype %d", dtype);
   const int bias_on = bias != nullptr;
-  Key key{dtype, M, N, K, ldx, ldw, w_kn, bias_on, relu};
+  Key key{dtype, M, N, K, ldx, ldw, w_kn, bias_on, relu, batch, sx, sw, sy};
   std::lock_guard<std::mutex> lk(g->mu);
   auto it = g->plans.find(key);
   if (it == g->plans.end()) {
@@ -239,6 +270,16 @@ int gm_gemm_run(gm_gemm g, int dtype, int w_kn, const void* x, int64_t ldx, cons
       g_lt.LayoutCreate(&p.la, dt, K, N, ldw);
     g_lt.LayoutCreate(&p.lb, dt, K, M, ldx);
     g_lt.LayoutCreate(&p.lc, dt, N, M, N);
+    if (batch > 1) {
+      // strided batches: [batch][M][K] x [batch][K][N] -> [batch][M][N]
+      const int32_t bc = (int32_t)batch;
+      g_lt.LayoutSet(p.la, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
+      g_lt.LayoutSet(p.la, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sw, sizeof(sw));
+      g_lt.LayoutSet(p.lb, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
+      g_lt.LayoutSet(p.lb, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sx, sizeof(sx));
+      g_lt.LayoutSet(p.lc, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
+      g_lt.LayoutSet(p.lc, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sy, sizeof(sy));
+    }
     cublasLtMatmulPreference_t pref;
     g_lt.PrefCreate(&pref);
     size_t cap = ws_bytes;
@@ -266,6 +307,45 @@ int gm_gemm_run(gm_gemm g, int dtype, int w_kn, const void* x, int64_t ldx, cons
   const cublasStatus_t st = g_lt.Matmul(g->h, p.desc, &alpha, w, p.la, x, p.lb, &beta, y, p.lc, y, p.lc, &p.algo, workspace,
                              ws_bytes, (cudaStream_t)stream);
   if (st != 0) return gfail(GM_E_CUDA, "gm_gemm: cublasLtMatmul status %d", (int)st);
+  return GM_OK;
+}
+
+int gm_gemm_run(gm_gemm g, int dtype, int w_kn, const void* x, int64_t ldx, const void* w, int64_t ldw,
+                const void* bias, int relu, void* y, int64_t M, int64_t N, int64_t K, void* workspace,
+                size_t ws_bytes, void* stream) {
+  return gemm_impl(g, dtype, w_kn, x, ldx, 0, w, ldw, 0, bias, relu, y, 0, M, N, K, 1, workspace, ws_bytes, stream);
+}
+
+int gm_gemm_run_batched(gm_gemm g, int dtype, int w_kn, const void* x, int64_t ldx, int64_t stride_x, const void* w,
+                        int64_t ldw, int64_t stride_w, void* y, int64_t stride_y, int64_t M, int64_t N, int64_t K,
+                        int64_t batch, void* workspace, size_t ws_bytes, void* stream) {
+  return gemm_impl(g, dtype, w_kn, x, ldx, stride_x, w, ldw, stride_w, nullptr, 0, y, stride_y, M, N, K, batch,
+                   workspace, ws_bytes, stream);
+}
+
+int gm_copy_strided(const void* src, void* dst, int ndim, const int64_t* sizes, const int64_t* strides,
+                    int elem_bytes, void* stream) {
+  if (!src || !dst || !sizes || !strides || ndim < 1 || ndim > 6 || elem_bytes <= 0)
+    return gfail(GM_E_INVALID, "gm_copy_strided: bad argument");
+  const int64_t inner_bytes = sizes[ndim - 1] * elem_bytes;
+  if (strides[ndim - 1] != 1 || inner_bytes % 16 || ((uintptr_t)src | (uintptr_t)dst) & 15)
+    return gfail(GM_E_INVALID, "gm_copy_strided: the innermost dim must be contiguous, 16-byte sized and aligned");
+  CopyDesc d{};
+  d.ndim = ndim;
+  long long nvec = 1;
+  for (int j = 0; j < ndim; ++j) {
+    const int64_t sb = strides[j] * elem_bytes;
+    if (j < ndim - 1 && sb % 16) return gfail(GM_E_INVALID, "gm_copy_strided: stride %d not 16-byte aligned", j);
+    d.size[j] = j == ndim - 1 ? inner_bytes / 16 : sizes[j];
+    d.stride[j] = j == ndim - 1 ? 1 : sb / 16;
+    nvec *= d.size[j];
+  }
+  if (nvec == 0) return GM_OK;
+  long long blocks = (nvec + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gm_copy_strided_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, d, nvec);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return gfail(GM_E_CUDA, "gm_copy_strided: %s", cudaGetErrorString(e));
   return GM_OK;
 }
 

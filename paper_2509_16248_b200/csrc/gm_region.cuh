@@ -130,6 +130,18 @@ __device__ __forceinline__ float sigmoid(float a) {
   return y;
 }
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
+// exp(a) = 2^(a * log2 e) on the SFU (MUFU.EX2, subnormal results kept):
+// relative error ~2^-22 plus |a| * 2^-24 * ln 2 from rounding the product
+__device__ __forceinline__ float ex2(float a) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(a));
+  return y;
+}
+__device__ __forceinline__ float fexp(float a) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(a, 1.4426950408889634f)));
+  return y;
+}
 // Python-style `%` and `//` on floats, as torch's CPU kernels compute them
 // (remainder: fmod, then + b when the signs differ; floor_divide:
 // div_floor_floating — (a - fmod(a, b)) / b, corrected and rounded to an
@@ -502,6 +514,11 @@ __device__ __forceinline__ void sts16(u32 s, u32 a, u32 b, u32 c, u32 d) {
 }
 __device__ __forceinline__ void cp_async16(u32 s, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+// L2 prefetch of the 32-byte sector holding one vector
+__device__ __forceinline__ void prefetch_l2(const char* p, int bytes) {
+  (void)bytes;
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import math
 import threading
 
 import torch
@@ -34,7 +35,7 @@ WS_BYTES = 32 << 20
 _handles: dict = {}
 _ws: dict = {}
 _lock = threading.Lock()
-stats = {"gm_gemm": 0, "torch_gemm": 0, "select_gemm": 0, "select_both": 0}
+stats = {"gm_gemm": 0, "torch_gemm": 0, "select_gemm": 0, "select_both": 0, "gm_copy": 0}
 
 
 def _handle(dev: torch.device):
@@ -124,9 +125,88 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = No
     return _tag(y, "linear_relu" if relu else "linear", (x, weight, bias))
 
 
+def contiguous(t: torch.Tensor) -> torch.Tensor:
+    """t.contiguous() with the strided gather of gm_copy_strided when the
+    innermost dim is contiguous and 16-byte sized (the head split of
+    attention: [b, n, h, d] viewed as [b, h, n, d]), torch's copy otherwise."""
+    if t.is_contiguous():
+        return t
+    es = t.element_size()
+    if not (t.is_cuda and 1 <= t.dim() <= 6 and t.numel() > 0 and t.stride(-1) == 1
+            and (t.shape[-1] * es) % 16 == 0 and t.data_ptr() % 16 == 0
+            and all((st * es) % 16 == 0 for st in t.stride()[:-1])):
+        return t.contiguous()
+    dst = torch.empty(t.shape, dtype=t.dtype, device=t.device)
+    nd = t.dim()
+    sizes = (ctypes.c_int64 * nd)(*t.shape)
+    strides = (ctypes.c_int64 * nd)(*t.stride())
+    nat.count_launches()
+    nat.check(nat.lib().gm_copy_strided(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(dst.data_ptr()), nd, sizes,
+                                        strides, es, ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)),
+              "gm_copy_strided")
+    stats["gm_copy"] += 1
+    return dst
+
+
+def _batched_operand(t: torch.Tensor, rows: int, cols: int):
+    """`t` ([..., rows, cols], CUDA) as packed [batch, rows, cols] matrices
+    with one batch stride: (tensor, transposed) where `transposed` means the
+    memory holds [batch, cols, rows] (a `.transpose(-1, -2)` view, read with
+    op T).  When neither layout is a view (the head-split q / k / v of
+    attention) the orientation whose innermost dim is contiguous is gathered
+    (`contiguous`), so `k.transpose(-1, -2)` is read as k's rows with op T."""
+    tt = t.transpose(-1, -2)
+    for cand, trans in ((t, False), (tt, True)):
+        r, c = (cols, rows) if trans else (rows, cols)
+        try:
+            v = cand.view(-1, r, c)
+        except RuntimeError:
+            continue
+        if v.is_contiguous() and v.data_ptr() % 256 == 0:
+            return v, trans
+    if t.stride(-1) != 1 and tt.stride(-1) == 1:
+        return contiguous(tt).view(-1, cols, rows), True
+    return contiguous(t).view(-1, rows, cols), False
+
+
+def matmul_batched(a: torch.Tensor, b: torch.Tensor):
+    """torch.matmul of [..., M, K] @ [..., K, N] with equal batch dims (CUDA):
+    ONE strided-batched cuBLASLt GEMM (gm_gemm_run_batched) — fp32 on the
+    BF16x9 emulation instead of torch's SIMT SGEMM batches, bf16 / fp16 with
+    fp32 accumulation — on operands gathered by gm_copy_strided only when no
+    strided view exists."""
+    M, K = a.shape[-2:]
+    N = b.shape[-1]
+    a3, ta = _batched_operand(a, M, K)
+    if ta:
+        a3 = contiguous(a3.transpose(-1, -2))   # x must be row-major [M, K]
+    b3, tb = _batched_operand(b, K, N)
+    batch = a3.shape[0]
+    y = torch.empty(*a.shape[:-1], N, dtype=a.dtype, device=a.device)
+    dev = a.device
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ws = _workspace(dev)
+    nat.count_launches()
+    code = {torch.float32: nat.GM_F32, torch.bfloat16: nat.GM_BF16, torch.float16: nat.GM_F16}[a.dtype]
+    # w_kn=1: w memory is [K, N] row-major (op N); w_kn=0: [N, K] (op T)
+    nat.check(nat.lib().gm_gemm_run_batched(
+        _handle(dev), code, 0 if tb else 1, ctypes.c_void_p(a3.data_ptr()), K, M * K,
+        ctypes.c_void_p(b3.data_ptr()), K if tb else N, K * N, ctypes.c_void_p(y.data_ptr()), M * N, M, N, K, batch,
+        ctypes.c_void_p(ws.data_ptr()), WS_BYTES, ctypes.c_void_p(stream)), "gm_gemm_run_batched")
+    stats["gm_gemm"] += 1
+    return _tag(y, "matmul", (a, b))
+
+
 def matmul(a: torch.Tensor, b: torch.Tensor):
     """torch.matmul(a, b) / `a @ b`: an fp32 CUDA [.., M, K] @ [K, N] on
-    gm_gemm_run, anything else on torch's cuBLAS call."""
+    gm_gemm_run, [..., M, K] @ [..., K, N] with equal batch dims on
+    gm_gemm_run_batched, anything else on torch's cuBLAS call."""
+    if (a.dtype in (torch.float32, torch.bfloat16, torch.float16) and b.dtype == a.dtype and a.is_cuda
+            and b.device == a.device
+            and a.dim() >= 3 and b.dim() == a.dim() and a.shape[:-2] == b.shape[:-2]
+            and a.shape[-1] == b.shape[-2] and a.numel() > 0 and b.numel() > 0
+            and math.prod(a.shape[:-2]) < 2 ** 31):
+        return matmul_batched(a, b)
     if not (_fast(a, b) and b.dim() == 2 and a.dim() >= 2 and a.shape[-1] == b.shape[0] and b.shape[0] > 0
             and a.numel() > 0 and b.shape[1] > 0):
         stats["torch_gemm"] += 1

@@ -31,7 +31,10 @@ region before it, whose 0-d output the row kernel reads.
 
 Numerics follow torch's CPU kernels for the last dim (aten/src/ATen/native/
 cpu/SoftMaxKernel.cpp `_vec_softmax_lastdim` / `_vec_log_softmax_lastdim`,
-ReduceOps): max, then exp(x - max) in the input's float type, its sum, then
+ReduceOps): max, then exp(x - max) in the input's float type (gm::fexp: one
+MUFU.EX2 of (x - max) * log2(e), relative error <= 2e-6 for the arguments a
+softmax sees — inside the 1e-5 bound, and the SFU keeps the kernel on the
+HBM roofline where accurate expf made it ALU-bound), its sum, then
 x * (1 / sum) (softmax) or x - max - log(sum) (log_softmax); sums accumulate
 in fp32 per thread and fp64 across threads, rounded once to the dtype; mean
 = (float)sum / C rounded once.
@@ -41,6 +44,7 @@ from __future__ import annotations
 
 import hashlib
 import math
+import os
 
 import torch
 
@@ -87,6 +91,9 @@ class RowPlan(Plan):
         self.hoisted = {}
         self.decisions = []
         self.spec = False
+        self.stage = {ip.slot: "none" for ip in self.inputs}
+        self._preloaded = {}
+        self._tail = False
         self.source = self._emit_rows()
         digest = hashlib.sha1(self.source.encode()).hexdigest()[:16]
         self.kernel = f"gm_row_{digest}"
@@ -173,6 +180,7 @@ class RowPlan(Plan):
             raise Unsupported(f"row of {self.C} elements exceeds the on-chip row ({MAX_TPR * UMAX * 8})")
         self.TPR = tpr
         self.U = -(-nv_row // tpr)
+        self.full_vecs = self.vec8 and nv_row % tpr == 0
         self.threads = max(CTA_THREADS, tpr)
         self.RPC = self.threads // tpr
         self.grid = -(-self.R // self.RPC)
@@ -250,7 +258,8 @@ class RowPlan(Plan):
         if ip.mode == MODE_FULL:
             fn = "load8_gmem" if self.vec8 else "load8_elems"
         elif ip.mode == MODE_PERIODIC:
-            fn = "load8_periodic" if self.vec8 else "load8_periodic_elems"
+            fn = "load8_gmem" if self.vec8 else "load8_elems"
+            return f"gm::{fn}<{dt}>(P.in[{k}], pb{k} + c{u}, nv{u}, {dst});"
         else:
             fn = "load8_strided"
         return f"gm::{fn}<{dt}>(P.in[{k}], e{u}, nv{u}, {dst});"
@@ -281,6 +290,8 @@ class RowPlan(Plan):
         for s in self._used_scalars(nodes, guards):
             w(f"  const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")
             w(f"  const bool sb{s.uid} = s_scal[{self.slot[s.uid]}] != 0.0; (void)sb{s.uid};")
+            if (s.op == "free" and s.kind == "host") or (s.kind == "dscalar" and s.dtype == torch.bfloat16):
+                w(f"  const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
         w(f"  const int tr_ = threadIdx.x % {TPR};")
         w(f"  const i64 row_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
         w(f"  const bool rok_ = row_ < {self.R}ll;")
@@ -288,8 +299,18 @@ class RowPlan(Plan):
         w("  (void)tr_; (void)rok_;")
         for u in range(U):
             w(f"  const i64 c{u} = ((i64){u} * {TPR} + tr_) * GM_VEC;")
-            w(f"  const int nv{u} = rok_ ? (int)max(0ll, min((i64)GM_VEC, {self.C}ll - c{u})) : 0;")
+            if self.full_vecs:
+                # every vector of a row is full: lanes are valid iff the row is
+                w(f"  const int nv{u} = rok_ ? GM_VEC : 0;")
+            else:
+                w(f"  const int nv{u} = rok_ ? (int)max(0ll, min((i64)GM_VEC, {self.C}ll - c{u})) : 0;")
             w(f"  const i64 e{u} = rb_ + c{u}; (void)e{u}; (void)nv{u};")
+        # periodic inputs (a [.., C] tensor broadcast over the leading dims):
+        # the row's offset into the period, once per row
+        for ip in self.inputs:
+            if ip.mode == MODE_PERIODIC and ip.node.kind == "elem" and ip.node in nodes:
+                reps = self._periods[ip.slot] // self.C
+                w(f"  const i64 pb{ip.slot} = (row_ % {reps}ll) * {self.C}ll;")
         # inputs read once per row / once per launch
         for ip in self.inputs:
             if ip.node.kind != "elem" or ip.node not in nodes:
@@ -312,16 +333,20 @@ class RowPlan(Plan):
         TRUE = frozenset({frozenset()})
         first = [n for n in nodes if n.op == "free" and n.uid not in self.rowval
                  and not self._guard_expr(guards.get(n.uid, TRUE))]
+        self._plan_packing(nodes, roots)
+        pref, needs = self._pref, self._needs
         # every value is declared here: guarded blocks only assign
         for n in nodes:
             if n.uid in self.rowval:
                 if n.op != "free":
                     w(f"  float rs{n.uid} = 0.f;")
-            else:
+                continue
+            if "F" in needs[n.uid]:
                 w(f"  float {', '.join(f'n{n.uid}_{u}[GM_VEC]' for u in range(U))};")
+            if "P" in needs[n.uid]:
+                w(f"  u32 {', '.join(f'p{n.uid}_{u}[4]' for u in range(U))};")
         for n in first:
-            for u in range(U):
-                w("  " + self._free_full(n, u))
+            self._emit_node(w, n)
         rest = [n for n in nodes if n not in first]
         cur = None
         for n in rest:
@@ -341,6 +366,9 @@ class RowPlan(Plan):
             dt = DT_CODE[o.dtype]
             if o.uid in self.rowval:
                 w(f"  if (rok_ && tr_ == 0) gm::store_at<{dt}>(P.out[{k}], row_, rs{o.uid});")
+            elif pref.get(o.uid) == "P":
+                for u in range(U):
+                    w(f"  if (nv{u}) gm::stg_raw(P.out[{k}], e{u}, p{o.uid}_{u});")
             else:
                 fn = "store8" if self.vec8 else "store8_elems"
                 for u in range(U):
@@ -365,24 +393,100 @@ class RowPlan(Plan):
     def _inputs(self, args) -> None:
         super()._inputs(args)
         self._row_layout = {}
+        self._periods = {}
         for ip in self.inputs:
+            if ip.mode == MODE_PERIODIC:
+                self._periods[ip.slot] = args[ip.free_index].numel()
             if ip.mode == MODE_ROWIN:
                 t = args[ip.free_index]
                 self._row_layout[ip.slot] = self.row_offsets(t)
 
+    def _plan_packing(self, nodes: list[Node], roots: list[Node]) -> None:
+        """bf16 chains before / after the row operators stay packed (the
+        grid kernel's bf16x2 path, codegen.Plan._packed_plan / _node_code):
+        `scores * 0.125 + mask` is two `bf16x2` ops per element pair instead
+        of an unpack, two fp32 ops and two roundings per element.  Values
+        with one element per row stay fp32 registers.  A bf16 value that
+        only a packed consumer or a store reads skips its own rounding: the
+        pack (cvt.rn.bf16x2) is that rounding."""
+        full = [n for n in nodes if n.uid not in self.rowval]
+        pref = {n.uid: "F" for n in full}
+        if self.full_vecs and not os.environ.get("GM_NO_PACKED"):
+            cand = [n for n in full if n.op not in ROW_OPS]
+            pp = self._packed_plan(cand)
+            for n in cand:
+                if n.op == "free" and n.dtype == torch.bfloat16 and self._raw_ok(n):
+                    pp[n.uid] = "P"   # periodic inputs too: their vectors are aligned per row
+            for n in full:
+                if pp.get(n.uid) == "P" and not any(a.uid in self.rowval for a in n.args if a.kind == "elem"):
+                    pref[n.uid] = "P"
+        needs: dict[int, set] = {n.uid: {pref[n.uid]} for n in full}
+        f_cons: dict[int, bool] = {}
+        for n in nodes:
+            for a in n.args:
+                if a.kind != "elem" or a.uid in self.rowval:
+                    continue
+                if n.uid in self.rowval or n.op in ROW_OPS:
+                    needs[a.uid].add("F")
+                    f_cons[a.uid] = True
+                elif pref[n.uid] == "P" and not (n.op == "where" and a is n.args[0]):
+                    needs[a.uid].add("P")
+                else:
+                    needs[a.uid].add("F")
+                    f_cons[a.uid] = True
+        self._pref, self._needs, self._f_consumers = pref, needs, f_cons
+        # stores of a bf16 / f16 F value round it themselves (cvt.rn)
+        self._store_rounds = {o.uid for o in roots if o.uid not in self.rowval and pref[o.uid] == "F"
+                              and o.dtype in (torch.bfloat16, torch.float16)}
+
+    def _raw_ok(self, n: Node) -> bool:
+        """A full-size / periodic input read as raw aligned vectors."""
+        ip = self.in_by_uid.get(n.uid)
+        return (ip is not None and self.full_vecs and ip.mode in (MODE_FULL, MODE_PERIODIC)
+                and ip.dtype in (torch.float32, torch.bfloat16, torch.float16))
+
+    def _skip_round(self, n: Node) -> bool:
+        """`n`'s own rounding is redundant: every reader packs it (RN) or a
+        store of the same dtype converts it (RN) — and nothing reads the
+        fp32 lanes."""
+        if n.dtype not in (torch.bfloat16, torch.float16) or self._f_consumers.get(n.uid):
+            return False
+        return "P" in self._needs[n.uid] or n.uid in self._store_rounds
+
     def _emit_node(self, w, n: Node) -> None:
         U = self.U
+        pref, needs = self._pref, self._needs
         if n.op == "free":
             if n.uid in self.rowval:
                 return  # loaded above (rs<uid>)
+            ip = self.in_by_uid[n.uid]
+            if self._raw_ok(n):
+                # raw 16/32-byte vectors (no per-lane masking: a row is
+                # either valid, every vector full, or skipped)
+                dt, k = DT_CODE[ip.dtype], ip.slot
+                addr = "pb{k} + c{u}" if ip.mode == MODE_PERIODIC else "e{u}"
+                for u in range(U):
+                    a = addr.format(k=k, u=u)
+                    w(f"  gm::Raw<{dt}> rl{k}_{u} = {{}}; if (rok_) gm::rload<{dt}>(P.in[{k}], {a}, rl{k}_{u});")
+                for u in range(U):
+                    if "P" in needs[n.uid]:
+                        w(f"#pragma unroll\n  for (int j = 0; j < 4; ++j) p{n.uid}_{u}[j] = rl{k}_{u}.w[j];")
+                    if "F" in needs[n.uid]:
+                        w(f"  gm::rcvt<{dt}>(rl{k}_{u}, n{n.uid}_{u});")
+                return
             for u in range(U):
                 w("  " + self._free_full(n, u))
+                if "P" in needs[n.uid]:
+                    w(f"  gm::pack8(n{n.uid}_{u}, p{n.uid}_{u});")
             return
         if n.op in ROW_RED:
             self._emit_row_reduce(w, n)
             return
         if n.op in ROW_NORM:
             self._emit_row_norm(w, n)
+            if "P" in needs[n.uid]:
+                for u in range(U):
+                    w(f"  gm::pack8(n{n.uid}_{u}, p{n.uid}_{u});")
             return
         if n.uid in self.rowval:
             # one value per row: computed once per thread
@@ -394,7 +498,17 @@ class RowPlan(Plan):
             w("  }")
             return
         for u in range(U):
-            for line in self._elem_code(n, u):
+            if pref[n.uid] == "F":
+                self._no_round = self._skip_round(n)
+                try:
+                    lines = self._elem_code(n, u)
+                finally:
+                    self._no_round = False
+                if "P" in needs[n.uid]:
+                    lines.append(f"gm::pack8(n{n.uid}_{u}, p{n.uid}_{u});")
+            else:
+                lines = self._node_code(n, u, pref, needs)
+            for line in lines:
                 w("  " + line.replace("\n", "\n  "))
 
     def _row_stat(self, w, name: str, x: Node, op: str, expr=None) -> None:
@@ -402,16 +516,22 @@ class RowPlan(Plan):
         expr(x lane) over its valid lanes; sums: fp32 per thread, fp64 across
         threads, rounded once to fp32."""
         U, TPR = self.U, self.TPR
-        ident = {"max": "__int_as_float(0xff800000)", "min": "__int_as_float(0x7f800000)", "sum": "0.f"}[op]
+        ident = {"max": "__int_as_float(0xff800000)", "fmax": "__int_as_float(0xff800000)",
+                 "min": "__int_as_float(0x7f800000)", "sum": "0.f"}[op]
         w(f"  float {name}_t = {ident}; (void){name}_t;")
         for u in range(U):
             v = f"n{x.uid}_{u}[l]" if expr is None else expr(u)
             if op == "sum":
                 upd = f"{name}_t = gm::add({name}_t, {v});"
+            elif op == "fmax":
+                upd = f"{name}_t = fmaxf({name}_t, {v});"
             else:
                 upd = f"{name}_t = gm::n{op}({name}_t, {v});"
-            w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) if (l < nv{u}) {upd}")
-        code = {"sum": "GM_R_SUM", "max": "GM_R_MAX", "min": "GM_R_MIN"}[op]
+            # full vectors: every lane of a valid row is valid, and an
+            # invalid row (past R, loads read 0) is never stored
+            mask = "" if self.full_vecs else f"if (l < nv{u}) "
+            w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) {mask}{upd}")
+        code = {"sum": "GM_R_SUM", "max": "GM_R_MAX", "fmax": "GM_R_MAX", "min": "GM_R_MIN"}[op]
         w(f"  const float {name} = (float)gm::row_combine<{TPR}, {code}>((double){name}_t, s_rw);")
 
     def _emit_row_reduce(self, w, n: Node) -> None:
@@ -432,11 +552,23 @@ class RowPlan(Plan):
         x = n.args[0]
         U = self.U
         R = _round_f(n.dtype)
+        if self._skip_round(n):
+            R = ""
         m = f"mx{n.uid}"
-        self._row_stat(w, m, x, "max")
-        for u in range(U):
-            w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = "
-              f"expf(gm::sub(n{x.uid}_{u}[l], {m}));")
+        # the shift needs no NaN propagation: a NaN lane makes exp(x - m) and
+        # so the row's sum NaN, and every output NaN, as torch's propagating
+        # max does (one FMNMX per element instead of a compare and select)
+        self._row_stat(w, m, x, "fmax")
+        if n.op == "softmax":
+            # exp(x - max) = 2^(x·log2 e - max·log2 e): one FFMA + one MUFU.EX2
+            w(f"  const float ml{n.uid} = gm::mul({m}, 1.4426950408889634f);")
+            for u in range(U):
+                w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = "
+                  f"gm::ex2(__fmaf_rn(n{x.uid}_{u}[l], 1.4426950408889634f, -ml{n.uid}));")
+        else:
+            for u in range(U):
+                w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = "
+                  f"gm::fexp(gm::sub(n{x.uid}_{u}[l], {m}));")
         s = f"sm{n.uid}"
         self._row_stat(w, s, n, "sum")
         if n.op == "softmax":

@@ -119,3 +119,71 @@ def test_select_gemm_under_graph_capture():
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(y, gemm.matmul(x, wa if p else wb)), p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["qk", "pv", "contig", "odd"])
+def test_batched_matmul_fp32(case):
+    """Attention-shaped batched contractions (gm_gemm_run_batched, BF16x9):
+    scores = q @ k^T with head-split (non-viewable) operands, ctx = p @ v,
+    plain contiguous batches and odd sizes — at least as close to the fp64
+    product as torch's SIMT SGEMM."""
+    torch.manual_seed(0)
+    b, h, n, d = 2, 12, 256, 64
+    if case == "qk":
+        x = torch.randn(b, n, h, d).transpose(1, 2)
+        k = torch.randn(b, n, h, d).transpose(1, 2)
+        A, B = x, k.transpose(-1, -2)
+    elif case == "pv":
+        A = torch.softmax(torch.randn(b, h, n, n), -1)
+        B = torch.randn(b, n, h, d).transpose(1, 2)
+    elif case == "contig":
+        A, B = torch.randn(6, 100, 48), torch.randn(6, 48, 72)
+    else:
+        A, B = torch.randn(3, 5, 17, 33), torch.randn(3, 5, 33, 9)
+    ref64 = torch.matmul(A.double(), B.double())
+    torch.backends.cuda.matmul.allow_tf32 = False
+    c0 = gemm.stats["gm_gemm"]
+    y = gemm.matmul(A.cuda(), B.cuda())
+    assert gemm.stats["gm_gemm"] == c0 + 1, "the batched BF16x9 path did not run"
+    assert y.shape == ref64.shape and y.dtype == torch.float32
+    sg = torch.matmul(A.cuda(), B.cuda())
+    e_gm, _ = _errs(y, ref64)
+    e_sg, _ = _errs(sg, ref64)
+    assert e_gm <= 1.5 * e_sg + 1e-6, (e_gm, e_sg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16], ids=["fp32", "bf16", "fp16"])
+def test_copy_strided_is_contiguous(dtype):
+    """gm_copy_strided (the head split / merge gather) equals torch's
+    .contiguous() bit for bit; layouts it cannot take fall back to torch."""
+    torch.manual_seed(0)
+    x = torch.randn(2, 256, 12, 64).to(dtype).cuda()
+    for view in (x.transpose(1, 2), x.permute(2, 0, 1, 3), x[:, ::2].transpose(1, 2), x.transpose(1, 2)[..., :32]):
+        c0 = gemm.stats["gm_copy"]
+        y = gemm.contiguous(view)
+        assert torch.equal(y, view.contiguous()) and y.is_contiguous()
+        assert gemm.stats["gm_copy"] == c0 + 1
+    odd = x.transpose(-1, -2)                     # innermost dim strided: torch's copy
+    c0 = gemm.stats["gm_copy"]
+    assert torch.equal(gemm.contiguous(odd), odd.contiguous()) and gemm.stats["gm_copy"] == c0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16], ids=["bf16", "fp16"])
+def test_batched_matmul_half(dtype):
+    """bf16 / fp16 attention contractions through gm_gemm_run_batched: as
+    close to the fp64 product as torch's own cuBLAS call."""
+    torch.manual_seed(1)
+    b, h, n, d = 2, 12, 256, 64
+    q = torch.randn(b, n, h, d).transpose(1, 2).to(dtype)
+    k = torch.randn(b, n, h, d).transpose(1, 2).to(dtype)
+    ref64 = torch.matmul(q.double(), k.double().transpose(-1, -2))
+    c0 = gemm.stats["gm_gemm"]
+    y = gemm.matmul(q.cuda(), k.cuda().transpose(-1, -2))
+    assert gemm.stats["gm_gemm"] == c0 + 1 and y.dtype == dtype
+    t = torch.matmul(q.cuda(), k.cuda().transpose(-1, -2))
+    e_gm, _ = _errs(y, ref64)
+    e_t, _ = _errs(t, ref64)
+    assert e_gm <= 1.5 * e_t + 1e-6, (e_gm, e_t)
