@@ -167,23 +167,39 @@ __global__ void gm_select_copy_tail_kernel(const unsigned char* __restrict__ pre
 // vectors).  Stores are fully coalesced; loads are 16-byte pieces of the
 // source rows (a [b, n, h, d] -> [b, h, n, d] head split reads whole d rows).
 struct CopyDesc {
-  long long size[6];
-  long long stride[6];  // in 16-byte vectors
+  long long stride[6];    // in 16-byte vectors
+  unsigned size[6];
+  unsigned mul[6], shr[6];  // x / size = umulhi(x, mul) >> shr (32-bit index space)
   int ndim;
 };
 
+// round-up magic numbers for unsigned 32-bit division by d (d >= 1)
+static void fast_divmod(unsigned d, unsigned& mul, unsigned& shr) {
+  if (d == 1) { mul = 0; shr = 0; return; }
+  unsigned s = 0;
+  while ((1ull << s) < d) ++s;
+  mul = (unsigned)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  shr = s;
+}
+
+__device__ __forceinline__ unsigned fdiv(unsigned x, unsigned mul, unsigned shr) {
+  if (mul == 0 && shr == 0) return x;
+  const unsigned t = __umulhi(x, mul);
+  return (t + ((x - t) >> 1)) >> (shr - 1);
+}
+
 __global__ void __launch_bounds__(256) gm_copy_strided_kernel(const uint4* __restrict__ src,
                                                               uint4* __restrict__ dst, const CopyDesc d,
-                                                              long long nvec) {
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec;
-       v += (long long)gridDim.x * blockDim.x) {
-    long long i = v, off = 0;
+                                                              unsigned nvec) {
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
+    unsigned i = v;
+    long long off = 0;
 #pragma unroll
     for (int j = 5; j >= 0; --j) {
       if (j >= d.ndim) continue;
-      const long long sz = d.size[j];
-      off += (i % sz) * d.stride[j];
-      i /= sz;
+      const unsigned q = fdiv(i, d.mul[j], d.shr[j]);
+      off += (long long)(i - q * d.size[j]) * d.stride[j];
+      i = q;
     }
     dst[v] = __ldg(src + off);
   }
@@ -336,14 +352,18 @@ int gm_copy_strided(const void* src, void* dst, int ndim, const int64_t* sizes, 
   for (int j = 0; j < ndim; ++j) {
     const int64_t sb = strides[j] * elem_bytes;
     if (j < ndim - 1 && sb % 16) return gfail(GM_E_INVALID, "gm_copy_strided: stride %d not 16-byte aligned", j);
-    d.size[j] = j == ndim - 1 ? inner_bytes / 16 : sizes[j];
+    const long long sz = j == ndim - 1 ? inner_bytes / 16 : sizes[j];
+    if (sz <= 0) return GM_OK;
+    d.size[j] = (unsigned)sz;
     d.stride[j] = j == ndim - 1 ? 1 : sb / 16;
-    nvec *= d.size[j];
+    fast_divmod(d.size[j], d.mul[j], d.shr[j]);
+    nvec *= sz;
   }
-  if (nvec == 0) return GM_OK;
+  if (nvec >= (1ll << 31)) return gfail(GM_E_INVALID, "gm_copy_strided: more than 2^31 vectors");
   long long blocks = (nvec + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  gm_copy_strided_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, d, nvec);
+  gm_copy_strided_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, d,
+                                                                          (unsigned)nvec);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return gfail(GM_E_CUDA, "gm_copy_strided: %s", cudaGetErrorString(e));
   return GM_OK;

@@ -465,6 +465,24 @@ class ModuleRuntime:
         return gemm.linear(x, w, b)
 
     @staticmethod
+    def reshape(t, *shape):
+        """`t.reshape(*shape)`: the view when one exists, else a packed copy —
+        torch's semantics — made by gm_copy_strided when the innermost dim is
+        contiguous (attention's head merge `ctx.transpose(1, 2).reshape(b, n,
+        h)`), not torch's per-element permute copy."""
+        if not torch.is_tensor(t):
+            return t.reshape(*shape)
+        try:
+            return t.view(*shape)
+        except RuntimeError:
+            return gemm.contiguous(t).view(*shape)
+
+    @staticmethod
+    def contiguous(t):
+        """`t.contiguous()` through gemm.contiguous."""
+        return gemm.contiguous(t) if torch.is_tensor(t) else t.contiguous()
+
+    @staticmethod
     def select_gemm(pred, kind, then_ops, else_ops):
         """The one GEMM a GEMM-bearing predicated block needs (gemm.select_gemm)."""
         return gemm.select_gemm(pred, kind, then_ops, else_ops)

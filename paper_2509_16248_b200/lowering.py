@@ -437,6 +437,25 @@ class _FunctionLowerer:
             return ast.Call(rt("call"), [e.func, e.args[0]], [])
         return None
 
+    def _copy_call(self, e: ast.expr) -> ast.expr | None:
+        """`X.reshape(*shape)` / `X.contiguous()` (X a computed value, e.g.
+        attention's `matmul(p, v).transpose(1, 2).reshape(b, n, h)`) -> the
+        module runtime's reshape / contiguous (gm_copy_strided when a copy is
+        needed)."""
+        if not (isinstance(e, ast.Call) and isinstance(e.func, ast.Attribute) and not e.keywords
+                and not any(isinstance(a, ast.Starred) for a in e.args)):
+            return None
+        f = e.func
+        if attr_chain(f.value) is not None and attr_chain(f.value)[0] in (self.owner.torch_names
+                                                                       | self.owner.functional_names):
+            return None   # torch.reshape(...) itself: left as written
+        rt = lambda name: ast.Attribute(ast.Name(GM_RT, ast.Load()), name, ast.Load())  # noqa: E731
+        if f.attr == "reshape" and e.args:
+            return ast.Call(rt("reshape"), [f.value] + list(e.args), [])
+        if f.attr == "contiguous" and not e.args:
+            return ast.Call(rt("contiguous"), [f.value], [])
+        return None
+
     def _route_gemms(self, stmts: list[ast.stmt]) -> list[ast.stmt]:
         outer = self
 
@@ -448,6 +467,8 @@ class _FunctionLowerer:
                 node = super().generic_visit(node)
                 if isinstance(node, ast.expr):
                     r = outer._gemm_call(node)
+                    if r is None:
+                        r = outer._copy_call(node)
                     if r is not None:
                         return ast.copy_location(r, node)
                 return node

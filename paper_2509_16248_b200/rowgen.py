@@ -31,10 +31,10 @@ region before it, whose 0-d output the row kernel reads.
 
 Numerics follow torch's CPU kernels for the last dim (aten/src/ATen/native/
 cpu/SoftMaxKernel.cpp `_vec_softmax_lastdim` / `_vec_log_softmax_lastdim`,
-ReduceOps): max, then exp(x - max) in the input's float type (gm::fexp: one
-MUFU.EX2 of (x - max) * log2(e), relative error <= 2e-6 for the arguments a
-softmax sees — inside the 1e-5 bound, and the SFU keeps the kernel on the
-HBM roofline where accurate expf made it ALU-bound), its sum, then
+ReduceOps): max, then exp(x - max) in the input's float type (accurate expf
+for fp32 outputs; for 16-bit outputs one MUFU.EX2 of x·log2 e - max·log2 e,
+relative error <= 2e-6, far below their rounding — accurate expf made the
+bf16 kernel ALU-bound), its sum, then
 x * (1 / sum) (softmax) or x - max - log(sum) (log_softmax); sums accumulate
 in fp32 per thread and fp64 across threads, rounded once to the dtype; mean
 = (float)sum / C rounded once.
@@ -559,16 +559,23 @@ class RowPlan(Plan):
         # so the row's sum NaN, and every output NaN, as torch's propagating
         # max does (one FMNMX per element instead of a compare and select)
         self._row_stat(w, m, x, "fmax")
-        if n.op == "softmax":
-            # exp(x - max) = 2^(x·log2 e - max·log2 e): one FFMA + one MUFU.EX2
+        if n.op == "softmax" and n.dtype != torch.float32:
+            # 16-bit outputs: exp(x - max) = 2^(x·log2 e - max·log2 e), one
+            # FFMA + one MUFU.EX2 (the bf16 rounding dwarfs its ~2e-6 error;
+            # accurate expf made the bf16 kernel ALU-bound).  fp32 keeps
+            # torch's own sequence, x - max then an accurate expf: the fp32
+            # kernel is HBM-bound either way, and programs that threshold or
+            # deduplicate softmax outputs (moe_minicpm_like's nonzero /
+            # unique of x > 0.05) flip far fewer decisions
             w(f"  const float ml{n.uid} = gm::mul({m}, 1.4426950408889634f);")
             for u in range(U):
                 w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = "
                   f"gm::ex2(__fmaf_rn(n{x.uid}_{u}[l], 1.4426950408889634f, -ml{n.uid}));")
         else:
+            ex = "expf" if n.dtype == torch.float32 else "gm::fexp"
             for u in range(U):
                 w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = "
-                  f"gm::fexp(gm::sub(n{x.uid}_{u}[l], {m}));")
+                  f"{ex}(gm::sub(n{x.uid}_{u}[l], {m}));")
         s = f"sm{n.uid}"
         self._row_stat(w, s, n, "sum")
         if n.op == "softmax":
