@@ -237,3 +237,52 @@ def test_gemm_arms_become_one_selected_gemm(programs):
         mod, low = lowering.load(p["transformed"], allow_eager=True)
         out, t = orc.call_captured(getattr(mod, p["callable"]), args)
         assert t == rt and torch.equal(out, ref)
+
+
+def test_rematerialise_only_when_safe():
+    """lowering._rematerialise: a cheap elementwise value read by a grid
+    reduction AND a row operator is recomputed at each use — never when a
+    name it reads is rebound before its last use, when it is read in a
+    nested scope, or when it is assigned twice."""
+    base = '''
+import torch
+def f(t, b):
+    s = t / 8.0
+    p = s.abs().mean() > 0.3
+    y = torch.where(p, torch.softmax(s + b, -1), torch.softmax(s, -1))
+    return y
+'''
+    low, _ = lowering.lower(base)
+    assert "s = " not in low.source.split("def f")[1].split("regions")[0]
+    assert all("s" not in r.out_names for r in low.regions)
+    rebound = base.replace("    p = s.abs().mean() > 0.3\n", "    p = s.abs().mean() > 0.3\n    t = t * 2\n")
+    low, _ = lowering.lower(rebound)
+    assert any("s" in r.out_names for r in low.regions)
+    nested = base.replace("    return y\n", "    g = lambda: s\n    return y\n")
+    low, _ = lowering.lower(nested)
+    assert any("s" in r.out_names for r in low.regions)
+    # values the same: CPU eager of the lowered program
+    t, b = torch.randn(4, 8, 16), torch.randn(16)
+    mod, _ = lowering.load(base, allow_eager=True)
+    ns = {}
+    exec(compile(base, "f", "exec"), ns)
+    assert torch.equal(mod.f(t, b), ns["f"](t, b))
+
+
+def test_reshape_of_computed_values_routes_through_runtime():
+    text = '''
+import torch
+def f(x, w):
+    y = torch.matmul(x, w).transpose(1, 2).reshape(2, 8, 12)
+    z = x.contiguous()
+    return y, z
+'''
+    low, _ = lowering.lower(text)
+    src = low.source
+    assert "__gm_rt__.reshape(" in src and "__gm_rt__.contiguous(x)" in src
+    mod, _ = lowering.load(text, allow_eager=True)
+    x, w = torch.randn(2, 3, 8, 5), torch.randn(5, 4)
+    ns = {}
+    exec(compile(text, "f", "exec"), ns)
+    a, b = mod.f(x, w), ns["f"](x, w)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
