@@ -1,16 +1,26 @@
-# One GPU call that regenerates the round's evidence under gpurun_out/:
-# GPU tests, smoke, the default bench line, the reference arm, the config
-# sweep, the launch list, one ncu --set full capture of the region kernels,
-# the region timelines and the conditional-node cost.
+# One GPU call that regenerates a round's evidence under gpurun_out/ (copy
+# what is judged into profiles/<round>_*): the GPU suite, smoke, the default
+# bench line and the reference arm, every workload x dtype, the torch.compile
+# comparators (untransformed Inductor, and the gm_compile front door), the
+# launch list of the default bench and one `ncu --set full` capture of its
+# fused kernels.
 set -x
-python -m pytest tests -m gpu -q > gpurun_out/gputests.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-bash tools/sweep.sh > gpurun_out/sweep.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bb.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gm_region -s 2 -c 4 -o gpurun_out/prof_bb python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-GM_PROFILE=1 python tools/region_timeline.py --workload bigbird_like --dtype bf16 > gpurun_out/tl_bb_bf16.txt 2>&1
-GM_PROFILE=1 python tools/region_timeline.py --workload phi4_like --dtype fp32 > gpurun_out/tl_phi4_fp32.txt 2>&1
-timeout 120 ./tools/cond_node_bench > gpurun_out/cond_node.txt 2>&1
+R=${ROUND:-r02}
+timeout 2700 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${R}_gputests.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${R}_smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err
+timeout 900 python bench.py --impl reference > gpurun_out/${R}_bench_ref.json 2> gpurun_out/${R}_bench_ref.err
+: > gpurun_out/${R}_sweep.jsonl
+for w in bigbird_like bigbird_attn gemm_arms bart_step longformer_like phi4_like qwen_audio_like biogpt_like blenderbot_like flan_t5_like pegasus_like moe_minicpm_like; do
+  for d in bf16 fp32; do
+    timeout 600 python bench.py --workload $w --dtype $d --steps 100 --warmup 10 --no-compile --no-cpu-baseline 2>/dev/null >> gpurun_out/${R}_sweep.jsonl || echo "{\"workload\": \"$w\", \"dtype\": \"$d\", \"error\": true}" >> gpurun_out/${R}_sweep.jsonl
+  done
+done
+ALL=bigbird_like,bigbird_attn,gemm_arms,bart_step,longformer_like,phi4_like,qwen_audio_like,biogpt_like,blenderbot_like,flan_t5_like,pegasus_like,moe_minicpm_like
+timeout 1800 python tools/compare_inductor.py --workloads $ALL --dtype fp32 > gpurun_out/${R}_inductor_fp32.jsonl 2>/dev/null
+timeout 1800 python tools/compare_inductor.py --workloads $ALL --dtype bf16 > gpurun_out/${R}_inductor_bf16.jsonl 2>/dev/null
+timeout 1800 python tools/compare_frontdoor.py > gpurun_out/${R}_frontdoor.jsonl 2>/dev/null
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-compile > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'gm_(region|row)_' -s 4 -c 4 -o gpurun_out/${R}_prof python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compile > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/${R}_prof.ncu-rep gpurun_out/${R}_ncu_regions.json
 ls -la gpurun_out

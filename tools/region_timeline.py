@@ -1,6 +1,9 @@
 """Per-pass timeline of the fused region kernels of a workload (GM_PROFILE=1).
 
     GM_PROFILE=1 python tools/region_timeline.py --workload bigbird_like --dtype bf16
+
+Speculative regions: GM_SPEC_CONFIDENT=99 times the exact entry, =0 the
+speculative sweep (the input repeats, so every launch hits).
 """
 import argparse
 import json
@@ -15,7 +18,7 @@ os.environ.setdefault("GM_PROFILE", "1")
 def main():
     import torch
 
-    from bench import WORKLOADS, _inputs
+    from bench import WORKLOADS, _all_inputs
     from paper_2509_16248_b200 import compile_program
     from paper_2509_16248_b200.harness import programs
 
@@ -25,7 +28,7 @@ def main():
     a = ap.parse_args()
     dtype = {"bf16": torch.bfloat16, "fp32": torch.float32}[a.dtype]
     prog = programs()[a.workload]
-    x = [t.cuda() for t in _inputs(prog, WORKLOADS[a.workload][1], dtype)]
+    x = [t.cuda() for t in _all_inputs(prog, WORKLOADS[a.workload][1], dtype)[0]]
     ex, mod, low = compile_program(prog["transformed"], prog["callable"], dtype=dtype)
     ex(*x)
     torch.cuda.synchronize()
