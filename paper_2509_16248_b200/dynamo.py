@@ -117,15 +117,12 @@ def gm_compile(model, **kwargs):
     lowering turns them into device scalars and fixed-shape reductions
     (SURVEY §8f ranks 1-2).  The whole forward is then one FX graph, one
     CUDA graph, no host sync — as on the direct path (compile_program)."""
-    compiled = torch.compile(model, backend="gm_b200", **kwargs)
-
-    @functools.wraps(getattr(model, "forward", model))
-    def call(*args, **kw):
-        with torch._dynamo.config.patch(capture_scalar_outputs=True, capture_dynamic_output_shape_ops=True):
-            return compiled(*args, **kw)
-
-    call.compiled = compiled
-    return call
+    # Dynamo reads these when it traces (first call, recompiles); set once,
+    # process-wide, rather than entering a config patch on every call (a
+    # per-call patch costs more than the whole forward of small programs)
+    torch._dynamo.config.capture_scalar_outputs = True
+    torch._dynamo.config.capture_dynamic_output_shape_ops = True
+    return torch.compile(model, backend="gm_b200", **kwargs)
 
 
 try:  # `torch.compile(model, backend="gm_b200")`

@@ -431,7 +431,8 @@ class _FunctionLowerer:
             return ast.Call(rt("matmul"), list(e.args), [])
         is_f = (len(chain) == 2 and chain[0] in fn) or (len(chain) == 4 and chain[0] in tn
                                                         and chain[1:3] == ["nn", "functional"])
-        if is_f and chain[-1] == "linear" and len(e.args) in (2, 3):
+        is_c = len(chain) == 4 and chain[0] in tn and chain[1:3] == ["_C", "_nn"]   # Dynamo's FX spelling
+        if (is_f or is_c) and chain[-1] == "linear" and len(e.args) in (2, 3):
             return ast.Call(rt("linear"), list(e.args), [])
         if chain[0] == "self" and len(chain) >= 2 and len(e.args) == 1:
             return ast.Call(rt("call"), [e.func, e.args[0]], [])

@@ -14,7 +14,9 @@ term, measured rather than assumed: the accumulation order of a GEMM is
 unspecified on both sides (MKL on the CPU, cuBLAS here), so the absolute
 floor becomes max(floor, 2 * max|torch_cuda - ref|), where torch_cuda is
 stock PyTorch's own eager CUDA execution of the same transformed program
-(TF32 off).  I.e. the B200 path may deviate from the CPU oracle by at most
+(TF32 off).  Programs with softmax get the same term from the oracle run
+with fp64 softmaxes (`rowop_fp64_reference`): a program that thresholds or
+deduplicates softmax outputs moves under any last-bit change of them.  I.e. the B200 path may deviate from the CPU oracle by at most
 twice what PyTorch's own GPU execution of the same text deviates.  The
 harness's max-based form (max rel and max abs over the tensor) is reported
 in every failure message.
@@ -56,9 +58,11 @@ def ulp(r: torch.Tensor, dtype) -> torch.Tensor:
 
 
 def assert_parity(out: torch.Tensor, ref: torch.Tensor, dtype=torch.float32, what: str = "",
-                  noise: torch.Tensor | None = None):
-    """`noise`: stock PyTorch's CUDA output of the same program (only for
-    programs with dense contractions), see the module docstring."""
+                  noise=None):
+    """`noise`: stock PyTorch's CUDA output of the same program (programs
+    with dense contractions) and / or the fp64-row-operator oracle
+    (`rowop_fp64_reference`, programs with softmax), a tensor or a list;
+    see the module docstring."""
     out = out.detach().to("cpu")
     ref = ref.detach().to("cpu")
     assert out.shape == ref.shape, (what, out.shape, ref.shape)
@@ -73,10 +77,14 @@ def assert_parity(out: torch.Tensor, ref: torch.Tensor, dtype=torch.float32, wha
     else:
         floor = ulp(r, dtype)
     gemm_floor = 0.0
-    if noise is not None:
-        n = noise.detach().to("cpu").double()
+    for nz in ([] if noise is None else (noise if isinstance(noise, (list, tuple)) else [noise])):
+        if nz is None:
+            continue
+        n = nz.detach().to("cpu").double()
         finite = torch.isfinite(n) & torch.isfinite(r)
-        gemm_floor = 2.0 * float((n - r).abs()[finite].max()) if bool(finite.any()) else 0.0
+        if bool(finite.any()):
+            gemm_floor = max(gemm_floor, 2.0 * float((n - r).abs()[finite].max()))
+    if gemm_floor:
         floor = floor.clamp_min(gemm_floor)
     d = (o - r).abs()
     bad = (d > tol * r.abs()) & (d > floor)
@@ -117,6 +125,48 @@ def torch_cuda_reference(text: str, callable_name: str, args: list, dtype=None):
         return out.cpu() if torch.is_tensor(out) else out
     finally:
         torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = prev
+
+
+def has_row_reduction(text: str) -> bool:
+    """softmax / log_softmax in the program: a row reduction whose
+    accumulation order (and exp implementation) is unspecified."""
+    return "softmax(" in text
+
+
+def rowop_fp64_reference(text: str, callable_name: str, args: list, dtype=None):
+    """The oracle (CPU eager) with every softmax / log_softmax evaluated in
+    fp64 and rounded to its dtype — an implementation at least as accurate as
+    torch's.  Its deviation from the fp32 oracle measures how far the
+    program's output moves under last-bit changes of those row operators
+    (moe_minicpm_like thresholds and deduplicates softmax outputs: this
+    yardstick moves it 1.4e-5 relative); it is the noise term for programs
+    with row reductions, as torch CUDA's own run is for GEMMs."""
+    from oracle import executor as orc
+
+    saved = (torch.softmax, torch.log_softmax, torch.nn.functional.softmax, torch.nn.functional.log_softmax,
+             torch.Tensor.softmax, torch.Tensor.log_softmax)
+
+    def wrap(f):
+        def g(x, *a, **k):
+            k.pop("dtype", None)
+            return f(x.double(), *a, **k).to(x.dtype)
+        return g
+
+    torch.softmax, torch.log_softmax = wrap(saved[0]), wrap(saved[1])
+    torch.nn.functional.softmax, torch.nn.functional.log_softmax = wrap(saved[2]), wrap(saved[3])
+    torch.Tensor.softmax, torch.Tensor.log_softmax = wrap(saved[4]), wrap(saved[5])
+    try:
+        fn = orc.reference_callable(text, callable_name, dtype)
+        logging.disable(logging.CRITICAL)
+        try:
+            with torch.no_grad(), contextlib.redirect_stdout(io.StringIO()):
+                out = fn(*[a.clone() if torch.is_tensor(a) else a for a in args])
+        finally:
+            logging.disable(logging.NOTSET)
+        return out
+    finally:
+        (torch.softmax, torch.log_softmax, torch.nn.functional.softmax, torch.nn.functional.log_softmax,
+         torch.Tensor.softmax, torch.Tensor.log_softmax) = saved
 
 
 def has_dense_contraction(text: str) -> bool:

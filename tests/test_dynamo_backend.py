@@ -165,5 +165,9 @@ def test_gm_compile_on_b200_is_one_sync_free_graph(programs, name):
         ref, _ = orc.run_reference(prog["transformed"], prog["callable"], args, torch.float32)
         with torch.no_grad():
             out = c(*[a.cuda() for a in args])
-        assert_parity(out, ref, torch.float32, what=name)
+        from parity import has_row_reduction, rowop_fp64_reference
+
+        noise = rowop_fp64_reference(prog["transformed"], prog["callable"], args) \
+            if has_row_reduction(prog["transformed"]) else None
+        assert_parity(out, ref, torch.float32, what=name, noise=noise)
     assert counters["stats"]["unique_graphs"] == 1, dict(counters["stats"])

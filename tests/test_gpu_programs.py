@@ -9,7 +9,7 @@ import torch
 
 from oracle import executor as orc
 from paper_2509_16248_b200 import harness
-from parity import assert_parity, check_scalars, has_dense_contraction, torch_cuda_reference
+from parity import has_row_reduction, rowop_fp64_reference, assert_parity, check_scalars, has_dense_contraction, torch_cuda_reference
 
 CORPUS = ["biogpt_like", "blenderbot_like", "flan_t5_like", "longformer_like", "moe_minicpm_like",
           "pegasus_like", "phi4_like", "qwen_audio_like"]
@@ -26,9 +26,11 @@ def _run(programs, name, idx, dtype=None, scaled=False):
     out, text = harness.call_captured(ex, [a.cuda() for a in args])
     # branch decisions = the oracle's; predicate statistics within tolerance
     check_scalars(low, prog["transformed"], prog["callable"], args, dtype, what=f"{name}[{idx}]")
-    noise = None
+    noise = []
     if isinstance(ref_out, torch.Tensor) and has_dense_contraction(prog["transformed"]):
-        noise = torch_cuda_reference(prog["transformed"], prog["callable"], args, dtype)
+        noise.append(torch_cuda_reference(prog["transformed"], prog["callable"], args, dtype))
+    if isinstance(ref_out, torch.Tensor) and has_row_reduction(prog["transformed"]):
+        noise.append(rowop_fp64_reference(prog["transformed"], prog["callable"], args, dtype))
     return prog, ref_out, ref_text, out, text, ex, low, noise
 
 

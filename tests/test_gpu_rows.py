@@ -16,7 +16,7 @@ import torch
 from oracle import executor as orc
 from paper_2509_16248_b200 import compile_program, harness
 from paper_2509_16248_b200.rowgen import RowPlan
-from parity import assert_parity, torch_cuda_reference
+from parity import assert_parity, rowop_fp64_reference, torch_cuda_reference
 
 SOFTMAX_ARM = '''
 import torch
@@ -64,6 +64,7 @@ def f(x, b):
 def _run(text, args, dtype, expect_row=True):
     ref, _ = orc.call_captured(orc.reference_callable(text, "f"), list(args))
     noise = torch_cuda_reference(text, "f", list(args))
+    noise64 = rowop_fp64_reference(text, "f", list(args))
     ex, mod, low = compile_program(text, "f")
     out, _ = harness.call_captured(ex, [a.cuda() for a in args])
     torch.cuda.synchronize()
@@ -76,8 +77,9 @@ def _run(text, args, dtype, expect_row=True):
     outs = out if isinstance(out, tuple) else (out,)
     refs = ref if isinstance(ref, tuple) else (ref,)
     nz = noise if isinstance(noise, tuple) else (noise,)
-    for o, r, n in zip(outs, refs, nz):
-        assert_parity(o, r, dtype, what=f"{text.split(chr(10))[2]} {tuple(r.shape)}", noise=n)
+    nz64 = noise64 if isinstance(noise64, tuple) else (noise64,)
+    for o, r, n, n64 in zip(outs, refs, nz, nz64):
+        assert_parity(o, r, dtype, what=f"{text.split(chr(10))[2]} {tuple(r.shape)}", noise=[n, n64])
     return low
 
 
