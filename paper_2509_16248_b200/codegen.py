@@ -767,6 +767,164 @@ class Plan:
             return False
         return all(d.dtype == torch.bool for d in self.decisions)
 
+    # -- sampled branch prediction -------------------------------------------------------
+    SAMPLE_SCALED = ("sum", "mean", "norm", "count_nonzero")
+    SAMPLE_PLAIN = ("amax", "amin", "any", "all")
+
+    def _sample_ok(self) -> bool:
+        """Can every predicted decision be estimated from a sample?  Sums,
+        means, norms and counts scale with the sampled fraction; max / min /
+        any / all are taken over the sample as they are.  prod, argmax /
+        argmin and coordinate sums have no useful sample estimate: such
+        regions keep the last launch's decisions as their prediction."""
+        if os.environ.get("GM_SAMPLE", "1") == "0" or self.vfull < 1:
+            return False
+        return all(r.op in self.SAMPLE_SCALED + self.SAMPLE_PLAIN for r in self.reductions)
+
+    def _simple_decision(self, d: Node):
+        """(reduction, comparison, other operand, reduction on the left) when
+        decision `d` is a reduction compared with a host / constant scalar
+        (the transform's `__gm_pred_k = P.red() ⋈ c`), else None."""
+        if d.op not in ("gt", "ge", "lt", "le") or len(d.args) != 2:
+            return None
+        a, b = d.args
+        if a.op in REDUCE and b.kind == "host":
+            return a, d.op, b, True
+        if b.op in REDUCE and a.kind == "host":
+            return b, d.op, a, False
+        return None
+
+    def _emit_sample(self, w) -> None:
+        """Predict the decisions from a sample, inside every CTA, before
+        anything else (no grid barrier): the CTA evaluates the exact passes'
+        reductions over the same GM_THREADS vectors of the iteration space —
+        vector (t * 2654435761) mod VF_ for thread t, a golden-ratio scramble
+        that spreads the sample over rows and columns — combines them
+        CTA-wide, scales sums / counts by n / n_sampled, and runs the scalar
+        levels on the estimates.  Every CTA computes the same sample, so all
+        agree on the prediction.  The speculative sweep then verifies the
+        prediction exactly; a wrong one costs the restart, never a wrong
+        result.  Inputs whose decisions change from launch to launch (the
+        bench rotates three draws whose decisions differ) are predicted from
+        their own data instead of from the previous launch."""
+        nsamp = min(self.vfull, self.threads)
+        scale = float(self.n) / float(nsamp * nat.VEC)
+        w("  { // ---- sampled prediction of the branch decisions")
+        w("    __shared__ double s_w_[GM_WARPS + 1];")
+        w("    __shared__ double s_m1_[GM_MAX_RED], s_m2_[GM_MAX_RED];  // sample moments (unscaled)")
+        if self.vfull <= self.threads:
+            w("    const i64 vs_ = threadIdx.x;")
+        else:
+            w("    const i64 vs_ = (i64)(((u64)threadIdx.x * 2654435761ull) % (u64)VF_);")
+        w("    const bool sok_ = vs_ < VF_;")
+        w("    const i64 es = vs_ * GM_VEC;")
+        w("    const int nvs = sok_ ? GM_VEC : 0; (void)nvs;")
+        w("    const i64 les = 0; (void)les;")
+        self._tail = True   # free inputs read with per-call gmem loads (e/nv)
+        try:
+            for p in range(self.npass):
+                reds = [r for r in self.pass_reds[p]]
+                feeds = [d for d in self.decisions if self.avail[d.uid] > p]
+                if not reds or not feeds:
+                    continue
+                roots = [r.args[0] for r in reds]
+                nodes = self._nodes(roots)
+                guards = self._guards_roots(roots)
+                w(f"    {{ // sample of pass {p}")
+                for sc in self._used_scalars(nodes, guards):
+                    w(f"      const float sf{sc.uid} = (float)s_scal[{self.slot[sc.uid]}]; (void)sf{sc.uid};")
+                    w(f"      const bool sb{sc.uid} = s_scal[{self.slot[sc.uid]}] != 0.0; (void)sb{sc.uid};")
+                for ip in self.inputs:
+                    if ip.mode == MODE_SCALAR and ip.node.kind == "elem" and ip.node in nodes:
+                        w(f"      const float sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
+                for n in nodes:
+                    w(f"      float n{n.uid}_s[GM_VEC] = {{}};")
+                cur = None
+                for n in nodes:
+                    g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
+                    if g != cur:
+                        if cur:
+                            w("      }")
+                        if g:
+                            w(f"      if ({g}) {{")
+                        cur = g
+                    for line in self._elem_code(n, "s"):
+                        w("      " + line.replace("\n", "\n      "))
+                if cur:
+                    w("      }")
+                for r in reds:
+                    k = self.red_index[r.uid]
+                    x = f"n{r.args[0].uid}_s"
+                    op = RED_OP[r.op]
+                    if r.op in self.SAMPLE_SCALED:
+                        # first and second moments of the summed term (x, x != 0, or x^2 for norm)
+                        term = {"count_nonzero": f"(({x}[l] != 0.f) ? 1.0 : 0.0)",
+                                "norm": f"((double){x}[l] * (double){x}[l])"}.get(r.op, f"(double){x}[l]")
+                        w(f"      double t{k}_ = 0.0, q{k}_ = 0.0;")
+                        w(f"      for (int l = 0; l < nvs; ++l) {{ const double z_ = {term}; t{k}_ += z_; q{k}_ += z_ * z_; }}")
+                        w(f"      const double v{k}_ = gm::cta_combine(GM_R_SUM, t{k}_, s_w_) * {scale!r};")
+                        w(f"      const double m{k}_ = gm::cta_combine(GM_R_SUM, q{k}_, s_w_);")
+                        w(f"      if (threadIdx.x == 0) {{ s_red[{k}] = v{k}_; s_m1_[{k}] = v{k}_ / {scale!r}; "
+                          f"s_m2_[{k}] = m{k}_; }}")
+                    else:
+                        w(f"      float t{k}_ = gm::acc8({op}, gm::acc_identity({op}), {x}, nvs);")
+                        w(f"      const double v{k}_ = gm::cta_combine({op}, sok_ ? (double)t{k}_ : "
+                          f"gm::red_identity({op}), s_w_);")
+                        w(f"      if (threadIdx.x == 0) s_red[{k}] = v{k}_;")
+                w("      if (threadIdx.x == 0) {")
+                for r in reds:
+                    w("        " + self._finish_reduction(r, self.red_index[r.uid]))
+                for n in self.scalars:
+                    if self.avail[n.uid] == p + 1 and n.op not in REDUCE:
+                        w("        " + self._scalar_code(n))
+                w("      }")
+                w("      __syncthreads();")
+                w("    }")
+        finally:
+            self._tail = False
+        # Per-launch certification: a decision `red ⋈ c` is certain when the
+        # sample estimate is more than 4 standard errors from c (sums, means,
+        # counts, norms), or when the sample max / min already decides it.
+        # Every decision certain -> speculate; otherwise the exact entry.
+        nsmp = float(nsamp * nat.VEC)
+        # a sample that covers the whole iteration space has no sampling error
+        exact_sample = nsamp == self.vfull and self.n == self.vfull * nat.VEC
+        w("    if (threadIdx.x == 0) {")
+        w("      int cert_ = 1;")
+        for j, d in enumerate(self.decisions):
+            w(f"      s_pred[{j}] = s_scal[{self.slot[d.uid]}] != 0.0 ? 1 : 0;")
+            form = self._simple_decision(d)
+            if form is None:
+                continue
+            r, cmp, c, red_left = form
+            k = self.red_index[r.uid]
+            est = f"s_scal[{self.slot[r.uid]}]"
+            cv = self._sv(c)
+            if r.op in self.SAMPLE_SCALED:
+                w("      {")
+                w(f"        const double mu_ = s_m1_[{k}] / {nsmp!r}, var_ = fmax(s_m2_[{k}] / {nsmp!r} - mu_ * mu_, 0.0);")
+                w(f"        double se_ = {'0.0 * ' if exact_sample else ''}sqrt(var_ / {nsmp!r});")
+                if r.op in ("sum", "count_nonzero"):
+                    w(f"        se_ *= {float(self.n)!r};")
+                elif r.op == "norm":
+                    w(f"        se_ = se_ * {float(self.n)!r} / (2.0 * fmax({est}, 1e-30));")
+                w(f"        if (!(fabs({est} - ({cv})) > 4.0 * se_ + 1e-12 * fabs({cv}))) cert_ = 0;")
+                w("      }")
+            else:
+                # a sample's max (any) bounds the true one from below, its
+                # min (all) from above: `max > c` is certain once the sample
+                # exceeds c, `max < c` once the sample does not
+                up = r.op in ("amax", "any")
+                gt = (cmp in ("gt", "ge")) == red_left
+                if up == gt:
+                    w(f"      if (!s_pred[{j}]) cert_ = 0;")
+                else:
+                    w(f"      if (s_pred[{j}]) cert_ = 0;")
+        w("      s_cert_ = cert_;")
+        w("    }")
+        w("    __syncthreads();")
+        w("  }")
+
     # -- launch layout and staging ---------------------------------------------------
     def _plan_layout(self) -> None:
         """Grid, vectors per thread and staging, decided from the shape and
@@ -814,6 +972,7 @@ class Plan:
         # entries (bigbird fp32: speculative hit 12.7 -> 15.2 us, exact
         # 17.9 -> 18.9 us; tools/ab_spec.sh).
         self.l2_prefetch: list[InputPlan] = []
+        self.sampled = self.spec and self._sample_ok()
         if self.spec:
             self.l2_prefetch = [ip for ip in self.inputs if ip.mode == MODE_FULL and ip.passes
                                 and min(ip.passes) > 0 and self._unguarded_in(ip, min(ip.passes))]
@@ -1001,6 +1160,14 @@ class Plan:
             w(f"    s_mode = c_ >= {SPEC_CONFIDENT} ? 1 : 0;")
             w("  }")
             self._emit_scalar_level(w, 0)
+            if self.sampled:
+                # sampled regions: the sample certifies (or not) THIS launch's
+                # decisions; the counter only guards against a predictor that
+                # keeps missing (a miss clears it, certified launches raise it)
+                w("  __shared__ int s_cert_;")
+                self._emit_sample(w)
+                w("  if (threadIdx.x == 0) s_mode = (s_cert_ && s_mode) ? 1 : 0;")
+                w("  __syncthreads();")
             w("  if (s_mode) {")
             saved = (self.stage, self.prefetch)
             self.stage = {k: "none" for k in self.stage}
@@ -1074,9 +1241,14 @@ class Plan:
             else:
                 w(f"{ind}  st_[2] += 1;")
                 w(f"{ind}  int same_ = 1;")
+                ref = "s_pred" if self.sampled else "pred_"
                 for j, d in enumerate(self.decisions):
-                    w(f"{ind}  same_ &= ((s_scal[{self.slot[d.uid]}] != 0.0) == (pred_[{j}] != 0)) ? 1 : 0;")
-                w(f"{ind}  *conf_ = same_ ? min(*conf_ + 1, {SPEC_CONF_MAX}) : 0;")
+                    w(f"{ind}  same_ &= ((s_scal[{self.slot[d.uid]}] != 0.0) == ({ref}[{j}] != 0)) ? 1 : 0;")
+                if self.sampled:
+                    # an uncertified launch says nothing about the predictor
+                    w(f"{ind}  if (s_cert_) *conf_ = same_ ? min(*conf_ + 1, {SPEC_CONF_MAX}) : 0;")
+                else:
+                    w(f"{ind}  *conf_ = same_ ? min(*conf_ + 1, {SPEC_CONF_MAX}) : 0;")
             if mode in ("miss", "exact"):
                 for j, d in enumerate(self.decisions):
                     w(f"{ind}  pred_[{j}] = (s_scal[{self.slot[d.uid]}] != 0.0) ? 1 : 0;")
@@ -1100,7 +1272,11 @@ class Plan:
         # data loads are issued (`late`), so their round trip overlaps them
         late: list[str] = []
         for s in self._used_scalars(elem_nodes, guards):
-            if spec and self.avail.get(s.uid, 0) >= 1:
+            if spec and self.avail.get(s.uid, 0) >= 1 and self.sampled:
+                j = self.decisions.index(s)
+                w(f"    const bool sb{s.uid} = s_pred[{j}] != 0; const float sf{s.uid} = sb{s.uid} ? 1.f : 0.f; "
+                  f"(void)sf{s.uid};")
+            elif spec and self.avail.get(s.uid, 0) >= 1:
                 j = self.decisions.index(s)
                 w(f"    float sf{s.uid} = 0.f; bool sb{s.uid} = false; (void)sf{s.uid}; (void)sb{s.uid};")
                 late.append(f"{{ int pd_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(pd_) : \"l\"(pred_ + {j})); "

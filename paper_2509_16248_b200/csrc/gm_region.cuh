@@ -1153,6 +1153,23 @@ __device__ __forceinline__ float acc8(int op, float acc, const float (&x)[8], in
   }
   return acc;
 }
+// CTA-wide combine (every thread returns the result); s_w holds GM_WARPS
+// doubles.  Used by the sampled branch predictor (codegen.Plan._emit_sample).
+__device__ __forceinline__ double cta_combine(int op, double v, double* s_w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_combine(op, v);
+  if (lane == 0) s_w[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < GM_WARPS ? s_w[lane] : red_identity(op);
+    t = warp_combine(op, t);
+    if (lane == 0) s_w[GM_WARPS] = t;
+  }
+  __syncthreads();
+  const double r = s_w[GM_WARPS];
+  __syncthreads();
+  return r;
+}
 __device__ __forceinline__ float acc_identity(int op) {
   switch (op) {
     case GM_R_MAX: return -__int_as_float(0x7f800000);

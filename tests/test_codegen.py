@@ -130,3 +130,29 @@ def test_speculative_region_has_adaptive_entries(programs):
     # its select pass reads first (`hidden`) into L2 during the norm pass
     assert plan.smem_bytes == 0 and all(st == "none" for st in plan.stage.values())
     assert "prefetch_l2" in exact_part and "prefetch_l2" not in spec_part
+
+
+def test_sampled_prediction(programs):
+    """Speculative regions whose reductions have a sample estimate (sum,
+    mean, norm, count, max, min, any, all) predict their decisions from a
+    CTA-local sample of the input; prod / argmax predicates keep the last
+    launch's decisions."""
+    plan = _plan(programs, "bigbird_like", torch.float32, (8, 1024, 768))
+    assert plan.spec and plan.sampled
+    src = plan.source
+    assert "sampled prediction" in src and "2654435761" in src and "cta_combine" in src
+    # the speculative sweep reads the sampled prediction, not the scratch
+    spec = src.split("// ---- speculative pass")[1].split("grid_arrive")[0]
+    assert "s_pred[0] != 0" in spec and "pred_ + 0" not in spec
+    text = '''
+import torch
+def f(x):
+    __gm_pred_0 = x.prod() > 0
+    __gm_then_y_0 = x * 2
+    y = torch.where(__gm_pred_0, __gm_then_y_0, x)
+    return y
+'''
+    low, _ = lowering.lower(text)
+    r = low.regions[0]
+    p = codegen.Plan(r.graph, r.out_nodes, [torch.randn(8, 1024, 768)], allow_cpu=True)
+    assert p.spec and not p.sampled and "sampled prediction" not in p.source

@@ -159,3 +159,41 @@ def test_every_entry_is_bit_identical(programs, mode):
             (l1, m1), e1 = r.last_spec.spec_stats(), r.last_spec.exact_entries()
             assert l1 == l0 + 1
             assert (m1 - m0, e1 - e0) == {"hit": (0, 0), "miss": (1, 0), "exact": (0, 1)}[mode], (name, mode)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,dtype,shapes", [("bigbird_like", torch.float32, None),
+                                               ("bigbird_like", torch.bfloat16, None),
+                                               ("phi4_like", torch.float32, [[8, 1024, 768]])])
+def test_rotating_inputs_are_predicted_from_their_data(programs, name, dtype, shapes):
+    """The bench's rotation (three manifest draws whose decisions differ, in
+    turn): the sampled predictor gets every launch right once its confidence
+    is built, so the regions speculate and hit instead of running their
+    exact passes — and every output still matches the first output for its
+    input bit for bit."""
+    prog = programs[name]
+    xs = [[a.cuda() for a in orc.make_args(s["args"], s["seed"], dtype, shapes)] for s in prog["inputs"]]
+    ex, mod, low, _ = harness.b200_program(name, dtype=dtype)
+    entry = ex.prepare(*xs[0])
+    firsts = []
+    for x in xs:
+        entry.load(x)
+        firsts.append(entry.run().clone())
+    spec = [r.last_spec for r in low.regions if r.last_spec is not None and r.last_spec.plan.spec]
+    assert spec and all(s.plan.sampled for s in spec)
+    base = [(s.spec_stats(), s.exact_entries()) for s in spec]
+    n = 30
+    for i in range(n):
+        entry.load(xs[i % 3])
+        out = entry.run()
+        assert torch.equal(out, firsts[i % 3])
+    torch.cuda.synchronize()
+    ex.flush()
+    for s, ((l0, m0), e0) in zip(spec, base):
+        (l1, m1), e1 = s.spec_stats(), s.exact_entries()
+        assert l1 - l0 == n
+        assert m1 - m0 == 0, (s.name, m1 - m0, e1 - e0)
+        # bigbird's margins are >= 10 standard errors of the sample: every
+        # launch is certified; phi4's randn draw sums to ~0 (its decisions
+        # are a coin toss for any sample) and takes the exact entry
+        assert e1 - e0 <= (2 if name == "bigbird_like" else 2 + n // 3), (s.name, e1 - e0)
