@@ -695,30 +695,31 @@ def _live_kernel_ms(ex, low, xs_dev, flush, dev, steps: int) -> dict:
 
 def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5, mode: str = "hit") -> float:
     """Average duration (ms) of one region launch with a cold L2.  For a
-    speculative region `mode` picks the path every launch takes: "hit"
-    (speculation on the correct decisions), "miss" (speculation on the wrong
-    decisions, then the restart) or "exact" (the exact staged entry)."""
+    speculative region `mode` picks the path every launch takes through the
+    scratch's diagnostics word: "hit" (speculation on the predicted
+    decisions — the sampled or the last launch's, both right here), "miss"
+    (speculation on every decision flipped, then the restart) or "exact"
+    (the exact entry)."""
     import torch
 
     nd = len(spec.plan.decisions) if spec.plan.spec else 0
-    from paper_2509_16248_b200.region import SCRATCH_CONF, SCRATCH_PRED, scratch_owner
+    from paper_2509_16248_b200.region import FORCE_EXACT, FORCE_SPEC, SCRATCH_FORCE, SCRATCH_PRED, scratch_owner
 
     owner = object()   # this measurement's own barrier scratch, zeroed before the captures
-    want_pred = want_conf = None
+    want_pred = want_force = None
     if nd:
         vals = spec.scalars()
         dec = [1 if vals[spec.plan.slot[d.uid]] != 0.0 else 0 for d in spec.plan.decisions]
-        if mode == "miss":
-            dec = [1 - v for v in dec]
-        want_pred = torch.tensor(dec, dtype=torch.int32, device=dev)
-        want_conf = torch.tensor([0 if mode == "exact" else 3], dtype=torch.int32, device=dev)
+        want_pred = torch.tensor(dec, dtype=torch.int32, device=dev)   # history predictor: right
+        word = {"hit": FORCE_SPEC, "miss": FORCE_SPEC | ((1 << nd) - 1), "exact": FORCE_EXACT}[mode]
+        want_force = torch.tensor([word], dtype=torch.int32, device=dev)
 
     side = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(side), scratch_owner(owner):
         spec.run(args, pdl=False)  # warm (allocator, module, this owner's scratch)
         pred = spec.scratch[SCRATCH_PRED: SCRATCH_PRED + 4 * nd].view(torch.int32) if nd else None
-        conf = spec.scratch[SCRATCH_CONF: SCRATCH_CONF + 4].view(torch.int32) if nd else None
+        fw = spec.scratch[SCRATCH_FORCE: SCRATCH_FORCE + 4].view(torch.int32) if nd else None
     torch.cuda.current_stream(dev).wait_stream(side)
     torch.cuda.synchronize(dev)
     g_both, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -727,7 +728,7 @@ def _time_kernel_flushed(spec, args, flush, dev, reps: int = 20, trials: int = 5
     def force():
         if want_pred is not None:
             pred.copy_(want_pred)
-            conf.copy_(want_conf)
+            fw.copy_(want_force)
 
     with torch.cuda.graph(g_both), scratch_owner(owner):
         for _ in range(reps):

@@ -809,8 +809,16 @@ class Plan:
         their own data instead of from the previous launch."""
         nsamp = min(self.vfull, self.threads)
         scale = float(self.n) / float(nsamp * nat.VEC)
+        # the speculative sweep's unguarded inputs start their way into L2
+        # now, overlapping the sample pass (fire-and-forget prefetches)
+        for ip in self._preload_inputs("spec"):
+            w(f"  for (int k = 0; k < {self.K}; ++k) {{")
+            w("    const i64 v = t0_ + (i64)k * T_;")
+            w(f"    if (v < VF_) gm::prefetch_l2((const char*)P.in[{ip.slot}].ptr + v * GM_VEC * "
+              f"{DT_SIZE[ip.dtype]}, {nat.VEC * DT_SIZE[ip.dtype]});")
+            w("  }")
         w("  { // ---- sampled prediction of the branch decisions")
-        w("    __shared__ double s_w_[GM_WARPS + 1];")
+        w("    __shared__ double s_w_[2 * GM_WARPS + 2];")
         w("    __shared__ double s_m1_[GM_MAX_RED], s_m2_[GM_MAX_RED];  // sample moments (unscaled)")
         if self.vfull <= self.threads:
             w("    const i64 vs_ = threadIdx.x;")
@@ -862,8 +870,9 @@ class Plan:
                                 "norm": f"((double){x}[l] * (double){x}[l])"}.get(r.op, f"(double){x}[l]")
                         w(f"      double t{k}_ = 0.0, q{k}_ = 0.0;")
                         w(f"      for (int l = 0; l < nvs; ++l) {{ const double z_ = {term}; t{k}_ += z_; q{k}_ += z_ * z_; }}")
-                        w(f"      const double v{k}_ = gm::cta_combine(GM_R_SUM, t{k}_, s_w_) * {scale!r};")
-                        w(f"      const double m{k}_ = gm::cta_combine(GM_R_SUM, q{k}_, s_w_);")
+                        w(f"      double v{k}_ = t{k}_, m{k}_ = q{k}_;")
+                        w(f"      gm::cta_sum2(v{k}_, m{k}_, s_w_);")
+                        w(f"      v{k}_ *= {scale!r};")
                         w(f"      if (threadIdx.x == 0) {{ s_red[{k}] = v{k}_; s_m1_[{k}] = v{k}_ / {scale!r}; "
                           f"s_m2_[{k}] = m{k}_; }}")
                     else:
@@ -910,16 +919,12 @@ class Plan:
                     w(f"        se_ = se_ * {float(self.n)!r} / (2.0 * fmax({est}, 1e-30));")
                 w(f"        if (!(fabs({est} - ({cv})) > 4.0 * se_ + 1e-12 * fabs({cv}))) cert_ = 0;")
                 w("      }")
-            else:
-                # a sample's max (any) bounds the true one from below, its
-                # min (all) from above: `max > c` is certain once the sample
-                # exceeds c, `max < c` once the sample does not
-                up = r.op in ("amax", "any")
-                gt = (cmp in ("gt", "ge")) == red_left
-                if up == gt:
-                    w(f"      if (!s_pred[{j}]) cert_ = 0;")
-                else:
-                    w(f"      if (s_pred[{j}]) cert_ = 0;")
+            # max / min / any / all: a sample's extreme bounds the true one
+            # from one side only, so `max > c` is certain once the sample
+            # exceeds c but `max <= c` never is.  Such decisions are taken
+            # from the sample without certification (a miss then clears the
+            # confidence counter); requiring it would leave every chain with
+            # a `c.min() < 0` that holds false unspeculated (phi4_like).
         w("      s_cert_ = cert_;")
         w("    }")
         w("    __syncthreads();")
@@ -1142,22 +1147,25 @@ class Plan:
             self._emit_scalar_level(w, 0)
         else:
             # Adaptive speculation.  A confidence counter in the scratch
-            # (+56) picks the entry: >= 2 speculates on the last launch's
-            # decisions; below, the exact staged passes run (one HBM read of
-            # each input, kept on chip across the grid barriers) and the
-            # counter grows while consecutive launches repeat their decisions.
-            # A hit keeps the counter, a miss resets it: inputs whose decisions
-            # alternate settle on the exact entry instead of paying a
-            # speculative sweep plus a restart on most launches.
+            # (+56) picks the entry: >= 2 speculates; below, the exact passes
+            # run and the counter grows while launches confirm the predictor.
+            # A hit keeps the counter, a miss resets it.  Sampled regions
+            # predict from this launch's own data and speculate only when the
+            # sample certifies the decisions; the others predict the last
+            # launch's decisions, so inputs whose decisions alternate settle
+            # on the exact entry instead of paying a sweep plus a restart.
             nd = len(self.decisions)
             w(f"  __shared__ int s_pred[{nd}];")
             w("  __shared__ int s_miss;")
             w("  __shared__ int s_mode;  // 1: speculate on the predicted decisions")
             w("  int* pred_ = (int*)(P.barrier + GM_SCRATCH_PRED);  // last launch's decisions")
             w("  int* conf_ = (int*)(P.barrier + GM_SCRATCH_CONF);  // prediction confidence")
+            w("  __shared__ int s_force_;  // diagnostics word (GM_SCRATCH_FORCE)")
             w("  if (threadIdx.x == 0) {")
             w("    int c_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(c_) : \"l\"(conf_));")
+            w("    int f_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(f_) : \"l\"((int*)(P.barrier + GM_SCRATCH_FORCE)));")
             w(f"    s_mode = c_ >= {SPEC_CONFIDENT} ? 1 : 0;")
+            w("    s_force_ = f_;")
             w("  }")
             self._emit_scalar_level(w, 0)
             if self.sampled:
@@ -1167,7 +1175,14 @@ class Plan:
                 w("  __shared__ int s_cert_;")
                 self._emit_sample(w)
                 w("  if (threadIdx.x == 0) s_mode = (s_cert_ && s_mode) ? 1 : 0;")
-                w("  __syncthreads();")
+            w("  if (threadIdx.x == 0) {  // diagnostics: forced entry / flipped predictions")
+            w("    if (s_force_ & (1 << 30)) s_mode = 0;")
+            w("    if (s_force_ & (int)0x80000000u) s_mode = 1;")
+            if self.sampled:
+                for j in range(nd):
+                    w(f"    s_pred[{j}] ^= (s_force_ >> {j}) & 1;")
+            w("  }")
+            w("  __syncthreads();")
             w("  if (s_mode) {")
             saved = (self.stage, self.prefetch)
             self.stage = {k: "none" for k in self.stage}
@@ -1280,6 +1295,7 @@ class Plan:
                 j = self.decisions.index(s)
                 w(f"    float sf{s.uid} = 0.f; bool sb{s.uid} = false; (void)sf{s.uid}; (void)sb{s.uid};")
                 late.append(f"{{ int pd_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(pd_) : \"l\"(pred_ + {j})); "
+                            f"pd_ = (pd_ != 0) ^ ((s_force_ >> {j}) & 1); "
                             f"sf{s.uid} = pd_ ? 1.f : 0.f; sb{s.uid} = pd_ != 0; if (threadIdx.x == 0) s_pred[{j}] = pd_; }}")
             else:
                 w(f"    const float sf{s.uid} = (float)s_scal[{self.slot[s.uid]}]; (void)sf{s.uid};")

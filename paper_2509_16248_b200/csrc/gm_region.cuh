@@ -835,6 +835,8 @@ __device__ __forceinline__ void st_release64(u64* p, u64 v) {
 // and P.partials = double[slot][gridDim.x] at +GM_SCRATCH_PARTIALS.
 #define GM_SCRATCH_STATS 32     // u64 [launches, mispredictions, exact entries] (speculative regions)
 #define GM_SCRATCH_CONF 56      // int prediction confidence (adaptive speculation)
+#define GM_SCRATCH_FORCE 60     // int diagnostics: bit j flips predicted decision j, bit 30 forces
+                                // the exact entry, bit 31 the speculative one (tests, bench timing)
 #define GM_SCRATCH_FLAG 128     // (free: tools/barrier_bench.py protocol variants)
 #define GM_SCRATCH_RESULTS 136
 #define GM_SCRATCH_PRED 288     // int[24] predicted decisions (speculative regions)
@@ -1169,6 +1171,31 @@ __device__ __forceinline__ double cta_combine(int op, double v, double* s_w) {
   const double r = s_w[GM_WARPS];
   __syncthreads();
   return r;
+}
+// CTA-wide sum of two doubles at once (one set of barriers); s_w holds
+// 2 * GM_WARPS + 2 doubles.
+__device__ __forceinline__ void cta_sum2(double& a, double& b, double* s_w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  if (lane == 0) { s_w[2 * warp] = a; s_w[2 * warp + 1] = b; }
+  __syncthreads();
+  if (warp == 0) {
+    double x = lane < GM_WARPS ? s_w[2 * lane] : 0.0, y = lane < GM_WARPS ? s_w[2 * lane + 1] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      x += __shfl_xor_sync(0xffffffffu, x, off);
+      y += __shfl_xor_sync(0xffffffffu, y, off);
+    }
+    if (lane == 0) { s_w[2 * GM_WARPS] = x; s_w[2 * GM_WARPS + 1] = y; }
+  }
+  __syncthreads();
+  a = s_w[2 * GM_WARPS];
+  b = s_w[2 * GM_WARPS + 1];
+  __syncthreads();
 }
 __device__ __forceinline__ float acc_identity(int op) {
   switch (op) {

@@ -35,6 +35,8 @@ from .rowgen import RowPlan, has_row_ops
 SCRATCH_PARTIALS = 2432  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
 SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [launches, mispredictions, exact entries]
 SCRATCH_CONF = 56       # GM_SCRATCH_CONF: int prediction confidence (adaptive speculation)
+SCRATCH_FORCE = 60      # GM_SCRATCH_FORCE: diagnostics (flip decisions / force an entry)
+FORCE_EXACT, FORCE_SPEC = 1 << 30, -(1 << 31)   # bits 30 / 31 of the (int32) force word
 SCRATCH_PRED = 288      # GM_SCRATCH_PRED: int predicted decisions
 SCRATCH_SUBCNT = 384    # GM_SCRATCH_SUBCNT: arrival sub-counters
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
@@ -400,6 +402,12 @@ class _Spec:
         and bench).  Launches count both entries; see exact_entries()."""
         v = self.scratch[SCRATCH_STATS:SCRATCH_STATS + 16].view(torch.int64).tolist()
         return int(v[0]), int(v[1])
+
+    def force(self, word: int) -> None:
+        """Diagnostics: set the force word of the current scratch (bit j flips
+        predicted decision j; FORCE_EXACT / FORCE_SPEC pick the entry); 0
+        restores normal operation.  Stream-ordered, no sync."""
+        self.scratch[SCRATCH_FORCE:SCRATCH_FORCE + 4].view(torch.int32).fill_(int(word))
 
     def exact_entries(self) -> int:
         """Launches of a speculative region that took the exact entry (the

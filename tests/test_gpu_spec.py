@@ -69,14 +69,13 @@ def test_forced_mispredictions_match_hits(programs):
     for r in low.regions:
         sp = r.last_spec
         nd = len(sp.plan.decisions)
-        vals = sp.scalars()
-        wrong = [0 if vals[sp.plan.slot[d.uid]] != 0.0 else 1 for d in sp.plan.decisions]
-        sp.scratch[reg.SCRATCH_PRED: reg.SCRATCH_PRED + 4 * nd].view(torch.int32).copy_(torch.tensor(wrong, dtype=torch.int32))
-        # confident: the launch speculates (on the wrong decisions)
-        sp.scratch[reg.SCRATCH_CONF: reg.SCRATCH_CONF + 4].view(torch.int32).fill_(3)
+        # speculate, every prediction flipped (diagnostics word)
+        sp.force(reg.FORCE_SPEC | ((1 << nd) - 1))
     before = [r.last_spec.spec_stats()[1] for r in low.regions]
     miss = ex(*args).clone()
     ex.flush()
+    for r in low.regions:
+        r.last_spec.force(0)
     after = [r.last_spec.spec_stats()[1] for r in low.regions]
     assert all(a == b + 1 for a, b in zip(after, before)), (before, after)
     assert torch.equal(hit, miss)
@@ -141,16 +140,19 @@ def test_every_entry_is_bit_identical(programs, mode):
                 stats0.append(None)
                 continue
             nd = len(sp.plan.decisions)
-            vals = sp.scalars()
-            dec = [1 if vals[sp.plan.slot[d.uid]] != 0.0 else 0 for d in sp.plan.decisions]
-            if mode == "miss":
-                dec = [1 - v for v in dec]
-            sp.scratch[reg.SCRATCH_PRED: reg.SCRATCH_PRED + 4 * nd].view(torch.int32).copy_(
-                torch.tensor(dec, dtype=torch.int32))
-            sp.scratch[reg.SCRATCH_CONF: reg.SCRATCH_CONF + 4].view(torch.int32).fill_(0 if mode == "exact" else 3)
+            if not sp.plan.sampled:
+                # history predictor: the last launch's decisions are right
+                vals = sp.scalars()
+                dec = [1 if vals[sp.plan.slot[d.uid]] != 0.0 else 0 for d in sp.plan.decisions]
+                sp.scratch[reg.SCRATCH_PRED: reg.SCRATCH_PRED + 4 * nd].view(torch.int32).copy_(
+                    torch.tensor(dec, dtype=torch.int32))
+            sp.force({"hit": reg.FORCE_SPEC, "miss": reg.FORCE_SPEC | ((1 << nd) - 1),
+                      "exact": reg.FORCE_EXACT}[mode])
             stats0.append((sp.spec_stats(), sp.exact_entries()))
         out = ex(*args).clone()
         ex.flush()
+        for r in low.regions:
+            r.last_spec.force(0)
         assert torch.equal(out, ref), (name, mode)
         for r, st in zip(low.regions, stats0):
             if st is None:
