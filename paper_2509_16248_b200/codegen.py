@@ -779,7 +779,17 @@ class Plan:
         regions keep the last launch's decisions as their prediction."""
         if os.environ.get("GM_SAMPLE", "1") == "0" or self.vfull < 1:
             return False
-        return all(r.op in self.SAMPLE_SCALED + self.SAMPLE_PLAIN for r in self.reductions)
+        if not all(r.op in self.SAMPLE_SCALED + self.SAMPLE_PLAIN for r in self.reductions):
+            return False
+        # The sample pass costs ~2 us at the kernel front.  It pays where the
+        # exact entry is expensive: chains of decisions (>= 3 passes: qwen
+        # 36 -> 25 us, phi4 53 -> 40 us per forward under rotating inputs)
+        # and fp32 predicated blocks (bigbird 224 -> 219 us); a 2-pass 16-bit
+        # block's exact entry is within ~1.5 us of its speculative hit, so it
+        # keeps the history predictor (profiles/r02_ab_sampling*.jsonl)
+        if os.environ.get("GM_SAMPLE") == "always":
+            return True
+        return self.npass >= 3 or any(DT_SIZE.get(ip.dtype, 2) >= 4 for ip in self.inputs if ip.mode == MODE_FULL)
 
     def _simple_decision(self, d: Node):
         """(reduction, comparison, other operand, reduction on the left) when
@@ -809,14 +819,6 @@ class Plan:
         their own data instead of from the previous launch."""
         nsamp = min(self.vfull, self.threads)
         scale = float(self.n) / float(nsamp * nat.VEC)
-        # the speculative sweep's unguarded inputs start their way into L2
-        # now, overlapping the sample pass (fire-and-forget prefetches)
-        for ip in self._preload_inputs("spec"):
-            w(f"  for (int k = 0; k < {self.K}; ++k) {{")
-            w("    const i64 v = t0_ + (i64)k * T_;")
-            w(f"    if (v < VF_) gm::prefetch_l2((const char*)P.in[{ip.slot}].ptr + v * GM_VEC * "
-              f"{DT_SIZE[ip.dtype]}, {nat.VEC * DT_SIZE[ip.dtype]});")
-            w("  }")
         w("  { // ---- sampled prediction of the branch decisions")
         w("    __shared__ double s_w_[2 * GM_WARPS + 2];")
         w("    __shared__ double s_m1_[GM_MAX_RED], s_m2_[GM_MAX_RED];  // sample moments (unscaled)")

@@ -20,13 +20,11 @@ torch.library custom op with a fake implementation, so it traces.
 from __future__ import annotations
 
 import ast
-import ctypes
 import functools
 import textwrap
 
 import torch
 
-from . import _native as nat
 from .executor import B200Executor
 from .lowering import load
 from .region import RegionUnsupported

@@ -48,8 +48,7 @@ import os
 
 import torch
 
-from .codegen import (B200_DEVICE, DT_CODE, DT_SIZE, MODE_FULL, MODE_PERIODIC, MODE_SCALAR, MODE_STRIDED, InputPlan,
-                      Plan, _round_f)
+from .codegen import B200_DEVICE, DT_CODE, MODE_FULL, MODE_PERIODIC, MODE_SCALAR, MODE_STRIDED, Plan, _round_f
 from . import _native as nat
 from .ir import ROW_NORM, ROW_OPS, ROW_RED, Graph, Node, Unsupported, infer, is_fusable_dtype, topo
 
