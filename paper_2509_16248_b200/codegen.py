@@ -832,13 +832,27 @@ class Plan:
         w("    const i64 les = 0; (void)les;")
         self._tail = True   # free inputs read with per-call gmem loads (e/nv)
         try:
+            levels = []
             for p in range(self.npass):
                 reds = [r for r in self.pass_reds[p]]
                 feeds = [d for d in self.decisions if self.avail[d.uid] > p]
-                if not reds or not feeds:
-                    continue
+                if reds and feeds:
+                    levels.append((p, reds))
+            # every sampled input vector is loaded once, up front (one
+            # round trip for the whole chain, not one per level)
+            frees = []
+            for p, reds in levels:
+                for n in self._nodes([r.args[0] for r in reds]):
+                    if n.op == "free" and n not in frees and self.in_by_uid[n.uid].mode != MODE_SCALAR:
+                        frees.append(n)
+            for n in frees:
+                w(f"    float n{n.uid}_s[GM_VEC];")
+            for n in frees:
+                for line in self._elem_code(n, "s"):
+                    w("    " + line.replace("\n", "\n    "))
+            for p, reds in levels:
                 roots = [r.args[0] for r in reds]
-                nodes = self._nodes(roots)
+                nodes = [n for n in self._nodes(roots) if n not in frees]
                 guards = self._guards_roots(roots)
                 w(f"    {{ // sample of pass {p}")
                 for sc in self._used_scalars(nodes, guards):
