@@ -1112,6 +1112,7 @@ class Plan:
         w('#include "gm_region.cuh"')
         w("#define gm_bool(x) (((x) != 0.0) ? 1.0 : 0.0)")
         w("#define gm_trunc(x) ((double)(long long)(x))")
+        w("#define GM_LIVE_EXIT() do { if (threadIdx.x == 0 && s_live_) gm::live_exit(P); } while (0)")
         w(f"// region {self.name}: shape {list(self.shape)}, {self.npass} pass(es), "
           f"{len(self.reductions)} reduction(s), {len(self.inputs)} input(s); grid {self.grid} x {self.threads}, "
           f"{self.K} vector(s)/thread{', speculative' if self.spec else ''}")
@@ -1133,6 +1134,12 @@ class Plan:
         # programmatic dependent launch: wait for the previous kernel's
         # results before the first global read (a no-op without PDL)
         w('  asm volatile("griddepcontrol.wait;" ::: "memory");')
+        w("  __shared__ int s_live_;  // live timer on (diagnostics word, bench.py)")
+        w("  if (threadIdx.x == 0) {")
+        w("    int f_; asm volatile(\"ld.global.u32 %0, [%1];\" : \"=r\"(f_) : \"l\"((int*)(P.barrier + GM_SCRATCH_FORCE)));")
+        w("    s_live_ = (f_ & GM_LIVE_BIT) != 0;")
+        w("    if (s_live_) gm::live_start(P);")
+        w("  }")
         w("  u64 ep_ = gm::grid_epoch_begin(P); (void)ep_;  // arrival epoch (thread 0)")
         w("  __shared__ int s_epi_;  // does this CTA write the scalar outputs / mirror")
         w("  if (threadIdx.x == 0) s_epi_ = blockIdx.x == 0;")
@@ -1206,6 +1213,7 @@ class Plan:
             self._emit_ctx(w, "spec")
             w("  if (!s_miss) {")
             self._emit_epilogue(w, "    ", mode="hit")
+            w("    GM_LIVE_EXIT();")
             w("    return;")
             w("  }")
             w("  // misprediction: the exact passes from the first mispredicted level (inputs re-read)")
@@ -1215,6 +1223,7 @@ class Plan:
                 self._emit_ctx(w, p)
                 w("  }")
             self._emit_epilogue(w, "  ", mode="miss")
+            w("  GM_LIVE_EXIT();")
             w("  return;")
             w("  }")
             self.stage, self.prefetch = saved
@@ -1239,6 +1248,7 @@ class Plan:
             w("  __syncthreads();")
             w("  if (threadIdx.x == 0) atomicMax(&prof_[63], gm::globaltimer());")
         self._emit_epilogue(w, "  ", mode="exact" if self.spec else "plain")
+        w("  GM_LIVE_EXIT();")
         w("}")
         return "\n".join(out) + "\n"
 
@@ -1405,7 +1415,8 @@ class Plan:
             vals = ", ".join(f"__longlong_as_double((long long)acc{k})" if r.op in ("argmax", "argmin")
                              else f"(double)acc{k}" for k, r in enumerate(reds))
             w(f"    {{ double vals_[{nr}] = {{{vals}}};")
-            w(f"      if (!gm::grid_reduce_last(P, {nr}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs})) return; }}")
+            w(f"      if (!gm::grid_reduce_last(P, {nr}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs})) "
+              f"{{ GM_LIVE_EXIT(); return; }} }}")
             w("    if (threadIdx.x == 0) s_epi_ = 1;  // this CTA writes the scalar outputs")
         elif reds:
             w(f"    grid_wait(P, {nr}, ops_, slots_, tgt_, s_red{pargs});")

@@ -835,8 +835,11 @@ __device__ __forceinline__ void st_release64(u64* p, u64 v) {
 // and P.partials = double[slot][gridDim.x] at +GM_SCRATCH_PARTIALS.
 #define GM_SCRATCH_STATS 32     // u64 [launches, mispredictions, exact entries] (speculative regions)
 #define GM_SCRATCH_CONF 56      // int prediction confidence (adaptive speculation)
-#define GM_SCRATCH_FORCE 60     // int diagnostics: bit j flips predicted decision j, bit 30 forces
-                                // the exact entry, bit 31 the speculative one (tests, bench timing)
+#define GM_SCRATCH_FORCE 60     // int diagnostics: bit j flips predicted decision j, bit 29 turns
+                                // the live timer on, bit 30 forces the exact entry, bit 31 the
+                                // speculative one (tests, bench timing)
+#define GM_SCRATCH_LIVE 256     // u64 [start ns, exits, sum of durations ns, launches] (live timer)
+#define GM_LIVE_BIT (1 << 29)
 #define GM_SCRATCH_FLAG 128     // (free: tools/barrier_bench.py protocol variants)
 #define GM_SCRATCH_RESULTS 136
 #define GM_SCRATCH_PRED 288     // int[24] predicted decisions (speculative regions)
@@ -1155,6 +1158,24 @@ __device__ __forceinline__ float acc8(int op, float acc, const float (&x)[8], in
   }
   return acc;
 }
+// Live timer (diagnostics word bit 29, set by bench.py for its timed loop):
+// CTA 0 stamps %globaltimer after griddepcontrol.wait; every CTA's thread 0
+// counts its exit, and the CTA completing a launch's count adds
+// (its stamp - the start) to a running sum — the kernel's own duration
+// inside the forward's graph, with no event nodes between kernels.
+__device__ __forceinline__ void live_start(const Params& P) {
+  if (blockIdx.x == 0) *(volatile u64*)(P.barrier + GM_SCRATCH_LIVE) = globaltimer();
+}
+__device__ __forceinline__ void live_exit(const Params& P) {
+  u64* lt = (u64*)(P.barrier + GM_SCRATCH_LIVE);
+  const u64 old = atomicAdd((unsigned long long*)&lt[1], 1ull);
+  if ((old + 1) % gridDim.x == 0) {
+    const u64 t1 = globaltimer(), t0 = ld_relaxed64(lt);
+    atomicAdd((unsigned long long*)&lt[2], (unsigned long long)(t1 - t0));
+    atomicAdd((unsigned long long*)&lt[3], 1ull);
+  }
+}
+
 // CTA-wide combine (every thread returns the result); s_w holds GM_WARPS
 // doubles.  Used by the sampled branch predictor (codegen.Plan._emit_sample).
 __device__ __forceinline__ double cta_combine(int op, double v, double* s_w) {

@@ -37,6 +37,8 @@ SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [launches, mispredictions, exact
 SCRATCH_CONF = 56       # GM_SCRATCH_CONF: int prediction confidence (adaptive speculation)
 SCRATCH_FORCE = 60      # GM_SCRATCH_FORCE: diagnostics (flip decisions / force an entry)
 FORCE_EXACT, FORCE_SPEC = 1 << 30, -(1 << 31)   # bits 30 / 31 of the (int32) force word
+LIVE_BIT = 1 << 29      # bit 29: the grid kernels' live timer (GM_SCRATCH_LIVE)
+SCRATCH_LIVE = 256      # GM_SCRATCH_LIVE: u64 [start ns, exits, sum of durations ns, launches]
 SCRATCH_PRED = 288      # GM_SCRATCH_PRED: int predicted decisions
 SCRATCH_SUBCNT = 384    # GM_SCRATCH_SUBCNT: arrival sub-counters
 _kernel_cache: dict[str, nat.CompiledRegion] = {}
@@ -408,6 +410,28 @@ class _Spec:
         predicted decision j; FORCE_EXACT / FORCE_SPEC pick the entry); 0
         restores normal operation.  Stream-ordered, no sync."""
         self.scratch[SCRATCH_FORCE:SCRATCH_FORCE + 4].view(torch.int32).fill_(int(word))
+
+    def set_live(self, on: bool) -> None:
+        """Turn the in-kernel live timer on (zeroing its sums) or off in every
+        scratch of this specialisation (each graph capture has its own).
+        Grid-region kernels only; stream-ordered, no sync."""
+        for t, _idx in self._scratches.values():
+            word = t[SCRATCH_FORCE:SCRATCH_FORCE + 4].view(torch.int32)
+            if on:
+                t[SCRATCH_LIVE:SCRATCH_LIVE + 32].zero_()
+                word.bitwise_or_(LIVE_BIT)
+            else:
+                word.bitwise_and_(~LIVE_BIT)
+
+    def live_stats(self) -> tuple[int, int]:
+        """(sum of kernel durations in ns, launches) the live timer recorded
+        since set_live(True), over every scratch (syncs)."""
+        tot, n = 0, 0
+        for t, _idx in self._scratches.values():
+            v = t[SCRATCH_LIVE:SCRATCH_LIVE + 32].view(torch.int64).tolist()
+            tot += int(v[2])
+            n += int(v[3])
+        return tot, n
 
     def exact_entries(self) -> int:
         """Launches of a speculative region that took the exact entry (the

@@ -50,6 +50,12 @@ def test_b200_arm_line():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5 and r["peak"] > 0
     assert all(k["speculative"] for k in d["kernels"])
+    # the grid kernels time themselves inside the timed loop (in-kernel
+    # %globaltimer, one launch per step and region); the event-bracketed
+    # duration of the same kernel includes the graph's launch gaps
+    for k in d["kernels"]:
+        assert k["how"].startswith("live, in-kernel") and "over the 5 launches" in k["how"], k["how"]
+        assert 0 < k["ms"] <= k["ms_events"] * 1.05, (k["ms"], k["ms_events"])
 
 
 @pytest.mark.gpu
