@@ -31,6 +31,8 @@ from . import _native as nat
 from .codegen import MODE_PERIODIC, MODE_STRIDED, Plan
 from .ir import Graph, Node, Unsupported, fold_host_predicates
 from .rowgen import RowPlan, has_row_ops
+from .split import is_mixed
+from .split import split as split_graph
 
 SCRATCH_PARTIALS = 2432  # GM_SCRATCH_PARTIALS in csrc/gm_region.cuh
 SCRATCH_STATS = 32      # GM_SCRATCH_STATS: u64 [launches, mispredictions, exact entries]
@@ -449,6 +451,80 @@ class _Spec:
         return self.scratch[off: off + 8 * self.nscal].view(torch.float64).tolist()
 
 
+class _SubRegion:
+    """The graph of one kernel of a split region (split.py)."""
+
+    def __init__(self, name: str, graph: Graph, outs: list[Node]):
+        self.name, self.graph, self.out_nodes = name, graph, outs
+
+
+class _SplitSpec:
+    """A region over several iteration spaces (split.py): the side kernels
+    run first and append their results to the argument list, then the main
+    kernel.  Looks like the main kernel's _Spec to the bench and the tests
+    (`plan`, `spec_stats`, `scalars`, ...); launch-wide queries (bytes,
+    live timer) cover every kernel."""
+
+    def __init__(self, region: "Region", graph: Graph, outs: list[Node], args: list):
+        steps, (mg, mouts) = split_graph(graph, outs, args)
+        ext = list(args)
+        self.sides = []
+        for i, (sg, souts, idx) in enumerate(steps):
+            sub = _SubRegion(f"{region.name}/side{i}", sg, souts)
+            sp = _SplitSpec(sub, sg, souts, ext) if is_mixed(sg, souts, ext) else _Spec(sub, ext)
+            self.sides.append((sp, idx))
+            probe = _probe_value(souts[0], ext)
+            ext.append(probe)
+        self.main = _Spec(_SubRegion(region.name, mg, mouts), ext)
+        self.nargs = len(args)
+
+    def __getattr__(self, name):
+        return getattr(self.main, name)
+
+    def run(self, args: list, pdl: bool | None = None):
+        ext = list(args)
+        for sp, _idx in self.sides:
+            ext.append(sp.run(list(ext), pdl)[0])
+        self._last_ext = ext
+        return self.main.run(ext, pdl)
+
+    _last_ext: list | None = None
+
+    def all_specs(self):
+        for sp, _ in self.sides:
+            yield from (sp.all_specs() if isinstance(sp, _SplitSpec) else [sp])
+        yield self.main
+
+    def bytes_alg(self, args: list) -> int:
+        """Every kernel's compulsory bytes (side results count as written by
+        their kernel and read by the main one)."""
+        ext = self._last_ext or list(args)
+        total = 0
+        for k, (sp, _idx) in enumerate(self.sides):
+            total += sp.bytes_alg(ext[:self.nargs + k])
+        return total + self.main.bytes_alg(ext)
+
+    def set_live(self, on: bool) -> None:
+        for sp in self.all_specs():
+            sp.set_live(on)
+
+    def live_stats(self) -> tuple[int, int]:
+        tot, n = 0, 0
+        for sp in self.all_specs():
+            t, k = sp.live_stats()
+            tot += t
+            n = max(n, k)
+        return tot, n
+
+
+def _probe_value(node: Node, args: list):
+    """A stand-in with the dtype / shape / device of a side result, so the
+    main kernel is specialised for it (the real tensor arrives at run time;
+    the specialisation key of the region covers its inputs only)."""
+    dev = next(a.device for a in args if torch.is_tensor(a) and a.device.type == "cuda")
+    return torch.empty(tuple(node.shape), dtype=node.dtype, device=dev)
+
+
 class Region:
     """One fused run of statements of a transformed forward."""
 
@@ -506,6 +582,9 @@ class Region:
             self.stats.fallback_reasons.append(reason)
             return reason
         try:
+            graph, outs = fold_host_predicates(self.graph, self.out_nodes, args)
+            if is_mixed(graph, outs, args):
+                return _SplitSpec(self, graph, outs, args)
             return _Spec(self, args)
         except Unsupported as exc:
             reason = str(exc)

@@ -179,3 +179,39 @@ def test_bigbird_attn_scores_are_rematerialised(programs):
     assert grid.out_names[-1] == "__gm_pred_0" and "scores" not in grid.out_names
     assert has_row_ops(rows.out_nodes) and rows.out_names == ["probs"]
     assert "/ 8.0" in rows.source and "/ 8.0" in grid.source
+
+
+def test_mixed_shapes_split_into_side_kernels():
+    """A run over two iteration spaces (a predicate over a [C] bias guarding
+    full arms, a [C]-shaped live-out, a softmax over the bias): the main
+    kernel covers the full shape, each other-shaped reduction / output / row
+    operator is a side kernel that runs first (split.py)."""
+    from paper_2509_16248_b200.split import is_mixed, split
+
+    text = '''
+import torch
+def f(x, b):
+    __gm_pred_0 = b.sum() > 0
+    __gm_then_y_0 = x * 2 + b
+    y = torch.where(__gm_pred_0, __gm_then_y_0, x)
+    c = torch.softmax(b, -1) * 3
+    z = y * x.mean()
+    return y, c, z
+'''
+    low, _ = lowering.lower(text)
+    # grid run (the predicated block), row run (the softmax), grid run (z)
+    assert len(low.regions) == 3
+    r = low.regions[0]
+    args = {"x": torch.randn(4, 8, 16), "b": torch.randn(16)}
+    a = [args[fv.text] for fv in r.graph.frees]
+    assert is_mixed(r.graph, r.out_nodes, a)
+    steps, (mg, mouts) = split(r.graph, r.out_nodes, a)
+    # the [C] bias sum is a side kernel; the main kernel writes y over [4, 8, 16]
+    assert [s[1][0].op for s in steps] == ["sum"]
+    ext = list(a)
+    for sg, souts, idx in steps:
+        assert not is_mixed(sg, souts, ext)
+        ext.append(torch.empty(tuple(souts[0].shape), dtype=souts[0].dtype))
+    assert not is_mixed(mg, mouts, ext)
+    p = codegen.Plan(mg, mouts, ext, allow_cpu=True)
+    assert len(nat.compile_cubin(p.source, (10, 0))) > 0
