@@ -771,6 +771,127 @@ class Plan:
     SAMPLE_SCALED = ("sum", "mean", "norm", "count_nonzero")
     SAMPLE_PLAIN = ("amax", "amin", "any", "all")
 
+    def _cta_ok(self) -> bool:
+        """Per-CTA prediction (the default where possible): every CTA
+        predicts the decisions from the first vector of each of its threads —
+        data the speculative sweep has just loaded — so the prediction costs a
+        CTA-wide combine, not a pass of its own.  CTAs may disagree; the grid
+        reduce carries every decision's min and max over CTAs (and whether
+        all certified), so all CTAs reach the same verdict."""
+        if os.environ.get("GM_SAMPLE", "cta") != "cta" or self.vfull < 1:
+            return False
+        if not all(r.op in self.SAMPLE_SCALED + self.SAMPLE_PLAIN for r in self.reductions):
+            return False
+        return len(self.reductions) + 2 * len(self.decisions) + 1 <= nat.MAX_RED
+
+    def extra_slots(self) -> int:
+        """Grid-reduce slots beyond the reductions (per-CTA prediction)."""
+        return 2 * len(self.decisions) + 1 if getattr(self, "cta_pred", False) else 0
+
+    def _cta_predict_lines(self) -> list[str]:
+        """Inside the speculative sweep's first register block, after its
+        loads are issued: the region's decision chain evaluated on each
+        thread's first vector (the loaded raw registers), combined CTA-wide,
+        scaled to the whole space, certified (4 standard errors), and the
+        decisions handed to the sweep through sb/sf."""
+        L: list[str] = []
+        w = L.append
+        scale_base = float(self.n)
+        w("{ // ---- per-CTA prediction from this CTA's first vectors")
+        w("  const bool sok_ = ok0;")
+        w("  const double cnt_ = 8.0 * (double)max(0ll, min((i64)GM_THREADS, VF_ - (i64)blockIdx.x * GM_THREADS));")
+        w("  int cert_ = 1;")
+        levels = []
+        for p in range(self.npass):
+            reds = list(self.pass_reds[p])
+            feeds = [d for d in self.decisions if self.avail[d.uid] > p]
+            if reds and feeds:
+                levels.append((p, reds))
+        done_free: set[int] = set()
+        for p, reds in levels:
+            roots = [r.args[0] for r in reds]
+            nodes = self._nodes(roots)
+            guards = self._guards_roots(roots)
+            w(f"  {{ // level {p}")
+            for n in nodes:
+                if n.op == "free" and n.uid in done_free:
+                    continue
+                w(f"  float n{n.uid}_q[GM_VEC];")
+            cur = None
+            for n in nodes:
+                g = self._guard_expr(guards.get(n.uid, frozenset({frozenset()})))
+                if g != cur:
+                    if cur:
+                        w("  }")
+                    if g:
+                        w(f"  if ({g}) {{")
+                    cur = g
+                if n.op == "free":
+                    ip = self.in_by_uid[n.uid]
+                    dt = DT_CODE[ip.dtype]
+                    if ip.mode == MODE_SCALAR:
+                        w(f"  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_q[l] = sin{ip.slot};")
+                    elif ip.mode == MODE_FULL and ip.slot in self._preloaded:
+                        w(f"  gm::rcvt<{dt}>({self._preloaded[ip.slot].format(u=0)}, n{n.uid}_q);")
+                    else:
+                        fn = {MODE_FULL: "load8_gmem", MODE_PERIODIC: "load8_periodic"}.get(ip.mode, "load8_strided")
+                        w(f"  gm::{fn}<{dt}>(P.in[{ip.slot}], e0, sok_ ? GM_VEC : 0, n{n.uid}_q);")
+                    continue
+                for line in self._elem_code(n, "q"):
+                    w("  " + line.replace("\n", "\n  "))
+            if cur:
+                w("  }")
+            for r in reds:
+                k = self.red_index[r.uid]
+                x = f"n{r.args[0].uid}_q"
+                op = RED_OP[r.op]
+                if r.op in self.SAMPLE_SCALED:
+                    term = {"count_nonzero": f"(({x}[l] != 0.f) ? 1.0 : 0.0)",
+                            "norm": f"((double){x}[l] * (double){x}[l])"}.get(r.op, f"(double){x}[l]")
+                    w(f"  double t{k}_ = 0.0, q{k}_ = 0.0;")
+                    w(f"  if (sok_) for (int l = 0; l < GM_VEC; ++l) {{ const double z_ = {term}; t{k}_ += z_; q{k}_ += z_ * z_; }}")
+                    w(f"  gm::cta_sum2(t{k}_, q{k}_, s_w_);")
+                    w(f"  if (threadIdx.x == 0) {{ s_red[{k}] = t{k}_ * ({scale_base!r} / fmax(cnt_, 1.0)); "
+                      f"s_m1_[{k}] = t{k}_; s_m2_[{k}] = q{k}_; }}")
+                else:
+                    w(f"  const float a{k}_ = gm::acc8({op}, gm::acc_identity({op}), {x}, sok_ ? GM_VEC : 0);")
+                    w(f"  const double v{k}_ = gm::cta_combine({op}, (double)a{k}_, s_w_);")
+                    w(f"  if (threadIdx.x == 0) s_red[{k}] = v{k}_;")
+            w("  if (threadIdx.x == 0) {")
+            for r in reds:
+                w("    " + self._finish_reduction(r, self.red_index[r.uid]))
+            for n in self.scalars:
+                if self.avail[n.uid] == p + 1 and n.op not in REDUCE:
+                    w("    " + self._scalar_code(n))
+            for j, d in enumerate(self.decisions):
+                if self.avail[d.uid] != p + 1:
+                    continue
+                w(f"    s_pred[{j}] = (s_scal[{self.slot[d.uid]}] != 0.0) ^ ((s_force_ >> {j}) & 1);")
+                form = self._simple_decision(d)
+                if form is not None and form[0].op in self.SAMPLE_SCALED:
+                    r, cmp, c, _left = form
+                    k = self.red_index[r.uid]
+                    est = f"s_scal[{self.slot[r.uid]}]"
+                    w("    {")
+                    w(f"      const double n_ = fmax(cnt_, 1.0), mu_ = s_m1_[{k}] / n_, "
+                      f"var_ = fmax(s_m2_[{k}] / n_ - mu_ * mu_, 0.0);")
+                    w("      double se_ = sqrt(var_ / n_);")
+                    if r.op in ("sum", "count_nonzero"):
+                        w(f"      se_ *= {float(self.n)!r};")
+                    elif r.op == "norm":
+                        w(f"      se_ = se_ * {float(self.n)!r} / (2.0 * fmax({est}, 1e-30));")
+                    w(f"      if (!(fabs({est} - ({self._sv(c)})) > 4.0 * se_)) cert_ = 0;")
+                    w("    }")
+            w("    s_cert_ = cert_;")
+            w("  }")
+            w("  __syncthreads();")
+            for j, d in enumerate(self.decisions):
+                if self.avail[d.uid] == p + 1:
+                    w(f"  sb{d.uid} = s_pred[{j}] != 0; sf{d.uid} = sb{d.uid} ? 1.f : 0.f;")
+            w("  }")
+        w("}")
+        return L
+
     def _sample_ok(self) -> bool:
         """Can every predicted decision be estimated from a sample?  Sums,
         means, norms and counts scale with the sampled fraction; max / min /
@@ -993,7 +1114,8 @@ class Plan:
         # entries (bigbird fp32: speculative hit 12.7 -> 15.2 us, exact
         # 17.9 -> 18.9 us; tools/ab_spec.sh).
         self.l2_prefetch: list[InputPlan] = []
-        self.sampled = self.spec and self._sample_ok()
+        self.cta_pred = self.spec and self._cta_ok()
+        self.sampled = self.spec and not self.cta_pred and self._sample_ok()
         if self.spec:
             self.l2_prefetch = [ip for ip in self.inputs if ip.mode == MODE_FULL and ip.passes
                                 and min(ip.passes) > 0 and self._unguarded_in(ip, min(ip.passes))]
@@ -1190,6 +1312,9 @@ class Plan:
             w(f"    s_mode = c_ >= {SPEC_CONFIDENT} ? 1 : 0;")
             w("    s_force_ = f_;")
             w("  }")
+            if self.cta_pred:
+                w("  __shared__ int s_cert_;")
+                w("  __shared__ double s_w_[2 * GM_WARPS + 2], s_m1_[GM_MAX_RED], s_m2_[GM_MAX_RED];")
             self._emit_scalar_level(w, 0)
             if self.sampled:
                 # sampled regions: the sample certifies (or not) THIS launch's
@@ -1278,7 +1403,12 @@ class Plan:
                 w(f"{ind}  *conf_ = min(*conf_ + 1, {SPEC_CONF_MAX});")
             elif mode == "miss":
                 w(f"{ind}  st_[1] += 1;")
-                w(f"{ind}  *conf_ = 0;")
+                # per-CTA prediction: an uncertified launch was expected to
+                # risk a miss; only a certified miss indicts the predictor
+                w(f"{ind}  if (s_cert_) *conf_ = 0;" if self.cta_pred else f"{ind}  *conf_ = 0;")
+            elif self.cta_pred:
+                w(f"{ind}  st_[2] += 1;")
+                w(f"{ind}  *conf_ = min(*conf_ + 1, {SPEC_CONF_MAX});  // no prediction on this entry")
             else:
                 w(f"{ind}  st_[2] += 1;")
                 w(f"{ind}  int same_ = 1;")
@@ -1313,7 +1443,9 @@ class Plan:
         # data loads are issued (`late`), so their round trip overlaps them
         late: list[str] = []
         for s in self._used_scalars(elem_nodes, guards):
-            if spec and self.avail.get(s.uid, 0) >= 1 and self.sampled:
+            if spec and self.avail.get(s.uid, 0) >= 1 and self.cta_pred:
+                w(f"    float sf{s.uid} = 0.f; bool sb{s.uid} = false; (void)sf{s.uid}; (void)sb{s.uid};")
+            elif spec and self.avail.get(s.uid, 0) >= 1 and self.sampled:
                 j = self.decisions.index(s)
                 w(f"    const bool sb{s.uid} = s_pred[{j}] != 0; const float sf{s.uid} = sb{s.uid} ? 1.f : 0.f; "
                   f"(void)sf{s.uid};")
@@ -1333,6 +1465,7 @@ class Plan:
                 w(f"    float sin{ip.slot} = 0.f;")
                 late.append(f"sin{ip.slot} = gm::load_scalar<{DT_CODE[ip.dtype]}>(P.in[{ip.slot}]);")
         self._late = late
+        self._cta_predict_here = spec and self.cta_pred
         for k, r in enumerate(reds):
             if r.op in ("argmax", "argmin"):
                 w(f"    u64 acc{k} = 0ull;")
@@ -1347,9 +1480,18 @@ class Plan:
         nr = len(reds)
         pidx = self.npass if spec else ctx
         pargs = f", prof_ + 40 + 4 * {pidx}" if prof else ""
+        nx = self.extra_slots() if spec else 0
         if reds:
-            w(f"    const int ops_[{nr}] = {{{', '.join(str(RED_OP[r.op]) for r in reds)}}};")
-            w(f"    const int slots_[{nr}] = {{{', '.join(str(self.red_index[r.uid]) for r in reds)}}};")
+            ops = [str(RED_OP[r.op]) for r in reds]
+            slots = [str(self.red_index[r.uid]) for r in reds]
+            for j in range(len(self.decisions) if nx else 0):
+                ops += [str(RED_OP["amin"]), str(RED_OP["amax"])]
+                slots += [str(len(self.reductions) + 2 * j), str(len(self.reductions) + 2 * j + 1)]
+            if nx:
+                ops.append(str(RED_OP["amin"]))
+                slots.append(str(len(self.reductions) + 2 * len(self.decisions)))
+            w(f"    const int ops_[{nr + nx}] = {{{', '.join(ops)}}};")
+            w(f"    const int slots_[{nr + nx}] = {{{', '.join(slots)}}};")
             w("    u64 tgt_ = 0; (void)tgt_;")
 
         def stamp_loop_end():
@@ -1360,10 +1502,14 @@ class Plan:
                   f"atomicMin(&prof_[{32 + idx}], t_); }}")
 
         def arrive():
-            vals = ", ".join(f"__longlong_as_double((long long)acc{k})" if r.op in ("argmax", "argmin")
-                             else f"(double)acc{k}" for k, r in enumerate(reds))
-            w(f"    {{ double vals_[{nr}] = {{{vals}}};")
-            w(f"      tgt_ = grid_arrive(P, {nr}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs}); }}")
+            vals = [f"__longlong_as_double((long long)acc{k})" if r.op in ("argmax", "argmin")
+                    else f"(double)acc{k}" for k, r in enumerate(reds)]
+            for j in range(len(self.decisions) if nx else 0):
+                vals += [f"(double)s_pred[{j}]", f"(double)s_pred[{j}]"]
+            if nx:
+                vals.append("(double)s_cert_")
+            w(f"    {{ double vals_[{nr + nx}] = {{{', '.join(vals)}}};")
+            w(f"      tgt_ = grid_arrive(P, {nr + nx}, ops_, slots_, vals_, s_warp, s_red, ep_{pargs}); }}")
 
         deferred = False
         if self.K:
@@ -1419,7 +1565,7 @@ class Plan:
               f"{{ GM_LIVE_EXIT(); return; }} }}")
             w("    if (threadIdx.x == 0) s_epi_ = 1;  // this CTA writes the scalar outputs")
         elif reds:
-            w(f"    grid_wait(P, {nr}, ops_, slots_, tgt_, s_red{pargs});")
+            w(f"    grid_wait(P, {nr + nx}, ops_, slots_, tgt_, s_red{pargs});")
         if reds:
             if prof:
                 idx = 2 + 2 * pidx
@@ -1439,9 +1585,19 @@ class Plan:
                 # under correct decisions, so their reductions and outputs
                 # are exact and the miss path restarts at that pass.
                 w("      int miss_ = 0x7fffffff;")
-                for j, d in enumerate(self.decisions):
-                    w(f"      if ((s_scal[{self.slot[d.uid]}] != 0.0) != (s_pred[{j}] != 0)) "
-                      f"miss_ = min(miss_, {self.avail[d.uid]});")
+                if self.cta_pred:
+                    # every CTA predicted for itself: a decision holds when
+                    # all CTAs predicted it (min == max) and it was right
+                    base = len(self.reductions)
+                    for j, d in enumerate(self.decisions):
+                        lo, hi = f"s_red[{base + 2 * j}]", f"s_red[{base + 2 * j + 1}]"
+                        w(f"      if (!({lo} == {hi} && (({lo} != 0.0) == (s_scal[{self.slot[d.uid]}] != 0.0)))) "
+                          f"miss_ = min(miss_, {self.avail[d.uid]});")
+                    w(f"      s_cert_ = s_red[{base + 2 * len(self.decisions)}] != 0.0 ? 1 : 0;  // all CTAs certified")
+                else:
+                    for j, d in enumerate(self.decisions):
+                        w(f"      if ((s_scal[{self.slot[d.uid]}] != 0.0) != (s_pred[{j}] != 0)) "
+                          f"miss_ = min(miss_, {self.avail[d.uid]});")
                 w("      s_miss = miss_ == 0x7fffffff ? 0 : miss_;")
                 w("    }")
                 w("    __syncthreads();")
@@ -1491,6 +1647,11 @@ class Plan:
                     w(f"{ind}if (ok{u}) gm::rlds<{dt}>(sres{k} + (u32)(le{u} * {DT_SIZE[ip.dtype]}), r{k}_{u});")
         for line in self._late:
             w(ind + line)
+        if getattr(self, "_cta_predict_here", False):
+            w(ind + (f"if ({kb} == 0) " if kb != "0" else "") + "{")
+            for line in self._cta_predict_lines():
+                w(ind + "  " + line)
+            w(ind + "}")
         if pref is None:
             pref = {n.uid: "F" for n in elem_nodes}
         needs: dict[int, set] = {n.uid: {pref[n.uid]} for n in elem_nodes}

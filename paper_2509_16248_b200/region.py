@@ -257,7 +257,7 @@ class _Spec:
                 raise nat.NativeError(f"region {region.name}: {grid} CTAs not co-resident "
                                       f"({occ}/SM at {smem} B smem, {sms} SMs)")
         self.grid, self.vpc, self.smem, self.threads = grid, vpc, smem, threads
-        self.nred = len(plan.reductions)
+        self.nred = len(plan.reductions) + plan.extra_slots()
         self.nscal = len(plan.scalars)
         # scratch: counter/epoch/status/results (192 B, see gm_region.cuh) |
         # partials | scalar mirror (+1 KB: the GM_PROFILE timeline at scal_out + 64 u64);
@@ -465,13 +465,15 @@ class _SplitSpec:
     (`plan`, `spec_stats`, `scalars`, ...); launch-wide queries (bytes,
     live timer) cover every kernel."""
 
-    def __init__(self, region: "Region", graph: Graph, outs: list[Node], args: list):
+    def __init__(self, region: "Region", graph: Graph, outs: list[Node], args: list, depth: int = 0):
+        if depth > 8:
+            raise Unsupported("shape split nested too deep")
         steps, (mg, mouts) = split_graph(graph, outs, args)
         ext = list(args)
         self.sides = []
         for i, (sg, souts, idx) in enumerate(steps):
             sub = _SubRegion(f"{region.name}/side{i}", sg, souts)
-            sp = _SplitSpec(sub, sg, souts, ext) if is_mixed(sg, souts, ext) else _Spec(sub, ext)
+            sp = _SplitSpec(sub, sg, souts, ext, depth + 1) if is_mixed(sg, souts, ext) else _Spec(sub, ext)
             self.sides.append((sp, idx))
             probe = _probe_value(souts[0], ext)
             ext.append(probe)

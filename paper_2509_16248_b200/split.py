@@ -58,7 +58,23 @@ def main_shape(outputs: list[Node]) -> tuple | None:
     reduction over a larger space than the outputs becomes a side, so a side
     graph never re-elects the shape its own output was split off from.)"""
     written = [s for n, s in sinks(outputs) if n.op not in REDUCE]
-    shapes = written or [s for _, s in sinks(outputs)]
+    if written:
+        return max(written, key=_numel)
+    # scalar outputs only: the reductions that produce them directly (through
+    # scalar arithmetic, not through another reduction's operand) — so a side
+    # split off for its own reduction is the main kernel of its graph
+    direct, seen, stack = [], set(), list(outputs)
+    while stack:
+        n = stack.pop()
+        if n.uid in seen:
+            continue
+        seen.add(n.uid)
+        if n.op in REDUCE:
+            direct.append(tuple(n.args[0].shape))
+            continue
+        if n.kind != "elem":
+            stack.extend(n.args)
+    shapes = direct or [s for _, s in sinks(outputs)]
     if not shapes:
         return None
     return max(shapes, key=_numel)

@@ -135,16 +135,26 @@ def test_speculative_region_has_adaptive_entries(programs):
     assert not plan.sampled
 
 
-def test_sampled_prediction(programs):
+def test_sampled_prediction(programs, monkeypatch):
     """Speculative regions whose reductions have a sample estimate (sum,
-    mean, norm, count, max, min, any, all) predict their decisions from a
-    CTA-local sample of the input; prod / argmax predicates keep the last
-    launch's decisions."""
+    mean, norm, count, max, min, any, all) predict their decisions from data:
+    by default every CTA from the first vector of each of its threads (the
+    sweep's own loads), the grid reduce carrying each decision's min / max
+    over CTAs and whether all certified; GM_SAMPLE=global predicts from one
+    scrambled 4K-element sample in every CTA (a pass of its own).  prod /
+    argmax predicates keep the last launch's decisions."""
     plan = _plan(programs, "bigbird_like", torch.float32, (8, 1024, 768))
-    assert plan.spec and plan.sampled
+    assert plan.spec and plan.cta_pred and not plan.sampled
+    src = plan.source
+    assert "per-CTA prediction" in src and "cta_sum2" in src
+    spec = src.split("// ---- speculative pass")[1].split("// exact entry")[0]
+    assert "pred_ + 0" not in spec                        # no last-launch prediction read
+    assert plan.extra_slots() == 3 and "const int ops_[4]" in spec   # 1 reduction + min/max + certified
+    monkeypatch.setenv("GM_SAMPLE", "global")
+    plan = _plan(programs, "bigbird_like", torch.float32, (8, 1024, 768))
+    assert plan.sampled and not plan.cta_pred
     src = plan.source
     assert "sampled prediction" in src and "2654435761" in src and "cta_sum2" in src
-    # the speculative sweep reads the sampled prediction, not the scratch
     spec = src.split("// ---- speculative pass")[1].split("grid_arrive")[0]
     assert "s_pred[0] != 0" in spec and "pred_ + 0" not in spec
     text = '''
