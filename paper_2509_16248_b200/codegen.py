@@ -772,13 +772,19 @@ class Plan:
     SAMPLE_PLAIN = ("amax", "amin", "any", "all")
 
     def _cta_ok(self) -> bool:
-        """Per-CTA prediction (the default where possible): every CTA
+        """Per-CTA prediction (GM_SAMPLE=cta; not the default): every CTA
         predicts the decisions from the first vector of each of its threads —
         data the speculative sweep has just loaded — so the prediction costs a
         CTA-wide combine, not a pass of its own.  CTAs may disagree; the grid
         reduce carries every decision's min and max over CTAs (and whether
         all certified), so all CTAs reach the same verdict."""
-        if os.environ.get("GM_SAMPLE", "cta") != "cta" or self.vfull < 1:
+        # Measured slower than the sampled pass on every workload (the
+        # CTA-wide combine inside the sweep waits for vector 0 of every warp
+        # and adds registers; phi4's randn draw then mispredicts instead of
+        # taking the exact entry): bigbird fp32 16.2 / 18.2 us per kernel vs
+        # 15.1 / 16.0, qwen 19.7 vs 16.9 (profiles/r02_ab_prediction.jsonl).
+        # Kept behind GM_SAMPLE=cta.
+        if os.environ.get("GM_SAMPLE") != "cta" or self.vfull < 1:
             return False
         if not all(r.op in self.SAMPLE_SCALED + self.SAMPLE_PLAIN for r in self.reductions):
             return False

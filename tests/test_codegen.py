@@ -138,11 +138,12 @@ def test_speculative_region_has_adaptive_entries(programs):
 def test_sampled_prediction(programs, monkeypatch):
     """Speculative regions whose reductions have a sample estimate (sum,
     mean, norm, count, max, min, any, all) predict their decisions from data:
-    by default every CTA from the first vector of each of its threads (the
-    sweep's own loads), the grid reduce carrying each decision's min / max
-    over CTAs and whether all certified; GM_SAMPLE=global predicts from one
-    scrambled 4K-element sample in every CTA (a pass of its own).  prod /
-    argmax predicates keep the last launch's decisions."""
+    one scrambled 4K-element sample evaluated in every CTA (the default), or
+    (GM_SAMPLE=cta, measured slower) every CTA from the first vector of each
+    of its threads, the grid reduce carrying each decision's min / max over
+    CTAs and whether all certified.  prod / argmax predicates keep the last
+    launch's decisions."""
+    monkeypatch.setenv("GM_SAMPLE", "cta")
     plan = _plan(programs, "bigbird_like", torch.float32, (8, 1024, 768))
     assert plan.spec and plan.cta_pred and not plan.sampled
     src = plan.source
@@ -150,7 +151,8 @@ def test_sampled_prediction(programs, monkeypatch):
     spec = src.split("// ---- speculative pass")[1].split("// exact entry")[0]
     assert "pred_ + 0" not in spec                        # no last-launch prediction read
     assert plan.extra_slots() == 3 and "const int ops_[4]" in spec   # 1 reduction + min/max + certified
-    monkeypatch.setenv("GM_SAMPLE", "global")
+    assert len(nat.compile_cubin(src, (10, 0))) > 0
+    monkeypatch.delenv("GM_SAMPLE")
     plan = _plan(programs, "bigbird_like", torch.float32, (8, 1024, 768))
     assert plan.sampled and not plan.cta_pred
     src = plan.source
