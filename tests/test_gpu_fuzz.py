@@ -44,6 +44,27 @@ def _expr(rng, names, depth):
     return op.format(*args)
 
 
+def _predicate(rng, names):
+    """One more predicate form (prod / argmax / any / all / count_nonzero
+    reductions of attr_table.cfg, logical and / or / not of 0-d predicates)
+    with an unambiguous outcome.  (Python `and` / `not` / `.item()` in a
+    predicate make the reference's own rewrite raise in eager torch —
+    tests/test_gpu_hardening.py covers those.)"""
+    e = _expr(rng, names, 1)
+    form = rng.randrange(6)
+    if form == 0:
+        return f"torch.sigmoid({e}).prod() > 2.0"                 # product of (0,1) values: always False
+    if form == 1:
+        return f"torch.logical_and(torch.sigmoid({e}).argmax() >= 0, ({e}).abs().sum() >= 0)"
+    if form == 2:
+        return f"torch.logical_not(torch.tanh({e}).amax() > 1.5)"
+    if form == 3:
+        return f"torch.sigmoid({e}).amin() > {rng.choice([1.5, -0.5])}"
+    if form == 4:
+        return f"torch.logical_or((torch.sigmoid({e}) > 2.0).any(), (({e}).abs() >= 0).all())"
+    return f"torch.count_nonzero(torch.relu({e}) + 1.0) > 0"
+
+
 def _program(seed: int, rows: bool) -> str:
     rng = random.Random(seed)
     names = ["x", "y"]
@@ -51,6 +72,15 @@ def _program(seed: int, rows: bool) -> str:
     k = 0
     for s in range(rng.randint(2, 4)):
         kind = rng.random()
+        if kind < 0.15:
+            t = f"v{s}"
+            lines.append(f"    __gm_pred_{k} = {_predicate(rng, names)}")
+            lines.append(f"    __gm_then_{t}_{k} = {_expr(rng, names, 2)}")
+            lines.append(f"    __gm_else_{t}_{k} = {_expr(rng, names, 2)}")
+            lines.append(f"    {t} = torch.where(__gm_pred_{k}, __gm_then_{t}_{k}, __gm_else_{t}_{k})")
+            k += 1
+            names.append(t)
+            continue
         if kind < 0.5:
             # a predicated block in the transform's emitted form
             red = rng.choice(REDS)
@@ -91,7 +121,7 @@ def _program(seed: int, rows: bool) -> str:
 
 SHAPES32 = [(4, 37, 24), (8, 1024, 768), (33, 100), (6, 2, 3, 10)]
 SHAPES16 = [(5, 13, 40), (4, 2048, 64), (7, 24)]
-CASES = [(seed, dtype, shape) for seed in range(40)
+CASES = [(seed, dtype, shape) for seed in range(56)
          for dtype, shape in ((torch.float32, SHAPES32[seed % len(SHAPES32)]),
                               (torch.bfloat16, SHAPES16[seed % len(SHAPES16)]))]
 
