@@ -335,8 +335,9 @@ class Plan:
                 self.host_frees.append(node)
         if len(self.host_frees) > nat.MAX_HS:
             raise Unsupported("too many host scalars")
+        read = {a.uid for n in self.order for a in n.args}
         for node in self.order:
-            if node.op == "free" and node.kind in ("elem", "dscalar"):
+            if node.op == "free" and node.kind in ("elem", "dscalar") and node.uid in read:
                 t = args[node.value]
                 if node.kind == "dscalar":
                     mode = MODE_SCALAR
@@ -581,6 +582,7 @@ class Plan:
                 "sigmoid": f"gm::sigmoid({x})", "tanh": f"tanhf({x})", "exp": f"expf({x})",
                 "log": f"logf({x})", "sqrt": f"gm::fsqrt({x})", "rsqrt": f"gm::recip(gm::fsqrt({x}))",
                 "sin": f"sinf({x})", "cos": f"cosf({x})", "silu": f"gm::silu({x})",
+                "gelu": f"gm::gelu({x})", "gelu_tanh": f"gm::gelu_tanh({x})", "erf": f"erff({x})",
                 "square": f"gm::mul({x}, {x})", "reciprocal": f"gm::recip({x})",
             }
             if op not in un:
@@ -698,6 +700,8 @@ class Plan:
             "sqrt": f"(double)gm::fsqrt((float){x})", "rsqrt": f"(double)gm::recip(gm::fsqrt((float){x}))",
             "sin": f"(double)sinf((float){x})", "cos": f"(double)cosf((float){x})",
             "silu": f"(double)gm::silu((float){x})", "square": f"({x} * {x})",
+            "gelu": f"(double)gm::gelu((float){x})", "gelu_tanh": f"(double)gm::gelu_tanh((float){x})",
+            "erf": f"(double)erff((float){x})",
             "reciprocal": f"(1.0 / {x})",
         }
         if op not in un:

@@ -130,6 +130,15 @@ __device__ __forceinline__ float sigmoid(float a) {
   return y;
 }
 __device__ __forceinline__ float silu(float a) { return __fmul_rn(a, sigmoid(a)); }
+// GELU as torch's CPU kernels evaluate it: (x * 0.5) * (1 + erf(x * M_SQRT1_2)),
+// and the tanh form 0.5 * x * (1 + tanh(sqrt(2 / pi) * (x + 0.044715 * x^3)))
+__device__ __forceinline__ float gelu(float a) {
+  return __fmul_rn(__fmul_rn(a, 0.5f), __fadd_rn(1.f, erff(__fmul_rn(a, 0.70710678118654752f))));
+}
+__device__ __forceinline__ float gelu_tanh(float a) {
+  const float inner = __fmul_rn(0.79788456080286536f, __fadd_rn(a, __fmul_rn(0.044715f, __fmul_rn(__fmul_rn(a, a), a))));
+  return __fmul_rn(__fmul_rn(0.5f, a), __fadd_rn(1.f, tanhf(inner)));
+}
 // exp(a) = 2^(a * log2 e) on the SFU (MUFU.EX2, subnormal results kept):
 // relative error ~2^-22 plus |a| * 2^-24 * ln 2 from rounding the product
 __device__ __forceinline__ float ex2(float a) {

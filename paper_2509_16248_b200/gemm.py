@@ -218,12 +218,40 @@ def matmul(a: torch.Tensor, b: torch.Tensor):
     return _tag(y, "matmul", (a, b))
 
 
+_ln_programs: dict = {}
+
+
+def _layer_norm(mod, x):
+    """nn.LayerNorm over the innermost dim as a row region (rowgen.py): the
+    statement `F.layer_norm(x, (C,), w, b, eps)` lowered once per (eps,
+    affine) and called like any region — one fused kernel instead of ATen's."""
+    key = (float(mod.eps), mod.weight is not None, mod.bias is not None)
+    fn = _ln_programs.get(key)
+    if fn is None:
+        from .lowering import load
+
+        w = "w" if key[1] else "None"
+        b = "b" if key[2] else "None"
+        text = ("import torch\n\ndef ln(x, w, b):\n"
+                f"    return torch.nn.functional.layer_norm(x, (x.shape[-1],), {w}, {b}, {key[0]!r})\n")
+        mod_, _low = load(text)
+        fn = _ln_programs[key] = mod_.ln
+    return fn(x, mod.weight, mod.bias)
+
+
 def module_call(mod, x):
     """`self.<sub>(x)` of the transformed forward: an nn.Linear without hooks
-    runs `linear`; every other module is called as written."""
+    runs `linear`, an nn.LayerNorm over the innermost dim a fused row region;
+    every other module is called as written."""
     if (type(mod) is torch.nn.Linear and not mod._forward_hooks and not mod._forward_pre_hooks
             and torch.is_tensor(x)):
         return linear(x, mod.weight, mod.bias)
+    if (type(mod) is torch.nn.LayerNorm and not mod._forward_hooks and not mod._forward_pre_hooks
+            and torch.is_tensor(x) and x.is_cuda and len(mod.normalized_shape) == 1 and x.dim() >= 1
+            and x.shape[-1] == mod.normalized_shape[0] and x.numel() > 0
+            and x.dtype in (torch.float32, torch.bfloat16, torch.float16)
+            and all(p is None or (p.dtype == x.dtype and p.device == x.device) for p in (mod.weight, mod.bias))):
+        return _layer_norm(mod, x)
     return mod(x)
 
 

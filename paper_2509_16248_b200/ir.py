@@ -36,7 +36,7 @@ ITEM = "item"
 
 UNARY = {
     "neg", "pos", "abs", "relu", "sigmoid", "tanh", "exp", "log", "sqrt", "rsqrt", "sin", "cos",
-    "silu", "square", "reciprocal", "logical_not",
+    "silu", "square", "reciprocal", "logical_not", "gelu", "gelu_tanh", "erf",
 }
 BINARY = {"add", "sub", "mul", "div", "pow", "maximum", "minimum", "gt", "ge", "lt", "le", "eq", "ne",
           "logical_and", "logical_or", "floordiv", "mod", "fmod"}
@@ -47,8 +47,9 @@ REDUCE = {"sum", "mean", "amax", "amin", "norm", "prod", "any", "all", "count_no
 # 265-289 admits any torch.* call in an arm).  They run in the row-region
 # kernel (rowgen.py), one row per thread group, the row held on chip.
 # Node.value = (dim, keepdim) as written; infer() checks dim is the last one.
-ROW_RED = {"row_sum": "sum", "row_mean": "mean", "row_amax": "amax", "row_amin": "amin"}
-ROW_NORM = {"softmax", "log_softmax"}
+ROW_RED = {"row_sum": "sum", "row_mean": "mean", "row_amax": "amax", "row_amin": "amin", "row_var": "var",
+           "row_std": "std"}
+ROW_NORM = {"softmax", "log_softmax", "layer_norm"}
 ROW_OPS = set(ROW_RED) | ROW_NORM
 # reductions whose result is an integer count/sum: accumulated exactly in fp64
 INT_REDUCE = {"count_nonzero", "nzsum"}
@@ -76,7 +77,7 @@ _TORCH_FUNCS = {
     "clip": "clamp", "sum": "sum", "mean": "mean", "amax": "amax", "amin": "amin", "prod": "prod",
     "any": "any", "all": "all", "count_nonzero": "count_nonzero", "norm": "norm",
     "argmax": "argmax", "argmin": "argmin", "max": "max", "min": "min",
-    "softmax": "softmax", "log_softmax": "log_softmax",
+    "softmax": "softmax", "log_softmax": "log_softmax", "gelu": "gelu", "erf": "erf", "var": "var", "std": "std",
     "floor_divide": "floordiv", "remainder": "mod", "fmod": "fmod",
 }
 # Tensor.<name>(...) spellings (pure_ops.cfg plus the attr_table reductions)
@@ -188,6 +189,42 @@ class Builder:
             if k in kw:
                 return self._const_int(kw[k])
         raise Unsupported("missing dim")
+
+    def layer_norm(self, c: ast.Call) -> Node:
+        """F.layer_norm(x, (C,), weight=None, bias=None, eps=1e-5) over the
+        innermost dim (a one-element normalized_shape): a row operator.
+        Missing weight / bias are the constants 1 / 0 (exact: x * 1 and
+        x + 0 change no bits but -0 + 0)."""
+        pos = list(c.args)
+        kw = {k.arg: k.value for k in c.keywords}
+        if None in kw or any(isinstance(a, ast.Starred) for a in pos):
+            raise Unsupported("layer_norm arguments")
+        names = ["input", "normalized_shape", "weight", "bias", "eps"]
+        vals = dict(zip(names, pos))
+        for k, v in kw.items():
+            if k not in names or k in vals:
+                raise Unsupported(f"layer_norm keyword {k}")
+            vals[k] = v
+        if "input" not in vals or "normalized_shape" not in vals:
+            raise Unsupported("layer_norm arguments")
+        ns = vals["normalized_shape"]
+        if not (isinstance(ns, (ast.Tuple, ast.List)) and len(ns.elts) == 1):
+            raise Unsupported("layer_norm over more than the innermost dim")
+        eps = 1e-5
+        if "eps" in vals:
+            e = vals["eps"]
+            if not (isinstance(e, ast.Constant) and isinstance(e.value, (int, float))):
+                raise Unsupported("non-constant eps")
+            eps = float(e.value)
+        x = self.expr(vals["input"])
+
+        def opt(key, default):
+            v = vals.get(key)
+            if v is None or (isinstance(v, ast.Constant) and v.value is None):
+                return self.const(default)
+            return self.expr(v)
+
+        return self.op("layer_norm", x, opt("weight", 1.0), opt("bias", 0.0), value=(-1, True, eps))
 
     def _row_reduce(self, name: str, args: list, kw: dict) -> Node:
         """x.sum(-1, keepdim=True) / x.mean(dim=-1) / x.amax(-1) / torch.sum(x, -1)."""
@@ -311,6 +348,8 @@ class Builder:
             or (len(chain) == 2 and chain[0] in self.functional_names)
             or (len(chain) == 4 and chain[0] in self.torch_names and chain[1:3] == ["nn", "functional"])
         )
+        if is_torch and chain[-1] == "layer_norm":
+            return self.layer_norm(c)
         if is_torch:
             name = _TORCH_FUNCS.get(chain[-1])
             if name is None:
@@ -340,6 +379,19 @@ class Builder:
                 return self.op("maximum" if name == "max" else "minimum", args[0], args[1])
             # max(dim) / min(dim) return (values, indices): not a tensor
             raise Unsupported(f"{name} with dim")
+        if name in ("var", "std"):
+            corr = 1
+            if "unbiased" in kw:
+                u = kw.pop("unbiased")
+                if not (isinstance(u, ast.Constant) and isinstance(u.value, bool)):
+                    raise Unsupported("non-constant unbiased")
+                corr = 1 if u.value else 0
+            if "correction" in kw:
+                cv = kw.pop("correction")
+                corr = self._const_int(cv)
+            node = self._row_reduce(name, args, kw)
+            node.value = node.value + (corr,)
+            return node
         if name in ("sum", "mean", "amax", "amin") and (len(args) > 1 or kw):
             return self._row_reduce(name, args, kw)
         if name in ("softmax", "log_softmax"):
@@ -355,6 +407,12 @@ class Builder:
             if len(args) != 1 or kw or not method:
                 raise Unsupported("item arguments")
             return self.op(ITEM, args[0])
+        if name == "gelu" and "approximate" in kw:
+            v = kw.pop("approximate")
+            if not (isinstance(v, ast.Constant) and v.value in ("none", "tanh")):
+                raise Unsupported("gelu approximate")
+            if v.value == "tanh":
+                name = "gelu_tanh"
         if name in UNARY:
             if len(args) != 1 or kw:
                 raise Unsupported(f"{name} arguments")
@@ -416,6 +474,9 @@ META_FNS = {
     "sin": lambda a: torch.sin(a),
     "cos": lambda a: torch.cos(a),
     "silu": lambda a: torch.nn.functional.silu(a),
+    "gelu": lambda a: torch.nn.functional.gelu(a),
+    "gelu_tanh": lambda a: torch.nn.functional.gelu(a, approximate="tanh"),
+    "erf": lambda a: torch.erf(a),
     "square": lambda a: torch.square(a),
     "reciprocal": lambda a: torch.reciprocal(a),
     "logical_not": lambda a: torch.logical_not(a),
@@ -453,15 +514,25 @@ META_FNS = {
 }
 
 
-def _meta_row(node: Node, a):
+def _meta_row(node: Node, a, rest=()):
     """Row operators: torch's own result; the dim must be the innermost."""
-    dim, keep = node.value
+    dim, keep = node.value[:2]
     if not torch.is_tensor(a) or a.dim() == 0:
         raise Unsupported(f"{node.op} of a scalar")
     if dim not in (-1, a.dim() - 1):
         raise Unsupported(f"{node.op} over dim {dim} (only the innermost dim is fused)")
+    if node.op == "layer_norm":
+        w, b = rest
+        for t in (w, b):
+            if torch.is_tensor(t) and tuple(t.shape) != (a.shape[-1],):
+                raise Unsupported("layer_norm weight / bias not of the row's length")
+        w = w if torch.is_tensor(w) else None
+        b = b if torch.is_tensor(b) else None
+        return torch.nn.functional.layer_norm(a, (a.shape[-1],), w, b, node.value[2])
     if node.op in ROW_NORM:
         return getattr(torch, node.op)(a, -1)
+    if node.op in ("row_var", "row_std"):
+        return getattr(a, ROW_RED[node.op])(-1, keepdim=keep, correction=node.value[2])
     return getattr(a, ROW_RED[node.op])(-1, keepdim=keep)
 
 
@@ -529,7 +600,7 @@ def infer(graph: Graph, args: list, needed: list[Node]) -> None:
                 elif node.op in (BOOL_AND, BOOL_OR, BOOL_NOT):
                     v = _meta_bool(node.op, vals)
                 elif node.op in ROW_OPS:
-                    v = _meta_row(node, vals[0])
+                    v = _meta_row(node, vals[0], vals[1:])
                 else:
                     if all(not torch.is_tensor(x) for x in vals) and node.op not in (
                         "add", "sub", "mul", "div", "pow", "neg", "pos", "abs", "gt", "ge", "lt", "le", "eq", "ne",
@@ -587,7 +658,7 @@ def evaluate(roots: list[Node], args: list) -> dict[int, Any]:
             elif node.op == NZSUM:
                 v = torch.nonzero(a[0]).sum()
             elif node.op in ROW_OPS:
-                v = _meta_row(node, a[0])
+                v = _meta_row(node, a[0], a[1:])
             else:
                 v = META_FNS[node.op](*a)
         vals[node.uid] = v

@@ -117,7 +117,10 @@ class RowPlan(Plan):
         nokeep = S[:-1]
         # rowval: one value per row; full: one value per element of S
         self.rowval: set[int] = set()
+        read = {a.uid for n in self.order for a in n.args}
         for node in self.order:
+            if node.op == "free" and node.uid not in read:
+                continue  # only passed through as an output alias
             if node.kind == "elem":
                 if not is_fusable_dtype(node.dtype):
                     raise Unsupported(f"elementwise dtype {node.dtype}")
@@ -544,13 +547,46 @@ class RowPlan(Plan):
         if x.dtype == torch.bool:
             raise Unsupported("row sum of a bool tensor")
         self._row_stat(w, f"st{n.uid}", x, "sum")
-        val = f"st{n.uid}" if fn == "sum" else f"__fdiv_rn(st{n.uid}, {float(self.C)!r}f)"
+        if fn in ("var", "std"):
+            # two passes over the row held in registers: mean, then the sum
+            # of squared deviations (torch's CPU var is a Welford / two-pass
+            # equivalent), divided by C - correction
+            corr = n.value[2]
+            w(f"  const float mu{n.uid} = __fdiv_rn(st{n.uid}, {float(self.C)!r}f);")
+            self._row_stat(w, f"sq{n.uid}", x, "sum",
+                           expr=lambda u: f"gm::mul(gm::sub(n{x.uid}_{u}[l], mu{n.uid}), gm::sub(n{x.uid}_{u}[l], mu{n.uid}))")
+            den = float(max(self.C - corr, 0))
+            val = f"__fdiv_rn(sq{n.uid}, {den!r}f)"
+            if fn == "std":
+                val = f"gm::fsqrt({val})"
+        else:
+            val = f"st{n.uid}" if fn == "sum" else f"__fdiv_rn(st{n.uid}, {float(self.C)!r}f)"
         w(f"  rs{n.uid} = {R}({val});" if R else f"  rs{n.uid} = {val};")
 
     def _emit_row_norm(self, w, n: Node) -> None:
         x = n.args[0]
         U = self.U
         R = _round_f(n.dtype)
+        if n.op == "layer_norm":
+            # torch's CPU LayerNorm: mean, rstd = 1 / sqrt(var + eps), then
+            # (x * rstd + (-rstd * mean)) * weight + bias, in fp32
+            if self._skip_round(n):
+                R = ""
+            wt, bs = n.args[1], n.args[2]
+            self._row_stat(w, f"ls{n.uid}", x, "sum")
+            w(f"  const float mu{n.uid} = __fdiv_rn(ls{n.uid}, {float(self.C)!r}f);")
+            self._row_stat(w, f"lq{n.uid}", x, "sum",
+                           expr=lambda u: f"gm::mul(gm::sub(n{x.uid}_{u}[l], mu{n.uid}), gm::sub(n{x.uid}_{u}[l], mu{n.uid}))")
+            w(f"  const float rstd{n.uid} = __frcp_rn(gm::fsqrt(gm::add(__fdiv_rn(lq{n.uid}, {float(self.C)!r}f), "
+              f"{float(n.value[2])!r}f)));")
+            w(f"  const float bia{n.uid} = gm::mul(-rstd{n.uid}, mu{n.uid});")
+            for u in range(U):
+                wv = self._ev(wt, "l", u) if wt.kind == "elem" else self._sf(wt)
+                bv = self._ev(bs, "l", u) if bs.kind == "elem" else self._sf(bs)
+                body = (f"gm::add(gm::mul(gm::add(gm::mul(n{x.uid}_{u}[l], rstd{n.uid}), bia{n.uid}), {wv}), {bv})")
+                w(f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = {R}({body});" if R else
+                  f"#pragma unroll\n  for (int l = 0; l < GM_VEC; ++l) n{n.uid}_{u}[l] = {body};")
+            return
         if self._skip_round(n):
             R = ""
         m = f"mx{n.uid}"

@@ -156,3 +156,53 @@ def test_mixed_shapes(shape, dtype):
         x = torch.randn(shape).to(dtype)
         b = (torch.rand(shape[-1]) * sign).to(dtype)
         _run(MIXED, [x, b], dtype, expect_row=None)
+
+
+LAYER = '''
+import torch
+import torch.nn.functional as F
+def f(x, w, b):
+    h = F.gelu(x) + torch.erf(x) * 0.5 + F.gelu(x, approximate="tanh")
+    y = F.layer_norm(h, (x.shape[-1],), w, b, 1e-12)
+    z = y + x.var(-1, keepdim=True) - x.std(-1, unbiased=False, keepdim=True)
+    return z
+'''
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("shape", [(8, 1024, 768), (4, 7, 20)], ids=["bigbird", "ragged"])
+def test_layer_norm_gelu_var(shape, dtype):
+    """GELU (erf and tanh forms), erf, layer_norm with weight and bias, var
+    and std over the innermost dim — one row kernel."""
+    torch.manual_seed(8)
+    x = torch.randn(shape).to(dtype)
+    w = torch.randn(shape[-1]).to(dtype)
+    b = torch.randn(shape[-1]).to(dtype)
+    low = _run(LAYER, [x, w, b], dtype)
+    assert len(low.regions) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+def test_layernorm_module_is_a_row_region(dtype):
+    """`self.ln(x)` with an nn.LayerNorm runs the fused row kernel (gemm.module_call)."""
+    from paper_2509_16248_b200 import gemm
+
+    torch.manual_seed(9)
+    ln = torch.nn.LayerNorm(768, eps=1e-12).to(dtype)
+    with torch.no_grad():
+        ln.weight.normal_()
+        ln.bias.normal_()
+    x = torch.randn(8, 1024, 768).to(dtype)
+    with torch.no_grad():
+        ref = ln(x)
+    lnc = ln.cuda()
+    with torch.no_grad():
+        y = gemm.module_call(lnc, x.cuda())
+    fn = gemm._ln_programs[(1e-12, True, True)]
+    assert fn is not None
+    # noise yardstick: the same layer norm evaluated in fp64 and rounded
+    n64 = torch.nn.functional.layer_norm(x.double(), (768,), ln.weight.double().cpu(), ln.bias.double().cpu(),
+                                         1e-12).to(dtype)
+    assert_parity(y, ref, dtype, what="nn.LayerNorm", noise=n64)
