@@ -42,6 +42,8 @@ WORKLOADS = {
     "gemm_arms": ("config 2 variant: BigBird-shaped layer whose predicated arms each hold a GEMM", None),
     "bigbird_attn": ("config 2 with attention: BigBird-RoBERTa-base-shaped self-attention, 12 heads, "
                      "block-sparse / full softmax over [8,12,1024,1024] scores", None),
+    "bigbird_layer": ("config 2 as a full encoder layer: BigBird-RoBERTa-base-shaped attention + FFN 3072 + "
+                      "post-LayerNorms + GELU, block-sparse / full softmax", None),
     "phi4_like": ("config 5: corpus phi4_like at [8,1024,768]", [[8, 1024, 768]]),
     "qwen_audio_like": ("config 5: corpus qwen_audio_like at [8,1024,768]", [[8, 1024, 768]]),
     "longformer_like": ("config 3: corpus longformer_like at [4,4096,768]", [[4, 4096, 768]]),

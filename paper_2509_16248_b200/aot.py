@@ -29,6 +29,7 @@ SPECS = [("bigbird_like", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("bart_step", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("gemm_arms", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("bigbird_attn", d, None) for d in (torch.bfloat16, torch.float32)] + \
+        [("bigbird_layer", d, None) for d in (torch.bfloat16, torch.float32)] + \
         [("toy", torch.float32, None)]
 
 

@@ -367,12 +367,30 @@ class _FunctionLowerer:
                     return ast.UnaryOp(e.op, split(e.operand))
                 if isinstance(e, ast.Call) and not e.keywords and not any(isinstance(a, ast.Starred) for a in e.args):
                     n_temps = len(temps)
-                    cand = ast.Call(e.func, [split(a) for a in e.args], [])
+                    args = [split(a) for a in e.args]
+                    cand = ast.Call(e.func, args, [])
                     if self._fusable(cand):
                         return cand
-                    # the call itself is hoisted: its arguments as written
-                    # (temporaries made for them would be dead)
-                    del temps[n_temps:]
+                    if attr_chain(e.func) is not None and attr_chain(e.func)[0] == "self":
+                        # a module call `self.m(<fusable expr>)`: the argument
+                        # becomes its own statement (a fused region: e.g. the
+                        # residual add before a LayerNorm) and the call reads it
+                        hoisted = []
+                        for a in args:
+                            if self._fusable(a) and not isinstance(a, (ast.Name, ast.Constant)):
+                                tn = f"__gm_t_{self.owner.next_tmp()}"
+                                temps.append(ast.copy_location(ast.Assign(targets=[ast.Name(tn, ast.Store())],
+                                                                          value=a), s))
+                                # read by the call, which follows the temp's statement
+                                self.loads.append(((s.end_lineno, s.end_col_offset + 1), tn))
+                                hoisted.append(ast.Name(tn, ast.Load()))
+                            else:
+                                hoisted.append(a)
+                        e = ast.Call(e.func, hoisted, [])
+                    else:
+                        # the call itself is hoisted: its arguments as written
+                        # (temporaries made for them would be dead)
+                        del temps[n_temps:]
                 name = f"__gm_t_{self.owner.next_tmp()}"
                 temps.append(ast.copy_location(ast.Assign(targets=[ast.Name(name, ast.Store())], value=e), s))
                 self.loads.append(((s.lineno, s.col_offset + 1), name))
@@ -385,6 +403,16 @@ class _FunctionLowerer:
                 res = ast.copy_location(ast.Assign(targets=s.targets, value=temps[0].value), s)
                 res.end_lineno, res.end_col_offset = s.end_lineno, s.end_col_offset
                 out.append(res)
+                continue
+            if (isinstance(new_value, ast.Name) and len(temps) > 1 and isinstance(temps[-1].targets[0], ast.Name)
+                    and temps[-1].targets[0].id == new_value.id):
+                # the statement is a call whose arguments were hoisted (a
+                # module call on a fusable expression): the argument
+                # statements, then the call assigned to the original target
+                res = ast.copy_location(ast.Assign(targets=s.targets, value=temps[-1].value), s)
+                res.end_lineno, res.end_col_offset = s.end_lineno, s.end_col_offset
+                ast.fix_missing_locations(res)
+                out.extend(temps[:-1] + [res])
                 continue
             if not temps or isinstance(new_value, ast.Name) or not self._fusable(new_value):
                 out.append(s)

@@ -13,7 +13,7 @@ from parity import has_row_reduction, rowop_fp64_reference, assert_parity, check
 
 CORPUS = ["biogpt_like", "blenderbot_like", "flan_t5_like", "longformer_like", "moe_minicpm_like",
           "pegasus_like", "phi4_like", "qwen_audio_like"]
-WORKLOADS = ["toy", "bigbird_like", "bart_step", "gemm_arms", "bigbird_attn"]
+WORKLOADS = ["toy", "bigbird_like", "bart_step", "gemm_arms", "bigbird_attn", "bigbird_layer"]
 
 
 def _run(programs, name, idx, dtype=None, scaled=False):

@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 SHAPES = {
-    "bigbird_like": None, "bart_step": None, "toy": None, "bigbird_attn": None, "gemm_arms": None,
+    "bigbird_like": None, "bart_step": None, "toy": None, "bigbird_attn": None, "bigbird_layer": None, "gemm_arms": None,
     "phi4_like": [[8, 1024, 768]], "qwen_audio_like": [[8, 1024, 768]], "biogpt_like": [[8, 1024, 768]] * 2,
     "blenderbot_like": [[8, 1024, 768]], "pegasus_like": [[8, 1024, 768]],
     "flan_t5_like": [[8192, 768], [768, 768]], "longformer_like": [[4, 4096, 768]],

@@ -11,12 +11,12 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${R}
 timeout 900 python bench.py > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/${R}_bench_ref.json 2> gpurun_out/${R}_bench_ref.err
 : > gpurun_out/${R}_sweep.jsonl
-for w in bigbird_like bigbird_attn gemm_arms bart_step longformer_like phi4_like qwen_audio_like biogpt_like blenderbot_like flan_t5_like pegasus_like moe_minicpm_like; do
+for w in bigbird_like bigbird_attn bigbird_layer gemm_arms bart_step longformer_like phi4_like qwen_audio_like biogpt_like blenderbot_like flan_t5_like pegasus_like moe_minicpm_like; do
   for d in bf16 fp32; do
     timeout 600 python bench.py --workload $w --dtype $d --steps 100 --warmup 10 --no-compile --no-cpu-baseline 2>/dev/null >> gpurun_out/${R}_sweep.jsonl || echo "{\"workload\": \"$w\", \"dtype\": \"$d\", \"error\": true}" >> gpurun_out/${R}_sweep.jsonl
   done
 done
-ALL=bigbird_like,bigbird_attn,gemm_arms,bart_step,longformer_like,phi4_like,qwen_audio_like,biogpt_like,blenderbot_like,flan_t5_like,pegasus_like,moe_minicpm_like
+ALL=bigbird_like,bigbird_attn,bigbird_layer,gemm_arms,bart_step,longformer_like,phi4_like,qwen_audio_like,biogpt_like,blenderbot_like,flan_t5_like,pegasus_like,moe_minicpm_like
 timeout 1800 python tools/compare_inductor.py --workloads $ALL --dtype fp32 > gpurun_out/${R}_inductor_fp32.jsonl 2>/dev/null
 timeout 1800 python tools/compare_inductor.py --workloads $ALL --dtype bf16 > gpurun_out/${R}_inductor_bf16.jsonl 2>/dev/null
 timeout 1800 python tools/compare_frontdoor.py > gpurun_out/${R}_frontdoor.jsonl 2>/dev/null
