@@ -26,7 +26,7 @@ def test_reference_arm_line():
     assert d["unit"] == "samples/s" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
-    assert d["config"]["workload"].startswith("bigbird_like") and d["dtype"] == "fp32"
+    assert d["config"]["workload"].startswith("bigbird_layer") and d["dtype"] == "fp32"
     assert set(d["config"]) == {"workload", "batch", "shape", "inputs"}   # identical keys in both arms
 
 
@@ -40,24 +40,26 @@ def test_b200_arm_line():
     assert set(d["config"]) == {"workload", "batch", "shape", "inputs"}
     assert d["host_syncs_per_forward"] == 0 and d["mode"] == "graph"
     assert d["host_syncs_profiler"]["cuda_syncs"] == 0 and d["host_syncs_profiler"]["d2h_copies"] == 0
-    # two fused regions + two fp32 GEMMs (cuBLASLt BF16x9) per forward
-    assert d["gpu_launches_per_forward"] == 4 and d["gpu_launches"] == 5 * 4
-    # the rotating inputs change the branch decisions every step; the fp32
-    # regions predict them from a sample of each input (no misses)
+    # config 2 as a full encoder layer: the predicate's grid region, the
+    # softmax row region, the residual adds, GELU, the two LayerNorm row
+    # regions, the head split / merge gathers and the fp32 GEMMs (BF16x9)
+    assert d["gpu_launches_per_forward"] >= 12 and d["gpu_launches"] == 5 * d["gpu_launches_per_forward"]
     sp = d["speculation"]
-    assert sp["launches"] == 5 * 2 and sp["mispredictions"] == 0
-    assert sp["speculated"] + sp["exact_entries"] == sp["launches"]
+    assert sp["launches"] == 0 and sp["mispredictions"] == 0   # a one-pass predicate feeding a row kernel
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 8 * 1024 * 768 * 4
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5 and r["peak"] > 0
-    assert all(k["speculative"] for k in d["kernels"])
+    assert r["kernel"].startswith("gm_row_")          # the softmax arms dominate
     # the grid kernels time themselves inside the timed loop (in-kernel
-    # %globaltimer, one launch per step and region); the event-bracketed
-    # duration of the same kernel includes the graph's launch gaps
+    # %globaltimer, one launch per step and region); row kernels are timed by
+    # CUDA events around their launch in a replay of the same graph
     for k in d["kernels"]:
-        assert k["how"].startswith("live, in-kernel") and "over the 5 launches" in k["how"], k["how"]
-        assert 0 < k["ms"] <= k["ms_events"] * 1.05, (k["ms"], k["ms_events"])
+        if k["name"].startswith("gm_region_"):
+            assert k["how"].startswith("live, in-kernel") and "over the 5 launches" in k["how"], k["how"]
+            assert 0 < k["ms"] <= k["ms_events"] * 1.05, (k["ms"], k["ms_events"])
+        else:
+            assert k["how"].startswith("live: CUDA events") and k["ms"] > 0
 
 
 @pytest.mark.gpu
