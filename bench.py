@@ -228,7 +228,8 @@ def run_reference(args, ws, rank):
     """`--impl reference`: the reference's CPU path on the box's host cores,
     rank 0 only (the other ranks exit without work).  Each of the K timed
     steps is a bounded sample: eager forwards over the rotating inputs for
-    ~10 s / K, so the whole run is a ~10 s window like `cpu_baseline`."""
+    ~30 s / K (of a sub-batch when one full-batch forward exceeds that), so
+    the whole run is a ~30 s window."""
     if rank != 0:
         return
     import torch
@@ -246,10 +247,11 @@ def run_reference(args, ws, rank):
     # step's share of the ~10 s window, else of its first `sub` samples (the
     # same program on the same data, fewer rows) — so a slow CPU forward
     # (the full bigbird_layer is ~2 s on 16 cores) keeps the run to minutes
+    orc.call_captured(fn, xs[0])                 # first call: lazy initialisation
     t0 = time.perf_counter()
-    orc.call_captured(fn, xs[0])
+    orc.call_captured(fn, xs[1 % len(xs)])
     t_full = time.perf_counter() - t0
-    per_step = 10.0 / max(1, args.steps)
+    per_step = 30.0 / max(1, args.steps)         # a ~30 s window over the K steps
     sub = max(1, min(batch, int(batch * per_step / max(t_full, 1e-9))))
     xsub = [[t[:sub] if torch.is_tensor(t) and t.dim() and t.shape[0] == batch else t for t in x] for x in xs]
     for k in range(args.warmup):
