@@ -440,6 +440,11 @@ def main():
     entry = ex.prepare(*xs_dev[0])
     torch.cuda.synchronize(dev)
     cold_ms = 1e3 * (time.perf_counter() - t0)
+    # the program's own regions and the row regions behind its module calls
+    # (nn.LayerNorm, gemm.module_call)
+    from paper_2509_16248_b200 import gemm as gemm_
+
+    all_regions = list(low.regions) + gemm_.module_regions(getattr(mod, prog["callable"], None))
     info = entry.info
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     flush_rd = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.int64, device=dev)
@@ -459,7 +464,7 @@ def main():
 
     def spec_totals():
         tot = [0, 0, 0]
-        for r in low.regions:
+        for r in all_regions:
             sp = r.last_spec
             if sp is not None and sp.plan.spec:
                 a, b = sp.spec_stats()
@@ -490,7 +495,7 @@ def main():
                 break
         barrier()
         spec0 = spec_totals()
-        fused_specs = [r.last_spec for r in low.regions if r.last_spec is not None]
+        fused_specs = [r.last_spec for r in all_regions if r.last_spec is not None]
         for sp in fused_specs:
             sp.set_live(True)        # grid kernels time themselves inside the graph
         for i in range(args.steps):
@@ -502,12 +507,12 @@ def main():
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     live_timer = {}
-    for r in low.regions:
+    for r in all_regions:
         if r.last_spec is not None:
             tot, n = r.last_spec.live_stats()
             r.last_spec.set_live(False)
             if n:
-                live_timer[r.rid] = (tot / n / 1e6, n)
+                live_timer[id(r)] = (tot / n / 1e6, n)
     spec1 = spec_totals()
     ex.flush()
     total_ms = max_over_ranks(sum(step_ms), pg)
@@ -523,24 +528,24 @@ def main():
     # ---- each fused kernel timed on its own stream, cold L2: a CUDA graph of
     #      R x [256 MB L2 flush, region launch] minus a graph of R x [flush],
     #      both replayed between CUDA events (no host work inside the window)
-    fused = [r for r in low.regions if r.last_spec is not None]
-    live = _live_kernel_ms(ex, low, xs_dev, flush_l2, dev, args.steps)
+    fused = [r for r in all_regions if r.last_spec is not None]
+    live = _live_kernel_ms(ex, fused, xs_dev, flush_l2, dev, args.steps)
     kernels = []
     for r in fused:
         spec = r.last_spec
         nbytes = spec.bytes_alg(list(r.last_args))
-        if r.rid in live_timer:
-            ms, how = live_timer[r.rid][0], (
+        if id(r) in live_timer:
+            ms, how = live_timer[id(r)][0], (
                 f"live, in-kernel: %globaltimer from CTA 0's start (after griddepcontrol.wait) to the last CTA's "
-                f"exit, summed by the kernel over the {live_timer[r.rid][1]} launches of the timed loop itself, mean")
+                f"exit, summed by the kernel over the {live_timer[id(r)][1]} launches of the timed loop itself, mean")
         else:
-            ms, how = live.get(r.rid, float("nan")), (
+            ms, how = live.get(id(r), float("nan")), (
                 "live: CUDA events captured around the launch inside the forward's graph, replayed over the "
                 "rotating inputs with the L2 flushed before every step (the timed loop's conditions), mean")
         k = {"name": f"{spec.plan.kernel} ({r.name})", "ms": ms,
              "bytes": nbytes, "grid": spec.grid, "smem": spec.smem,
              "passes": spec.plan.npass, "speculative": spec.plan.spec,
-             "how": how, "ms_events": live.get(r.rid, float("nan")),
+             "how": how, "ms_events": live.get(id(r), float("nan")),
              "ms_isolated": _time_kernel_flushed(spec, list(r.last_args), flush_l2, dev),
              "isolated_how": "graph of 20 x (L2 flush + launch) minus 20 x flush; cold L2; one input"}
         if spec.plan.spec:
@@ -697,7 +702,7 @@ def _copy_only_pipeline(x_host, outs, dev, steps: int) -> float:
     return time.perf_counter() - t0
 
 
-def _live_kernel_ms(ex, low, xs_dev, flush, dev, steps: int) -> dict:
+def _live_kernel_ms(ex, regions, xs_dev, flush, dev, steps: int) -> dict:
     """Per-region kernel duration (ms, mean) inside the forward's own CUDA
     graph under the timed loop's conditions: a fresh graph slot is captured
     with a pair of external CUDA events around every region launch, then
@@ -705,14 +710,13 @@ def _live_kernel_ms(ex, low, xs_dev, flush, dev, steps: int) -> dict:
     before each step; the events are read after each replay."""
     import torch
 
-    regions = [r for r in low.regions if r.last_spec is not None]
     for r in regions:
         r.probe = (torch.cuda.Event(enable_timing=True, external=True),
                    torch.cuda.Event(enable_timing=True, external=True))
     try:
         entry = ex.prepare(*xs_dev[0], slot="probe")
     finally:
-        probes = {r.rid: r.probe for r in regions}
+        probes = {id(r): r.probe for r in regions}
         for r in regions:
             r.probe = None
     acc = {rid: [] for rid in probes}

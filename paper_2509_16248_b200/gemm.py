@@ -25,6 +25,7 @@ import ctypes
 import functools
 import math
 import threading
+import weakref
 
 import torch
 
@@ -218,25 +219,42 @@ def matmul(a: torch.Tensor, b: torch.Tensor):
     return _tag(y, "matmul", (a, b))
 
 
-_ln_programs: dict = {}
+_ln_programs: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def _layer_norm(mod, x):
     """nn.LayerNorm over the innermost dim as a row region (rowgen.py): the
-    statement `F.layer_norm(x, (C,), w, b, eps)` lowered once per (eps,
-    affine) and called like any region — one fused kernel instead of ATen's."""
+    statement `F.layer_norm(x, (C,), w, b, eps)` lowered once per module (its
+    own Region, so its launches are counted and timed apart from the other
+    LayerNorms of the forward; the kernel source, and so the compiled cubin,
+    is shared by modules with the same eps / affine form) and called like any
+    region — one fused kernel instead of ATen's."""
     key = (float(mod.eps), mod.weight is not None, mod.bias is not None)
-    fn = _ln_programs.get(key)
-    if fn is None:
+    ent = _ln_programs.get(mod)
+    if ent is None or ent[0] != key:
         from .lowering import load
 
         w = "w" if key[1] else "None"
         b = "b" if key[2] else "None"
         text = ("import torch\n\ndef ln(x, w, b):\n"
                 f"    return torch.nn.functional.layer_norm(x, (x.shape[-1],), {w}, {b}, {key[0]!r})\n")
-        mod_, _low = load(text)
-        fn = _ln_programs[key] = mod_.ln
-    return fn(x, mod.weight, mod.bias)
+        mod_, low = load(text)
+        for r in low.regions:
+            r.name = f"nn.LayerNorm #{len(_ln_programs) + 1}"
+        ent = _ln_programs[mod] = (key, mod_.ln, low)
+    return ent[1](x, mod.weight, mod.bias)
+
+
+def module_regions(model) -> list:
+    """The fused regions behind module calls of `model`'s submodules (the
+    LayerNorm row regions), in creation order: for reports and timing next
+    to the lowered program's own regions."""
+    mods = set(id(m) for m in model.modules()) if isinstance(model, torch.nn.Module) else None
+    res = []
+    for mod, (_key, _fn, low) in list(_ln_programs.items()):
+        if mods is None or id(mod) in mods:
+            res.extend(low.regions)
+    return res
 
 
 def module_call(mod, x):

@@ -200,8 +200,9 @@ def test_layernorm_module_is_a_row_region(dtype):
     lnc = ln.cuda()
     with torch.no_grad():
         y = gemm.module_call(lnc, x.cuda())
-    fn = gemm._ln_programs[(1e-12, True, True)]
-    assert fn is not None
+    regions = gemm.module_regions(lnc)
+    assert len(regions) == 1 and regions[0].stats.launches == 1 and regions[0].last_spec is not None
+    assert regions[0].name.startswith("nn.LayerNorm")
     # noise yardstick: the same layer norm evaluated in fp64 and rounded
     n64 = torch.nn.functional.layer_norm(x.double(), (768,), ln.weight.double().cpu(), ln.bias.double().cpu(),
                                          1e-12).to(dtype)
