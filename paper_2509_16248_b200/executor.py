@@ -84,16 +84,17 @@ def _watch_side_effects():
         root.setLevel(old)
 
 
+_SCALARS = (int, float, bool, str, type(None))
+
+
 def _key(args) -> tuple:
-    k = []
-    for a in args:
-        if isinstance(a, torch.nn.Parameter):
-            k.append(("p", id(a)))          # read in place (see _Entry)
-        elif torch.is_tensor(a):
-            k.append(("t", a.dtype, tuple(a.shape)))
-        else:
-            k.append(("v", type(a), a if isinstance(a, (int, float, bool, str, type(None))) else id(a)))
-    return tuple(k)
+    """The entry key of a call: parameters by identity (read in place, see
+    _Entry), other tensors by dtype and shape, plain scalars by value."""
+    P, T = torch.nn.Parameter, torch.Tensor
+    return tuple(("p", id(a)) if type(a) is P
+                 else ("t", a.dtype, a.shape) if isinstance(a, T)
+                 else ("v", type(a), a if isinstance(a, _SCALARS) else id(a))
+                 for a in args)
 
 
 @dataclass

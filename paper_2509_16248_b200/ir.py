@@ -347,6 +347,8 @@ class Builder:
             (len(chain) == 2 and chain[0] in self.torch_names)
             or (len(chain) == 2 and chain[0] in self.functional_names)
             or (len(chain) == 4 and chain[0] in self.torch_names and chain[1:3] == ["nn", "functional"])
+            # Dynamo's FX spelling of the functional ops (`torch._C._nn.gelu`)
+            or (len(chain) == 4 and chain[0] in self.torch_names and chain[1:3] == ["_C", "_nn"])
         )
         if is_torch and chain[-1] == "layer_norm":
             return self.layer_norm(c)

@@ -298,20 +298,14 @@ class _FunctionLowerer:
             if roots & rebound:
                 i += 1
                 continue
-            kinds = set()
-            for j in uses:
-                if not self._eligible(out[j]):
-                    continue
-                try:
-                    gj, _ = self._build([out[j]])
-                except Unsupported:
-                    continue
-                oj = {n.op for n in gj.nodes}
-                if oj & ROW_OPS:
-                    kinds.add("row")
-                if oj & REDUCE:
-                    kinds.add("grid")
-            if kinds != {"row", "grid"}:
+            kinds, direct = self._use_kinds(out, i, V, 0)
+            # read (through cheap elementwise statements) by both a grid
+            # reduction and a row operator; or an elementwise producer whose
+            # every read is a row operator's statement (`add = scores + bias;
+            # p = softmax(add, -1)`, the FX graph's one-op-per-line form):
+            # the row region computes it instead of the region before it
+            # writing it out
+            if "other" in direct or not ({"row", "grid"} <= kinds or direct == {"row"}):
                 i += 1
                 continue
             expr = s.value
@@ -333,6 +327,39 @@ class _FunctionLowerer:
             self.owner.rematerialised.append(V)
             del out[i]
         return out
+
+    def _use_kinds(self, out: list[ast.stmt], i: int, V: str, depth: int) -> tuple[set, set]:
+        """What reads the value `V` assigned by out[i]: ({"row", "grid",
+        "other"} over its reads, followed through single-target elementwise
+        statements, {...} over its direct reads only)."""
+        kinds, direct = set(), set()
+        for j in range(i + 1, len(out)):
+            if V not in _names_read(out[j]):
+                continue
+            if not self._eligible(out[j]):
+                kinds.add("other")
+                direct.add("other")
+                continue
+            try:
+                gj, _ = self._build([out[j]])
+            except Unsupported:
+                kinds.add("other")
+                direct.add("other")
+                continue
+            oj = {n.op for n in gj.nodes}
+            k = set()
+            if oj & ROW_OPS:
+                k.add("row")
+            if oj & (REDUCE | {NZSUM, ITEM}):
+                k.add("grid")
+            direct |= k or {"elem"}
+            kinds |= k
+            W = out[j].targets[0].id
+            if not k and depth < 8 and W not in self.always_live:
+                kinds |= self._use_kinds(out, j, W, depth + 1)[0]
+            if isinstance(out[j], ast.Assign) and V in {t.id for t in out[j].targets if isinstance(t, ast.Name)}:
+                break                                       # V rebound: later reads are another value
+        return kinds, direct
 
     def _fusable(self, e: ast.expr) -> bool:
         try:

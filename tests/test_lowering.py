@@ -286,3 +286,32 @@ def f(x, w):
     exec(compile(text, "f", "exec"), ns)
     a, b = mod.f(x, w), ns["f"](x, w)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_fx_form_scores_rematerialised_and_gelu_fused():
+    """Dynamo's FX source writes one op per line (`scores = mm / 8.0`,
+    `abs_1 = scores.abs()`, `add = scores + bias`, `torch._C._nn.gelu`):
+    the scaled scores reach the predicate's reduction and the softmaxes only
+    through elementwise statements, and `add` feeds a softmax only.  Both are
+    recomputed where they are read, so the grid region writes the predicate
+    alone and the row region reads the GEMM output and the mask — neither
+    [B, H, L, L] intermediate is materialised."""
+    text = '''
+import torch
+def forward(mm, mask, h):
+    scores = mm / 8.0
+    abs_1 = scores.abs()
+    mean = abs_1.mean()
+    p = mean > 0.35
+    add = scores + mask
+    a = torch.softmax(add, dim=-1)
+    b = torch.softmax(scores, dim=-1)
+    probs = torch.where(p, a, b)
+    inter = torch._C._nn.gelu(h)
+    return probs, inter
+'''
+    low, _ = lowering.lower(text)
+    assert [r.out_names for r in low.regions] == [["p"], ["probs", "inter"]]
+    assert sorted(fv.text for fv in low.regions[1].graph.frees) == ["h", "mask", "mm", "p"]
+    assert "torch._C._nn.gelu" not in low.source
+    assert any("gelu" in {n.op for n in r.graph.nodes} for r in low.regions)
