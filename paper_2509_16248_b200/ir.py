@@ -208,7 +208,14 @@ class Builder:
         if "input" not in vals or "normalized_shape" not in vals:
             raise Unsupported("layer_norm arguments")
         ns = vals["normalized_shape"]
-        if not (isinstance(ns, (ast.Tuple, ast.List)) and len(ns.elts) == 1):
+        # `self.<ln>.normalized_shape`: written by lowering._inline_layer_norms
+        # for an nn.LayerNorm built with a one-dimensional shape
+        inlined = isinstance(ns, ast.Attribute) and ns.attr == "normalized_shape"
+        if inlined:
+            # a free value the kernel never reads (the region's eager
+            # statements, lowering.make_fallback, do read it)
+            self.free(ast.unparse(ns))
+        if not inlined and not (isinstance(ns, (ast.Tuple, ast.List)) and len(ns.elts) == 1):
             raise Unsupported("layer_norm over more than the innermost dim")
         eps = 1e-5
         if "eps" in vals:

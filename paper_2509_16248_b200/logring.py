@@ -455,6 +455,20 @@ class ModuleRuntime:
         return gemm.module_call(mod, x)
 
     @staticmethod
+    def inlined_layer_norms(owner, names: tuple) -> None:
+        """Guard of lowering._inline_layer_norms: every `self.<name>` the
+        lowering inlined as F.layer_norm must still be a plain nn.LayerNorm
+        (no forward hooks, a one-dimensional normalized_shape) — else the
+        inlined statement would not be what `self.<name>(x)` computes, so
+        raise instead of running it."""
+        for n in names:
+            m = getattr(owner, n, None)
+            if (type(m) is not torch.nn.LayerNorm or m._forward_hooks or m._forward_pre_hooks
+                    or len(m.normalized_shape) != 1):
+                raise RuntimeError(f"self.{n} was lowered as F.layer_norm (an nn.LayerNorm built in __init__), "
+                                   f"but is now a {type(m).__name__} with hooks or another shape")
+
+    @staticmethod
     def matmul(a, b):
         """`a @ b` / torch.matmul(a, b): gemm.matmul."""
         return gemm.matmul(a, b)

@@ -78,6 +78,113 @@ def _torch_aliases(tree: ast.Module) -> tuple[set[str], set[str]]:
     return torch_names or {"torch"}, functional
 
 
+def _layer_norm_attrs(cls: ast.ClassDef, torch_names: set[str], nn_names: set[str]) -> dict[str, float]:
+    """`self.X = torch.nn.LayerNorm(n[, eps=c])` at the top level of the
+    class's `__init__`, X assigned nowhere else in the class and the shape a
+    single dimension (an int, or a one-element tuple / list): {X: eps}."""
+    stores: dict[str, int] = {}
+    for node in ast.walk(cls):
+        if isinstance(node, (ast.Assign, ast.AnnAssign, ast.AugAssign, ast.Delete)):
+            targets = node.targets if isinstance(node, (ast.Assign, ast.Delete)) else [node.target]
+            for t in targets:
+                for sub in ast.walk(t):
+                    if isinstance(sub, ast.Attribute) and isinstance(sub.value, ast.Name) and sub.value.id == "self":
+                        stores[sub.attr] = stores.get(sub.attr, 0) + 1
+        if isinstance(node, ast.Call) and isinstance(node.func, ast.Name) and node.func.id in ("setattr", "delattr"):
+            return {}
+    init = next((f for f in cls.body if isinstance(f, ast.FunctionDef) and f.name == "__init__"), None)
+    if init is None:
+        return {}
+    found: dict[str, float] = {}
+    for st in init.body:
+        if not (isinstance(st, ast.Assign) and len(st.targets) == 1 and isinstance(st.targets[0], ast.Attribute)
+                and isinstance(st.targets[0].value, ast.Name) and st.targets[0].value.id == "self"
+                and isinstance(st.value, ast.Call)):
+            continue
+        chain = attr_chain(st.value.func)
+        if not (chain and chain[-1] == "LayerNorm"
+                and ((len(chain) == 3 and chain[0] in torch_names and chain[1] == "nn")
+                     or (len(chain) == 2 and chain[0] in nn_names))):
+            continue
+        c = st.value
+        if len(c.args) != 1 or isinstance(c.args[0], ast.Starred):
+            continue
+        a0 = c.args[0]
+        if isinstance(a0, (ast.Tuple, ast.List)) and len(a0.elts) != 1:
+            continue
+        eps, ok = 1e-5, True
+        for k in c.keywords:
+            v = k.value
+            if k.arg == "eps" and isinstance(v, ast.Constant) and isinstance(v.value, (int, float)) \
+                    and not isinstance(v.value, bool):
+                eps = float(v.value)
+            elif k.arg in ("elementwise_affine", "bias") and isinstance(v, ast.Constant) and v.value is True:
+                pass
+            elif k.arg not in ("device", "dtype"):
+                ok = False
+        if ok:
+            found[st.targets[0].attr] = eps
+    return {x: e for x, e in found.items() if stores.get(x) == 1}
+
+
+def _inline_layer_norms(tree: ast.Module, torch_names: set[str]) -> list[str]:
+    """`self.X(e)` with X an nn.LayerNorm the class builds in `__init__`
+    becomes `F.layer_norm(e, self.X.normalized_shape, self.X.weight,
+    self.X.bias, eps)` in the class's other methods — the form Dynamo's FX
+    graph has — so a residual add before a post-LayerNorm fuses with it into
+    one row region (`self.norm(self.out(h) + x)`: GEMM, then ONE kernel).  A
+    guard at the top of each rewritten method (ModuleRuntime.
+    inlined_layer_norms) raises if such an attribute is later replaced or
+    given hooks.  Returns the rewritten `Class.X` names."""
+    nn_names = set()
+    for node in ast.walk(tree):
+        if isinstance(node, ast.ImportFrom) and node.module == "torch":
+            nn_names |= {a.asname or a.name for a in node.names if a.name == "nn"}
+        if isinstance(node, ast.Import):
+            nn_names |= {a.asname for a in node.names if a.name == "torch.nn" and a.asname}
+    tname = "torch" if "torch" in torch_names else sorted(torch_names)[0]
+    done = []
+    for cls in [n for n in ast.walk(tree) if isinstance(n, ast.ClassDef)]:
+        attrs = _layer_norm_attrs(cls, torch_names, nn_names)
+        if not attrs:
+            continue
+
+        class _Sub(ast.NodeTransformer):
+            used: set = set()
+
+            def visit_Call(self, node):
+                self.generic_visit(node)
+                f = node.func
+                if (isinstance(f, ast.Attribute) and isinstance(f.value, ast.Name) and f.value.id == "self"
+                        and f.attr in attrs and len(node.args) == 1 and not node.keywords
+                        and not isinstance(node.args[0], ast.Starred)):
+                    self.used.add(f.attr)
+                    me = lambda a: ast.Attribute(ast.Attribute(ast.Name("self", ast.Load()), f.attr, ast.Load()),  # noqa: E731
+                                                 a, ast.Load())
+                    fn = ast.Attribute(ast.Attribute(ast.Attribute(ast.Name(tname, ast.Load()), "nn", ast.Load()),
+                                                     "functional", ast.Load()), "layer_norm", ast.Load())
+                    return ast.copy_location(ast.Call(fn, [node.args[0], me("normalized_shape"), me("weight"),
+                                                           me("bias"), ast.Constant(attrs[f.attr])], []), node)
+                return node
+
+        for fn in cls.body:
+            if not isinstance(fn, ast.FunctionDef) or fn.name == "__init__":
+                continue
+            sub = _Sub()
+            sub.used = set()
+            fn.body = [sub.visit(st) for st in fn.body]
+            if sub.used:
+                names = sorted(sub.used)
+                guard = ast.Expr(ast.Call(ast.Attribute(ast.Name(GM_RT, ast.Load()), "inlined_layer_norms",
+                                                        ast.Load()),
+                                          [ast.Name("self", ast.Load()),
+                                           ast.Tuple([ast.Constant(n) for n in names], ast.Load())], []))
+                fn.body.insert(0, ast.copy_location(guard, fn.body[0]))
+                done += [f"{cls.name}.{n}" for n in names]
+    ast.fix_missing_locations(tree)
+    return done
+
+
 def _is_capture(stmt: ast.stmt) -> str | None:
     if (
         isinstance(stmt, ast.Assign)
@@ -761,6 +868,7 @@ class _Lowerer:
         self.text = text
         self.tree = ast.parse(text)
         self.torch_names, self.functional_names = _torch_aliases(self.tree)
+        self.inlined_layer_norms = _inline_layer_norms(self.tree, self.torch_names)
         self.regions: list[Region] = []
         self.region_sources: list[str] = []
         self.sites: list[ReplaySite] = []

@@ -315,3 +315,52 @@ def forward(mm, mask, h):
     assert sorted(fv.text for fv in low.regions[1].graph.frees) == ["h", "mask", "mm", "p"]
     assert "torch._C._nn.gelu" not in low.source
     assert any("gelu" in {n.op for n in r.graph.nodes} for r in low.regions)
+
+
+LN_BLOCK = '''
+import torch
+class Block(torch.nn.Module):
+    def __init__(self, h):
+        super().__init__()
+        self.out = torch.nn.Linear(h, h)
+        self.norm = torch.nn.LayerNorm(h, eps=1e-12)
+        self.norm2d = torch.nn.LayerNorm((4, h))
+        self.swapped = torch.nn.LayerNorm(h)
+        self.swapped = torch.nn.Identity()
+    def forward(self, x):
+        y = self.norm(self.out(x) + x)
+        z = self.swapped(y) * 2
+        return z
+'''
+
+
+def test_layer_norm_modules_inlined_and_fused_with_the_residual_add():
+    """`self.norm(self.out(x) + x)` with `self.norm = nn.LayerNorm(h, eps)`
+    built once in __init__: the call becomes F.layer_norm with the module's
+    parameters (Dynamo's FX form), so the residual add and the LayerNorm are
+    ONE row region after the GEMM.  Attributes assigned twice, or with a
+    multi-dimensional shape, stay module calls."""
+    low, lw = lowering.lower(LN_BLOCK)
+    assert lw.inlined_layer_norms == ["Block.norm"]
+    assert "inlined_layer_norms(self, ('norm',))" in low.source
+    r = low.regions[0]
+    assert r.out_names == ["y"]
+    assert "layer_norm" in {n.op for n in r.graph.nodes} and "add" in {n.op for n in r.graph.nodes}
+    assert "__gm_rt__.call(self.swapped" in low.source
+
+
+def test_inlined_layer_norm_runs_and_guards_on_cpu():
+    """Eager (allow_eager, CPU) the inlined statement computes what the
+    module computes, bit for bit; a hook added to the module later makes the
+    forward raise instead of silently skipping it."""
+    mod, low = lowering.load(LN_BLOCK, allow_eager=True)
+    torch.manual_seed(0)
+    blk = mod.Block(16)
+    x = torch.randn(3, 5, 16)
+    with torch.no_grad():
+        y = blk(x)
+        ref = blk.swapped(blk.norm(blk.out(x) + x)) * 2
+    assert torch.equal(y, ref)
+    blk.norm.register_forward_hook(lambda m, i, o: o)
+    with pytest.raises(RuntimeError, match="lowered as F.layer_norm"):
+        blk(x)
