@@ -58,15 +58,24 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
     executor = B200Executor(forward, dev)
     stats = {"graph_calls": 0, "autograd_calls": 0}
 
+    tree_map = torch.utils._pytree.tree_map
+
     def run(*args):
-        if torch.is_grad_enabled() and any(torch.is_tensor(a) and a.requires_grad for a in args):
-            stats["autograd_calls"] += 1
-            return gm(*args)
-        stats["graph_calls"] += 1
-        with torch.no_grad():
+        if torch.is_grad_enabled():
+            if any(torch.is_tensor(a) and a.requires_grad for a in args):
+                stats["autograd_calls"] += 1
+                return gm(*args)
+            with torch.no_grad():
+                out = executor(*args)
+        else:
             out = executor(*args)
+        stats["graph_calls"] += 1
         if not static_outputs:
-            out = torch.utils._pytree.tree_map(lambda t: t.clone() if torch.is_tensor(t) else t, out)
+            # Dynamo graphs return a tuple of tensors: clone those directly
+            if type(out) is tuple and all(type(t) is torch.Tensor for t in out):
+                out = tuple(t.clone() for t in out)
+            else:
+                out = tree_map(lambda t: t.clone() if torch.is_tensor(t) else t, out)
         executor.flush()
         return out
 
