@@ -303,6 +303,7 @@ class LogRing:
             step, tmpl = self.pending[0]
             raw = None
             if tmpl.template_id is not None:
+                t_spin = None
                 while True:
                     if not self.arrived:
                         self._poll()
@@ -311,7 +312,14 @@ class LogRing:
                         break
                     if not block:
                         return False
-                    time.sleep(20e-6)
+                    # spin on the mapped commit word for the first 2 ms: a
+                    # sleep rounds up to the kernel's timer slack (~50-80 us),
+                    # longer than most forwards this waits on
+                    now = time.perf_counter()
+                    if t_spin is None:
+                        t_spin = now
+                    if now - t_spin > 2e-3:
+                        time.sleep(20e-6)
             self.pending.popleft()
             if raw is not None:
                 self.drained_gather_steps += 1

@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
 
-    from bench import WORKLOADS, _inputs, _time_kernel_flushed
+    from bench import WORKLOADS, _all_inputs, _time_kernel_flushed
     from paper_2509_16248_b200 import compile_program
     from paper_2509_16248_b200 import region as reg
     from paper_2509_16248_b200.harness import programs
@@ -35,7 +35,7 @@ def main():
     a = ap.parse_args()
     dtype = {"bf16": torch.bfloat16, "fp32": torch.float32}[a.dtype]
     prog = programs()[a.workload]
-    x = [t.cuda() for t in _inputs(prog, WORKLOADS[a.workload][1], dtype)]
+    x = [t.cuda() for t in _all_inputs(prog, WORKLOADS[a.workload][1], dtype)[0]]
     ex, mod, low = compile_program(prog["transformed"], prog["callable"], dtype=dtype)
     ex(*x)
     ex.flush()

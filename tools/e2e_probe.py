@@ -9,12 +9,12 @@ import time
 import torch
 
 sys.path.insert(0, '/root/repo')
-from bench import _copy_only_pipeline, _inputs  # noqa: E402
+from bench import _copy_only_pipeline, _all_inputs  # noqa: E402
 from paper_2509_16248_b200 import compile_program  # noqa: E402
 from paper_2509_16248_b200.harness import programs  # noqa: E402
 
 prog = programs()['bigbird_like']
-x_host = [t.pin_memory() for t in _inputs(prog, None, torch.bfloat16)]
+x_host = [t.pin_memory() for t in _all_inputs(prog, None, torch.bfloat16)[0]]
 ex, mod, low = compile_program(prog['transformed'], prog['callable'], dtype=torch.bfloat16)
 out0 = ex(*x_host)
 ex.flush()

@@ -74,6 +74,18 @@ def main():
                 res["backend_executor_flush_us"] = p50(lambda: (ex2(*args), ex2.flush()))
                 res["executor_only_us"] = p50(lambda: ex2(*args))
                 res["gm_compile_us"] = p50(lambda: c(*x))
+                # Dynamo's own per-call floor: the same program and guards,
+                # a backend that returns precomputed outputs without any work
+                outs = run(*args)
+
+                def noop_backend(gm, example_inputs):
+                    return lambda *a: outs
+
+                torch._dynamo.reset()
+                c0 = torch.compile(fn, backend=noop_backend)
+                c0(*x)
+                res["dynamo_noop_backend_us"] = p50(lambda: c0(*x))
+                res["sync_only_us"] = p50(lambda: None)
             print(json.dumps(res), flush=True)
 
 
