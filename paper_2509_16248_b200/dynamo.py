@@ -21,15 +21,18 @@ from __future__ import annotations
 
 import ast
 import functools
+import gc
+import os
 import textwrap
 
 import torch
 
 from .executor import B200Executor
 from .lowering import load
-from .region import RegionUnsupported
+from .region import RegionUnsupported, check_status
 
 _PRELUDE = "import math\nimport operator\nimport torch\n\n"
+OUTPUT_SLOTS = 2   # captured copies whose outputs are handed out without a copy (GM_OUTPUT_SLOTS)
 
 
 def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool = False,
@@ -37,10 +40,13 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
     """Dynamo backend: lower the FX graph's source into fused regions and run
     it as one CUDA graph per input signature.
 
-    torch.compile semantics are kept: every call returns fresh tensors (the
-    graph's static outputs are cloned unless `static_outputs=True`, the
-    make_graphed_callables contract), and a call that needs autograd (grad
-    mode on and an input requiring grad) runs the FX graph itself, so
+    torch.compile semantics are kept.  Every call returns tensors no later
+    call overwrites: the outputs of one of OUTPUT_SLOTS captured copies that
+    nothing the caller holds still references (checked before the replay,
+    by storage use count), else copies (`static_outputs=True` returns the
+    graph's static outputs, the make_graphed_callables contract).  A call
+    that needs autograd (grad mode on and an input requiring grad) runs the
+    FX graph itself, so
     gradients flow — the fused kernels are inference-only.  CPU inputs raise
     unless `allow_eager` (then the lowered statements run eagerly with
     PyTorch, bit-identical to the graph): there is no silent CPU path.
@@ -58,7 +64,28 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
     executor = B200Executor(forward, dev)
     stats = {"graph_calls": 0, "autograd_calls": 0}
 
-    tree_map = torch.utils._pytree.tree_map
+    tree_flatten = torch.utils._pytree.tree_flatten
+    use_count = torch._C._storage_Use_Count
+    n_slots = int(os.environ.get("GM_OUTPUT_SLOTS", OUTPUT_SLOTS))
+    held: dict[int, list] = {}   # id(slot entry) -> [(static output, storage use count with no alias out)]
+    stats["aliased"] = stats["cloned"] = 0
+
+    def slot_entry(args):
+        """The first output slot (a captured copy of this signature's entry)
+        none of whose outputs, nor views of them, the caller still holds —
+        storage use counts back at the entry's own, checked BEFORE the replay
+        that would overwrite them (the test cudagraph trees use) — or None
+        when every slot is held."""
+        for s in range(1, n_slots + 1):
+            e = executor.prepare(*args, slot=s)
+            h = held.get(id(e))
+            if h is None:
+                gc.collect()   # the capture's reference cycles: steady baseline counts
+                leaves = tree_flatten(e.outputs)[0] if e.graph is not None else []
+                h = held[id(e)] = [(t, use_count(t.untyped_storage()._cdata)) for t in leaves if torch.is_tensor(t)]
+            if all(use_count(t.untyped_storage()._cdata) == n for t, n in h):
+                return e
+        return None
 
     def run(*args):
         if torch.is_grad_enabled():
@@ -66,16 +93,24 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
                 stats["autograd_calls"] += 1
                 return gm(*args)
             with torch.no_grad():
-                out = executor(*args)
-        else:
-            out = executor(*args)
+                return run(*args)
         stats["graph_calls"] += 1
-        if not static_outputs:
-            # Dynamo graphs return a tuple of tensors: clone those directly
-            if type(out) is tuple and all(type(t) is torch.Tensor for t in out):
-                out = tuple(t.clone() for t in out)
+        if static_outputs:
+            out = executor(*args)
+        else:
+            check_status()
+            e = slot_entry(args)
+            if e is not None:
+                e.load(args)
+                stats["aliased"] += 1
+                # aliases (new tensor objects on the static storage): while
+                # the caller keeps one, or a view of one, the slot is held
+                out = _map_tensors(torch.Tensor.detach, e.run())
             else:
-                out = tree_map(lambda t: t.clone() if torch.is_tensor(t) else t, out)
+                # every slot's outputs are still held: replay the scratch
+                # entry (slot 0) and hand out copies
+                stats["cloned"] += 1
+                out = _map_tensors(torch.Tensor.clone, executor(*args))
         executor.flush()
         return out
 
@@ -83,6 +118,16 @@ def gm_b200_backend(gm: torch.fx.GraphModule, example_inputs, allow_eager: bool 
     run.lowered = lowered
     run.stats = stats
     return run
+
+
+def _map_tensors(fn, out):
+    """fn over the tensors of an output structure (Dynamo graphs return a
+    tuple of tensors: mapped without pytree)."""
+    if type(out) is tuple:
+        return tuple(fn(t) if isinstance(t, torch.Tensor) else t for t in out)
+    if isinstance(out, torch.Tensor):
+        return fn(out)
+    return torch.utils._pytree.tree_map(lambda t: fn(t) if isinstance(t, torch.Tensor) else t, out)
 
 
 def _fx_source(gm: torch.fx.GraphModule) -> str:

@@ -106,7 +106,7 @@ class EntryInfo:
 
 
 class _Entry:
-    def __init__(self, ex: "B200Executor", args: list, bound: bool = False):
+    def __init__(self, ex: "B200Executor", args: list, bound: bool = False, own_pool: bool = False):
         self.ex = ex
         dev = ex.device
         t0 = time.perf_counter()
@@ -146,7 +146,12 @@ class _Entry:
         if ex.use_graphs and syncs == 0 and not side_effects:
             g = torch.cuda.CUDAGraph()
             try:
-                with torch.cuda.graph(g, pool=ex.pool), _watch_side_effects(), scratch_owner(self):
+                # slot entries (double-buffered pipelines, the Dynamo backend's
+                # output slots) replay out of capture order, so each keeps its
+                # own pool: no slot's intermediates can land on another
+                # slot's live outputs
+                pool = torch.cuda.graph_pool_handle() if own_pool else ex.pool
+                with torch.cuda.graph(g, pool=pool), _watch_side_effects(), scratch_owner(self):
                     with logring.step(dev, discard=False) as st:
                         self.outputs = ex.fn(*self.static)
                 self.template = st.template
@@ -205,7 +210,7 @@ class B200Executor:
         e = self.entries.get(key)
         if e is None:
             with torch.cuda.device(self.device):
-                e = _Entry(self, list(args))
+                e = _Entry(self, list(args), own_pool=slot != 0)
             self.entries[key] = e
         return e
 
@@ -228,6 +233,15 @@ class B200Executor:
     def __call__(self, *args):
         check_status()  # a grid-barrier timeout of an earlier launch raises here (no sync)
         e = self.prepare(*args)
+        e.load(args)
+        return e.run()
+
+    def call_slot(self, slot: int, *args):
+        """__call__ on output slot `slot`: an independent captured copy of
+        the entry (own static buffers, graph and pool), so the outputs of
+        one slot survive replays of the others."""
+        check_status()
+        e = self.prepare(*args, slot=slot)
         e.load(args)
         return e.run()
 

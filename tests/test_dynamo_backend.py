@@ -114,6 +114,50 @@ def test_backend_returns_fresh_outputs_and_keeps_autograd():
     assert torch.equal(x.grad, torch.full((1024,), 2.0, device="cuda"))
 
 
+@pytest.mark.gpu
+def test_backend_output_slots_follow_what_the_caller_holds():
+    """Outputs are handed out without a copy from an output slot nothing the
+    caller holds still references (the alias object or any view of it);
+    when every slot is held the call copies.  Held outputs never change."""
+    from paper_2509_16248_b200 import dynamo
+
+    torch._dynamo.reset()
+    runs = []
+
+    def backend(gm, ex):
+        r = dynamo.gm_b200_backend(gm, ex)
+        runs.append(r)
+        return r
+
+    def f(x):
+        __gm_pred_0 = x.sum() > 0
+        y = torch.where(__gm_pred_0, x * 2, x - 1)
+        return y
+
+    c = torch.compile(f, backend=backend)
+    a = torch.ones(1024, device="cuda")
+    two, minus2 = torch.full((1024,), 2.0, device="cuda"), torch.full((1024,), -2.0, device="cuda")
+    with torch.no_grad():
+        for _ in range(4):
+            c(a)                       # dropped at once: slot 1 every time, no copy
+        st = runs[0].stats
+        assert st["cloned"] == 0 and st["aliased"] >= 4, st
+        y1 = c(a)
+        tail = y1[512:]                # a view keeps slot 1 held
+        del y1
+        y2 = c(-a)                     # slot 2
+        y3 = c(a)                      # both held: a copy
+        assert st["cloned"] == 1, st
+        assert torch.equal(tail, two[512:]) and torch.equal(y2, minus2) and torch.equal(y3, two)
+        y4 = c(-a)
+        assert torch.equal(y3, two) and torch.equal(y4, minus2) and torch.equal(tail, two[512:])
+        del tail, y2, y3, y4
+        n = st["cloned"]
+        for _ in range(3):
+            assert torch.equal(c(a), two)
+        assert st["cloned"] == n
+
+
 @pytest.mark.parametrize("name", ["longformer_like", "moe_minicpm_like"])
 def test_gm_compile_keeps_residual_breaks_in_one_graph(programs, name):
     """gm_compile traces `.item()` and dynamic-shape ops into the FX graph

@@ -8,6 +8,7 @@ host-timed p50 of each layer with a synchronize after every call.
   backend, no clone the same with static outputs
   gm_compile        the full front door (Dynamo guards + backend)
 """
+import functools
 import json
 import os
 import statistics
@@ -74,6 +75,17 @@ def main():
                 res["backend_executor_flush_us"] = p50(lambda: (ex2(*args), ex2.flush()))
                 res["executor_only_us"] = p50(lambda: ex2(*args))
                 res["gm_compile_us"] = p50(lambda: c(*x))
+                for tag, env in (("gm_compile_clone_us", "0"), ("gm_compile_slots_us", "2")):
+                    os.environ["GM_OUTPUT_SLOTS"] = env
+                    torch._dynamo.reset()
+                    cc = torch.compile(fn, backend="gm_b200")
+                    cc(*x)
+                    res[tag] = p50(lambda: cc(*x))
+                os.environ.pop("GM_OUTPUT_SLOTS")
+                torch._dynamo.reset()
+                cs = torch.compile(fn, backend=functools.partial(dynamo.gm_b200_backend, static_outputs=True))
+                cs(*x)
+                res["gm_compile_static_us"] = p50(lambda: cs(*x))
                 # Dynamo's own per-call floor: the same program and guards,
                 # a backend that returns precomputed outputs without any work
                 outs = run(*args)
