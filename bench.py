@@ -563,7 +563,11 @@ def main():
                     "traffic": _ncu_traffic(dom["name"].split(" ")[0]), "kernel": dom["name"],
                     "bytes_alg": dom["bytes"], "kernel_ms": dom["ms"],
                     "peak_kind": peak_kind, "share_of_step": dom["ms"] / statistics.mean(step_ms),
-                    "traffic_how": "ncu dram__bytes_read+write per launch from the committed profiles/ capture"}
+                    "traffic_how": "ncu dram__bytes_read+write per launch from the committed profiles/ capture",
+                    # also against north_star's nominal 8 TB/s
+                    "frac_nominal_8tbs": achieved / 8000.0,
+                    "fused_kernels_frac": {k["name"].split(" ")[0]: round(k["bytes"] / (k["ms"] / 1e3) / 1e9 / peak, 3)
+                                           for k in kernels if k["ms"] == k["ms"] and k["ms"] > 0}}
 
     # ---- end to end through the public API, host buffers in and out:
     # (a) single call latency: executor(*pinned host inputs) -> D2H into a

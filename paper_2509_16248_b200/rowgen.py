@@ -62,7 +62,7 @@ def _bcast_to(a: tuple, target: tuple) -> bool:
         return False
 UMAX = 4                  # vectors per thread (registers: U x 8 floats per live node)
 MAX_TPR = 1024
-CTA_THREADS = 256
+CTA_THREADS = 128        # threads per row-kernel CTA (GM_ROW_CTA; 128 vs 256: softmax bf16 62.6 -> 59.6 us, fp32 neutral)
 
 
 def has_row_ops(outputs: list[Node]) -> bool:
@@ -180,10 +180,18 @@ class RowPlan(Plan):
             tpr *= 2
         if -(-nv_row // tpr) > UMAX:
             raise Unsupported(f"row of {self.C} elements exceeds the on-chip row ({MAX_TPR * UMAX * 8})")
+        want_u = int(os.environ.get("GM_ROW_U", "0"))
+        if want_u and self.vec8 and nv_row % want_u == 0:
+            # a whole number of warps per row (any multiple of 32, combined
+            # through shared memory) holding want_u full vectors per thread
+            t = nv_row // want_u
+            if (t % 32 == 0 and t <= MAX_TPR) or (t <= 32 and t & (t - 1) == 0):
+                tpr = t
         self.TPR = tpr
         self.U = -(-nv_row // tpr)
         self.full_vecs = self.vec8 and nv_row % tpr == 0
-        self.threads = max(CTA_THREADS, tpr)
+        cta = int(os.environ.get("GM_ROW_CTA", CTA_THREADS))
+        self.threads = max(cta // tpr, 1) * tpr
         self.RPC = self.threads // tpr
         self.grid = -(-self.R // self.RPC)
         if self.grid >= 2 ** 31:
@@ -305,8 +313,15 @@ class RowPlan(Plan):
             if (s.op == "free" and s.kind == "host") or (s.kind == "dscalar" and s.dtype == torch.bfloat16):
                 w(f"  const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
         w(f"  const int tr_ = threadIdx.x % {TPR};")
-        w(f"  const i64 row_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
-        w(f"  const bool rok_ = row_ < {self.R}ll;")
+        if os.environ.get("GM_ROW_REVERSE"):
+            # last rows first: the tail of an input the previous kernel
+            # swept in address order is still in L2 when the first CTAs run
+            w(f"  const i64 ri_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
+            w(f"  const bool rok_ = ri_ < {self.R}ll;")
+            w(f"  const i64 row_ = rok_ ? {self.R - 1}ll - ri_ : 0ll;")
+        else:
+            w(f"  const i64 row_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
+            w(f"  const bool rok_ = row_ < {self.R}ll;")
         w(f"  const i64 rb_ = row_ * {self.C}ll;")
         w("  (void)tr_; (void)rok_;")
         for u in range(U):

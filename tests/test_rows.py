@@ -59,7 +59,7 @@ def test_softmax_arm_splits_into_grid_then_row_region():
     assert has_row_ops(low.regions[1].out_nodes) and low.regions[1].out_names == ["y"]
     row = plans[1]
     assert isinstance(row, RowPlan)
-    assert (row.R, row.C, row.TPR, row.U, row.RPC, row.grid) == (8192, 768, 32, 3, 8, 1024)
+    assert (row.R, row.C, row.TPR, row.U, row.RPC, row.grid) == (8192, 768, 32, 3, 4, 2048)
     assert row.vec8
     # the untaken arm is skipped by a uniform branch on the predicate
     assert "if (sb" in row.source
