@@ -6,7 +6,7 @@
 # fused kernels.
 set -x
 R=${ROUND:-r02}
-timeout 2700 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${R}_gputests.log 2>&1
+timeout 2700 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > gpurun_out/${R}_gputests.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${R}_smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/${R}_bench_ref.json 2> gpurun_out/${R}_bench_ref.err
@@ -24,3 +24,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'gm_(region|row)_' -s 4 -c 4 -o gpurun_out/${R}_prof python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compile > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/${R}_prof.ncu-rep gpurun_out/${R}_ncu_regions.json
 ls -la gpurun_out
+timeout 900 python tools/frontdoor_overhead.py blenderbot_like pegasus_like phi4_like bigbird_layer > gpurun_out/${R}_frontdoor_overhead.jsonl 2>/dev/null
+ROUND=$R bash tools/ncu_all_workloads.sh > gpurun_out/${R}_ncu_all.log 2>&1
+ls gpurun_out

@@ -5,7 +5,7 @@
 # misprediction) and captures the next 8.
 set -x
 ROUND=${ROUND:-r02}
-WORKLOADS=${WORKLOADS:-"longformer_like phi4_like qwen_audio_like biogpt_like blenderbot_like flan_t5_like pegasus_like moe_minicpm_like bart_step bigbird_like bigbird_attn gemm_arms"}
+WORKLOADS=${WORKLOADS:-"bigbird_layer longformer_like phi4_like qwen_audio_like biogpt_like blenderbot_like flan_t5_like pegasus_like moe_minicpm_like bart_step bigbird_like bigbird_attn gemm_arms"}
 mkdir -p gpurun_out
 for w in $WORKLOADS; do
   for d in bf16 fp32; do
