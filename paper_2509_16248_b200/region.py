@@ -250,6 +250,9 @@ class _Spec:
         threads = plan.threads
         grid, smem = plan.grid, plan.smem_bytes
         vpc = plan.K
+        if getattr(plan, "persist", False):
+            # a persistent row kernel loops over its row groups: one wave
+            grid = max(1, min(grid, self.kernel.occupancy(threads, smem) * sms))
         if plan.reductions and grid > 1:
             # the grid barrier needs every CTA resident at once
             occ = self.kernel.occupancy(threads, smem)

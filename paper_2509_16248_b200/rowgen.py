@@ -197,6 +197,9 @@ class RowPlan(Plan):
         if self.grid >= 2 ** 31:
             raise Unsupported("too many rows")
         self.K = self.U
+        # persistent CTAs looping over row groups (GM_ROW_PERSIST=1); the
+        # launch clamps the grid to the co-resident CTAs
+        self.persist = bool(int(os.environ.get("GM_ROW_PERSIST", "0")))
         self.smem_bytes = 0
         self.smem_off = {}
         self.minb = 1
@@ -313,14 +316,32 @@ class RowPlan(Plan):
             if (s.op == "free" and s.kind == "host") or (s.kind == "dscalar" and s.dtype == torch.bfloat16):
                 w(f"  const u32 spk{s.uid} = gm::f2bf2(sf{s.uid}, sf{s.uid}); (void)spk{s.uid};")
         w(f"  const int tr_ = threadIdx.x % {TPR};")
+        if self.persist:
+            # persistent: each CTA walks row groups g_ = blockIdx.x + k·gridDim.x
+            # (grid = the co-resident CTAs, region._Spec), and asks L2 for
+            # its next group's rows before working on this one
+            ng = self.grid
+            w(f"  for (i64 g_ = blockIdx.x; g_ < {ng}ll; g_ += gridDim.x) {{")
+            w(f"  {{ const i64 rn_ = (g_ + gridDim.x) * {self.RPC} + threadIdx.x / {TPR};")
+            w(f"    if (rn_ < {self.R}ll) {{")
+            for ip in self.inputs:
+                if ip.mode == MODE_FULL and ip.node.kind == "elem" and not os.environ.get("GM_ROW_NOPF"):
+                    es = torch.empty((), dtype=ip.dtype).element_size()
+                    for u in range(U):
+                        w(f"      asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"((const char*)P.in[{ip.slot}].ptr + "
+                          f"(rn_ * {self.C}ll + ((i64){u} * {TPR} + tr_) * GM_VEC) * {es}ll));")
+            w("  } }")
+            blk = "g_"
+        else:
+            blk = "(i64)blockIdx.x"
         if os.environ.get("GM_ROW_REVERSE"):
             # last rows first: the tail of an input the previous kernel
             # swept in address order is still in L2 when the first CTAs run
-            w(f"  const i64 ri_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
+            w(f"  const i64 ri_ = {blk} * {self.RPC} + threadIdx.x / {TPR};")
             w(f"  const bool rok_ = ri_ < {self.R}ll;")
             w(f"  const i64 row_ = rok_ ? {self.R - 1}ll - ri_ : 0ll;")
         else:
-            w(f"  const i64 row_ = (i64)blockIdx.x * {self.RPC} + threadIdx.x / {TPR};")
+            w(f"  const i64 row_ = {blk} * {self.RPC} + threadIdx.x / {TPR};")
             w(f"  const bool rok_ = row_ < {self.R}ll;")
         w(f"  const i64 rb_ = row_ * {self.C}ll;")
         w("  (void)tr_; (void)rok_;")
@@ -420,6 +441,8 @@ class RowPlan(Plan):
                 fn = "store8" if self.vec8 else "store8_elems"
                 for u in range(U):
                     w(f"  if (nv{u}) gm::{fn}<{dt}>(P.out[{k}], e{u}, nv{u}, n{o.uid}_{u});")
+        if self.persist:
+            w("  }  // row groups")
         # scalar outputs and the scalar mirror (CTA 0)
         w("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
         for j, o in enumerate(self.outputs):

@@ -215,3 +215,19 @@ def f(x, b):
     assert not is_mixed(mg, mouts, ext)
     p = codegen.Plan(mg, mouts, ext, allow_cpu=True)
     assert len(nat.compile_cubin(p.source, (10, 0))) > 0
+
+
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_persistent_row_kernels_compile(monkeypatch, persist):
+    """Row kernels as persistent CTAs walking row groups, with an L2
+    prefetch of each CTA's next group (GM_ROW_PERSIST=1), compile for
+    sm_100a; the loop uses gridDim.x, so any clamped grid covers all rows."""
+    monkeypatch.setenv("GM_ROW_PERSIST", persist)
+    shapes = {"x": (64, 1024), "b": (1024,), "m": (64, 1)}
+    for dt in (torch.float32, torch.bfloat16):
+        _, plans = _region_plans(ROWS, shapes, dt)
+        row = [p for p in plans if isinstance(p, RowPlan)][0]
+        assert row.persist == (persist == "1")
+        assert ("for (i64 g_ = blockIdx.x;" in row.source) == row.persist
+        assert ("prefetch.global.L2" in row.source) == row.persist
+        assert len(nat.compile_cubin(row.source, (10, 0))) > 0
