@@ -345,6 +345,9 @@ class Plan:
                     mode = self._mode(t)
                 self.inputs.append(InputPlan(node.value, node, mode, t.dtype, len(self.inputs),
                                              passes=used_passes.get(node.uid, set())))
+        # periods of the periodic inputs, fixed per specialisation (the
+        # kernel divides by a constant)
+        self._periods = {ip.slot: args[ip.free_index].numel() for ip in self.inputs if ip.mode == MODE_PERIODIC}
         if len(self.inputs) > nat.MAX_IN:
             raise Unsupported("too many tensor inputs")
         elem_out = [o for o in self.outputs if o.kind == "elem" and o.op != "free"]
@@ -500,6 +503,9 @@ class Plan:
                 pre, raw = self._raw_for(ip, u)
                 return pre + [f"gm::rcvt<{dt}>({raw}, n{node.uid}_{u});"]
             if ip.mode == MODE_PERIODIC:
+                per = getattr(self, "_periods", {}).get(k)
+                if per and not os.environ.get("GM_PERIODIC_RUNTIME"):
+                    return [f"gm::load8_periodic_c<{dt}, {per}ll>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
                 return [f"gm::load8_periodic<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]
             if ip.mode == MODE_STRIDED:
                 return [f"gm::load8_strided<{dt}>(P.in[{k}], e{u}, nv{u}, n{node.uid}_{u});"]

@@ -635,6 +635,19 @@ __device__ __forceinline__ void load8_periodic(const InDesc& d, i64 e, int nv, f
   }
 }
 
+// Same with the period known at specialisation: `e % PER` by a constant is
+// a multiply-high sequence instead of a 64-bit division routine per vector.
+template <int DT, long long PER>
+__device__ __forceinline__ void load8_periodic_c(const InDesc& d, i64 e, int nv, float (&x)[8]) {
+  typedef Elem<DT> E;
+  if ((PER % GM_VEC) == 0 && nv == GM_VEC) {
+    E::ldg8((const char*)d.ptr + (e % PER) * E::ES, x);
+  } else {
+#pragma unroll
+    for (int k = 0; k < GM_VEC; ++k) x[k] = (k < nv) ? E::ld((const void*)d.ptr, (e + k) % PER) : 0.f;
+  }
+}
+
 template <int DT>
 __device__ __forceinline__ float load_scalar(const InDesc& d) {
   return Elem<DT>::ld((const void*)d.ptr, 0);
