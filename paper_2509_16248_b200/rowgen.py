@@ -297,6 +297,34 @@ class RowPlan(Plan):
         w(f"  __shared__ double s_rw[{max(1, self.threads // 32)}];")
         w("  (void)s_rw;")
         w('  asm volatile("griddepcontrol.wait;" ::: "memory");')
+        # LayerNorm weight / bias ([C] inputs read once per row after the row
+        # statistics): one cp.async copy into shared memory per CTA at kernel
+        # start, in flight together with the rows' own loads, read back from
+        # shared memory after the statistics — no second global round trip
+        # on each row's critical path, no registers held across it
+        self._smem_wb = {}
+        if self.full_vecs and not os.environ.get("GM_ROW_NO_SMEM_WB"):
+            per = {ip.node.uid: ip for ip in self.inputs if ip.mode == MODE_PERIODIC and ip.node.kind == "elem"
+                   and self._periods.get(ip.slot) == self.C}
+            users: dict = {}
+            for n in self.order:
+                for j, a in enumerate(n.args):
+                    if a.uid in per:
+                        users.setdefault(a.uid, []).append((n.op, j))
+            total = 0
+            for uid, us in users.items():
+                ip = per[uid]
+                nb = self.C * torch.empty((), dtype=ip.dtype).element_size()
+                if all(op == "layer_norm" and j in (1, 2) for op, j in us) and nb % 16 == 0 and total + nb <= 32768:
+                    self._smem_wb[uid] = ip
+                    total += nb
+            for uid, ip in self._smem_wb.items():
+                nb = self.C * torch.empty((), dtype=ip.dtype).element_size()
+                w(f"  __shared__ __align__(16) unsigned char swb{ip.slot}[{nb}];")
+                w(f"  for (int i = threadIdx.x; i < {nb // 16}; i += {self.threads}) "
+                  f"gm::cp_async16(gm::smem_u32(swb{ip.slot} + 16 * i), (const char*)P.in[{ip.slot}].ptr + 16 * i);")
+            if self._smem_wb:
+                w("  gm::cp_async_commit();")
         # live timer (diagnostics word bit 29, bench.py's timed loop): CTA 0
         # stamps the start, every CTA counts its exit (gm::live_exit) — the
         # kernel's own duration inside the forward's graph, no event nodes
@@ -653,9 +681,21 @@ class RowPlan(Plan):
               f"{float(n.value[2])!r}f)));")
             w(f"  const float bia{n.uid} = gm::mul(-rstd{n.uid}, mu{n.uid});")
             late = getattr(self, "_late", {})
+            staged = [a for a in (wt, bs) if a.uid in late and a.uid in self._smem_wb]
+            if staged:
+                w("  gm::cp_async_wait_all();")
+                w("  __syncthreads();")
             for a in (wt, bs):
                 if a.uid in late:
-                    self._emit_node(w, late.pop(a.uid))
+                    if a.uid in self._smem_wb:
+                        late.pop(a.uid)
+                        ip = self._smem_wb[a.uid]
+                        dt, es = DT_CODE[ip.dtype], torch.empty((), dtype=ip.dtype).element_size()
+                        for u in range(U):
+                            w(f"  gm::Raw<{dt}> rl{ip.slot}_{u} = *(const gm::Raw<{dt}>*)(swb{ip.slot} + c{u} * {es});")
+                            w(f"  gm::rcvt<{dt}>(rl{ip.slot}_{u}, n{a.uid}_{u});")
+                    else:
+                        self._emit_node(w, late.pop(a.uid))
             for u in range(U):
                 wv = self._ev(wt, "l", u) if wt.kind == "elem" else self._sf(wt)
                 bv = self._ev(bs, "l", u) if bs.kind == "elem" else self._sf(bs)
