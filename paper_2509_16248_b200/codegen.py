@@ -59,7 +59,11 @@ MODE_FULL, MODE_PERIODIC, MODE_STRIDED, MODE_SCALAR = "full", "periodic", "strid
 STATIC_SMEM_RESERVE = 8 * 1024
 SMEM_PER_SM = 233472    # B200: 228 KB of shared memory per SM (shared by its resident CTAs)
 B200_DEVICE = (148, 232448)  # SMs, opt-in dynamic shared memory per block
-DATA_REGS = int(os.environ.get("GM_DATA_REGS", "40"))  # raw-vector registers per thread: register stage + one block's loads
+DATA_REGS = 40  # raw-vector registers per thread: register stage + one block's loads (GM_DATA_REGS)
+
+
+def _data_regs() -> int:
+    return int(os.environ.get("GM_DATA_REGS", DATA_REGS))
 VEC_REGS = {torch.float32: 8, torch.bfloat16: 4, torch.float16: 4, torch.bool: 2}
 MAX_DECISIONS = 24      # predicted decisions per speculative region (scratch ints at barrier + 288)
 # adaptive speculation: speculate once the confidence counter reaches
@@ -1150,7 +1154,7 @@ class Plan:
             live = sum(self.K * VEC_REGS[ip.dtype] for ip in staged)
             for p in range(self.npass):
                 tmp = sum(VEC_REGS[ip.dtype] for ip in self._preload_inputs(p) if ip not in staged)
-                if live + self.K * tmp > DATA_REGS:
+                if live + self.K * tmp > _data_regs():
                     return False
             return True
 
@@ -1533,7 +1537,7 @@ class Plan:
             if any(st == "reg" for st in self.stage.values()):
                 kb = self.K                      # register staging: one block by construction
             else:
-                kb = self.K if self.K * tmp <= DATA_REGS else max(1, DATA_REGS // max(1, tmp))
+                kb = self.K if self.K * tmp <= _data_regs() else max(1, _data_regs() // max(1, tmp))
                 nblk = -(-self.K // kb)
                 kb = -(-self.K // nblk)
             pref = None
