@@ -231,3 +231,27 @@ def test_persistent_row_kernels_compile(monkeypatch, persist):
         assert ("for (i64 g_ = blockIdx.x;" in row.source) == row.persist
         assert ("prefetch.global.L2" in row.source) == row.persist
         assert len(nat.compile_cubin(row.source, (10, 0))) > 0
+
+
+def test_layer_norm_weights_staged_in_shared_memory(monkeypatch):
+    """LayerNorm's [C] weight and bias are copied into shared memory by
+    cp.async at kernel start and read back after the row statistics; a
+    [C] input another operator reads stays a global load; the opt-out
+    (GM_ROW_NO_SMEM_WB) restores global loads.  Both forms compile."""
+    text = '''
+import torch
+def f(x, r, w, b, s):
+    y = torch.nn.functional.layer_norm(x + r, (768,), w, b, 1e-12) * s
+    return y
+'''
+    shapes = {"x": (64, 768), "r": (64, 768), "w": (768,), "b": (768,), "s": (768,)}
+    for opt_out in (False, True):
+        if opt_out:
+            monkeypatch.setenv("GM_ROW_NO_SMEM_WB", "1")
+        for dt in (torch.float32, torch.bfloat16):
+            _, plans = _region_plans(text, shapes, dt)
+            row = [p for p in plans if isinstance(p, RowPlan)][0]
+            src = row.source
+            assert ("cp_async16" in src) != opt_out
+            assert src.count("__shared__ __align__(16) unsigned char swb") == (0 if opt_out else 2)
+            assert len(nat.compile_cubin(src, (10, 0))) > 0
