@@ -595,6 +595,11 @@ class Plan:
                 "gelu": f"gm::gelu({x})", "gelu_tanh": f"gm::gelu_tanh({x})", "erf": f"erff({x})",
                 "square": f"gm::mul({x}, {x})", "reciprocal": f"gm::recip({x})",
             }
+            if op == "gelu" and node.dtype in (torch.bfloat16, torch.float16) and not os.environ.get("GM_ACCURATE_GELU16"):
+                # 16-bit outputs: erf from an erfc fit with relative error
+                # < 1.2e-7 on the SFU (gm::gelu16); the accurate erff made
+                # the bf16 GELU region ALU-bound
+                un["gelu"] = f"gm::gelu16({x})"
             if op not in un:
                 raise Unsupported(f"codegen for {op}")
             body = wrap(un[op])
